@@ -1,0 +1,230 @@
+"""Generate golden fixtures by running the REFERENCE package (read-only at
+/root/reference/pkg/src) in the build container.
+
+The GPU box has no /root/reference, so the outputs are committed as small
+``.npz`` files next to this script; tests and smoke() read only the .npz.
+
+    python tests/golden/make_golden.py            # rewrites tests/golden/*.npz
+
+Cases mirror the reference's own tests (pkg/tests/conftest.py make_codebook_pair,
+test_pq_core.py:129-197, test_attention.py:42-253, test_acceptance.py:41-72,
+test_kv_cache.py:51-212, test_fileio.py) at sizes that keep each file small.
+"""
+
+from __future__ import annotations
+
+import io
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import pqkv  # noqa: F401
+    from pqkv import attention, fileio, harness, kv_cache, pq_core
+    return pq_core, attention, kv_cache, fileio, harness
+
+
+def codebook_pair(pq_core, cfg, rng, spread=1.0):
+    """Same draw order as the reference fixture make_codebook_pair (conftest.py:12-22)."""
+    shape = (cfg.M, cfg.ksub, cfg.dsub)
+    ck = (spread * rng.standard_normal(shape)).astype(np.float32)
+    cv = (spread * rng.standard_normal(shape)).astype(np.float32)
+    return (pq_core.Codebook(config=cfg, centroids=ck, kind="key"),
+            pq_core.Codebook(config=cfg, centroids=cv, kind="value"))
+
+
+def make_encode(pq_core, harness):
+    out = {}
+    rng = np.random.default_rng(1234)
+    geoms = [(8, 4, 2), (32, 8, 4), (128, 64, 8), (128, 8, 4), (16, 2, 3),
+             (64, 4, 5), (128, 32, 12), (128, 64, 4)]
+    for gi, (d, M, nbits) in enumerate(geoms):
+        cfg = pq_core.PQConfig(d=d, M=M, nbits=nbits)
+        ck, _ = codebook_pair(pq_core, cfg, rng)
+        n = 256 if nbits < 12 else 64
+        X = rng.standard_normal((n, d)).astype(np.float32) * np.float32(1.5)
+        codes = pq_core.assign_codes(X, ck).codes
+        out[f"g{gi}_geom"] = np.array([d, M, nbits])
+        out[f"g{gi}_cents"] = ck.centroids
+        out[f"g{gi}_X"] = X
+        out[f"g{gi}_codes"] = codes
+
+    # exact ties: integer centroids, vectors on midpoints -> lowest index wins
+    cfg = pq_core.PQConfig(d=8, M=4, nbits=3)
+    cents = rng.integers(-4, 5, size=(4, 8, 2)).astype(np.float32) * 2
+    cb = pq_core.Codebook(config=cfg, centroids=cents, kind="key")
+    rows = []
+    for _ in range(200):
+        x = np.empty(8, np.float32)
+        for i in range(4):
+            a, b = rng.choice(8, 2, replace=False)
+            x[2 * i:2 * i + 2] = (cents[i, a] + cents[i, b]) / 2
+        rows.append(x)
+    X = np.stack(rows)
+    out["tie_cents"] = cents
+    out["tie_X"] = X
+    out["tie_codes"] = pq_core.assign_codes(X, cb).codes
+
+    # trained m64b8 codebook on outlier-channel synthetic keys (harness.py:209-212)
+    cfg = pq_core.PQConfig(d=128, M=64, nbits=8, kmeans_iters=6)
+    spec = harness.SynthSpec(n_tokens=2048, d=128, seed=0, outlier_channels=[7, 63])
+    K, V = harness.synth_kv(spec)
+    cbk = pq_core.train_codebooks(K, cfg, kind="key")
+    cbv = pq_core.train_codebooks(V, cfg, kind="value")
+    spec2 = harness.SynthSpec(n_tokens=1024, d=128, seed=5, outlier_channels=[7, 63],
+                              outlier_rate=0.001)
+    K2, V2 = harness.synth_kv(spec2)
+    out["trained_cents_k"] = cbk.centroids
+    out["trained_cents_v"] = cbv.centroids
+    out["trained_X_k"] = K2
+    out["trained_X_v"] = V2
+    out["trained_codes_k"] = pq_core.assign_codes(K2, cbk).codes
+    out["trained_codes_v"] = pq_core.assign_codes(V2, cbv).codes
+    np.savez_compressed(os.path.join(OUT, "encode.npz"), **out)
+
+
+def make_attention(pq_core, attention, kv_cache):
+    out = {}
+    rng = np.random.default_rng(42)
+    cases = [
+        # d, M, nbits, R, R_f, n_prefill, steps, block_size
+        (128, 64, 8, 0, 1, 300, 3, 1024),
+        (128, 64, 8, 16, 16, 300, 3, 1024),
+        (128, 64, 8, 32, 32, 257, 3, 1024),
+        (128, 64, 8, 32, 32, 2100, 2, 8192),   # n > 4*ksub -> centroid_accumulate
+        (128, 64, 8, 0, 1, 1300, 2, 1024),     # two blocks, gather
+        (8, 4, 2, 0, 1, 64, 4, 1024),
+        (8, 4, 2, 16, 16, 40, 4, 1024),
+        (128, 8, 4, 16, 16, 200, 3, 1024),
+        (32, 8, 8, 4, 4, 100, 3, 16),          # many tiny blocks
+        (128, 64, 8, 32, 32, 0, 3, 1024),      # empty cache start
+    ]
+    for ci, (d, M, nbits, R, R_f, npre, steps, bs) in enumerate(cases):
+        cfg = pq_core.PQConfig(d=d, M=M, nbits=nbits)
+        ck, cv = codebook_pair(pq_core, cfg, np.random.default_rng(100 + ci))
+        n = npre + steps
+        K = rng.standard_normal((n, d)).astype(np.float32)
+        V = rng.standard_normal((n, d)).astype(np.float32)
+        cache = kv_cache.LayerKVCache(ck, cv, recent_capacity=R, flush_threshold=R_f,
+                                      worker="sync")
+        if npre:
+            cache.prefill_ingest(K[:npre], V[:npre])
+        qs, outs, nqs, lut0 = [], [], [], None
+        snaps = []
+        for s in range(steps):
+            q = rng.standard_normal(d)
+            snap = cache.snapshot()
+            nqs.append(snap.n_q)
+            if s == 0:
+                snaps = [snap.codes_K.codes.copy(), snap.codes_V.codes.copy(),
+                         snap.recent_K.copy(), snap.recent_V.copy()]
+                lut0 = attention.build_key_lut(q, ck).table
+                if snap.n_q:
+                    qp = attention.quantized_partial(
+                        attention.build_key_lut(q, ck), snap.codes_K, snap.codes_V, cv)
+                    out[f"c{ci}_qp"] = np.concatenate([[qp.m, qp.l], qp.acc])
+            o = attention.decode_step(q, K[npre + s], V[npre + s], cache, ck, cv,
+                                      block_size=bs)
+            qs.append(q)
+            outs.append(o)
+        fin = cache.snapshot()
+        out[f"c{ci}_params"] = np.array([d, M, nbits, R, R_f, npre, steps, bs])
+        out[f"c{ci}_cents_k"] = ck.centroids
+        out[f"c{ci}_cents_v"] = cv.centroids
+        out[f"c{ci}_steps_k"] = K[npre:]
+        out[f"c{ci}_steps_v"] = V[npre:]
+        out[f"c{ci}_q"] = np.stack(qs)
+        out[f"c{ci}_out"] = np.stack(outs)
+        out[f"c{ci}_nq"] = np.array(nqs)
+        out[f"c{ci}_lut0"] = lut0
+        out[f"c{ci}_snap0_codes_k"], out[f"c{ci}_snap0_codes_v"] = snaps[0], snaps[1]
+        out[f"c{ci}_snap0_recent_k"], out[f"c{ci}_snap0_recent_v"] = snaps[2], snaps[3]
+        out[f"c{ci}_final_codes_k"] = fin.codes_K.codes
+        out[f"c{ci}_final_codes_v"] = fin.codes_V.codes
+        out[f"c{ci}_final_recent_k"] = fin.recent_K
+    out["ncases"] = np.array(len(cases))
+
+    # merge / dense / finalize pins (test_attention.py:172-236 style)
+    q = rng.standard_normal(8)
+    Kd = rng.standard_normal((30, 8))
+    Vd = rng.standard_normal((30, 8))
+    a = attention.dense_partial(q, Kd[:13], Vd[:13])
+    b = attention.dense_partial(q, Kd[13:], Vd[13:])
+    mg = attention.merge_partials(a, b)
+    out["merge_q"], out["merge_K"], out["merge_V"] = q, Kd, Vd
+    out["merge_a"] = np.concatenate([[a.m, a.l], a.acc])
+    out["merge_b"] = np.concatenate([[b.m, b.l], b.acc])
+    out["merge_ab"] = np.concatenate([[mg.m, mg.l], mg.acc])
+    out["merge_final"] = attention.finalize(mg)
+    np.savez_compressed(os.path.join(OUT, "attention.npz"), **out)
+
+
+def make_fileio(pq_core, fileio):
+    import tempfile
+    out = {}
+    rng = np.random.default_rng(7)
+    for gi, (d, M, nbits, kind) in enumerate([(128, 64, 8, "key"), (8, 4, 2, "value"),
+                                              (32, 8, 10, "key")]):
+        cfg = pq_core.PQConfig(d=d, M=M, nbits=nbits)
+        cents = rng.standard_normal((M, cfg.ksub, cfg.dsub)).astype(np.float32)
+        cb = pq_core.Codebook(config=cfg, centroids=cents, kind=kind)
+        with tempfile.TemporaryDirectory() as td:
+            p = os.path.join(td, "cb.pqkv")
+            fileio.write_codebook(p, cb)
+            raw = open(p, "rb").read()
+            back = fileio.read_codebook(p)
+        out[f"f{gi}_raw"] = np.frombuffer(raw, np.uint8)
+        out[f"f{gi}_geom"] = np.array([d, M, nbits, 0 if kind == "key" else 1])
+        out[f"f{gi}_cents"] = back.centroids
+    np.savez_compressed(os.path.join(OUT, "fileio.npz"), **out)
+
+
+def make_cache(pq_core, kv_cache):
+    """Random append/flush_recent sequences on the sync cache (test_kv_cache.py:102-212)."""
+    out = {}
+    rng = np.random.default_rng(99)
+    cfg = pq_core.PQConfig(d=8, M=4, nbits=2)
+    ck, cv = codebook_pair(pq_core, cfg, np.random.default_rng(0))
+    out["cents_k"], out["cents_v"] = ck.centroids, cv.centroids
+    for tr in range(12):
+        R = int(rng.choice([0, 4, 16]))
+        R_f = int(rng.choice([1, 4, 16]))
+        n = int(rng.integers(10, 50))
+        npre = int(rng.integers(0, 20))
+        K = rng.standard_normal((npre + n, 8)).astype(np.float32)
+        V = rng.standard_normal((npre + n, 8)).astype(np.float32)
+        cache = kv_cache.LayerKVCache(ck, cv, recent_capacity=R, flush_threshold=R_f)
+        if npre:
+            cache.prefill_ingest(K[:npre], V[:npre])
+        for t in range(npre, npre + n):
+            cache.append_decode(K[t], V[t])
+        s = cache.snapshot()
+        out[f"t{tr}_params"] = np.array([R, R_f, npre, n])
+        out[f"t{tr}_K"], out[f"t{tr}_V"] = K, V
+        out[f"t{tr}_codes_k"], out[f"t{tr}_codes_v"] = s.codes_K.codes, s.codes_V.codes
+        out[f"t{tr}_recent_k"], out[f"t{tr}_recent_v"] = s.recent_K, s.recent_V
+        out[f"t{tr}_nq"] = np.array([s.n_q, s.n_total])
+    out["ntrials"] = np.array(12)
+    np.savez_compressed(os.path.join(OUT, "cache.npz"), **out)
+
+
+def main():
+    pq_core, attention, kv_cache, fileio, harness = _ref()
+    make_encode(pq_core, harness)
+    make_attention(pq_core, attention, kv_cache)
+    make_fileio(pq_core, fileio)
+    make_cache(pq_core, kv_cache)
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
