@@ -1,0 +1,409 @@
+"""Benchmark: PQ decode attention tokens/s at 32K context (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config llama2-32k|llama3-gqa-32k|llama2-4k-1layer]
+
+A step is one decode step of the whole model's attention over its PQ cache:
+for each of the 32 layers, key LUTs for every query head, the fused
+quantized-span kernel over all heads, and the dense recent-window merge +
+finalize -- 96 launches captured in one CUDA graph.  Inputs are synthetic
+(seeded uniform uint8 codes, N(0,1) codebooks / queries / recent rows) of the
+named shape and are resident in HBM; the code stream (4.29 GB per step for
+config 2) exceeds L2, so no flush is needed between steps.
+
+Multi-GPU: one process per GPU (torchrun); each rank decodes its own
+sequences (batch sharding, no data-path collective) -> weak scaling; the
+reported value is the whole-job tokens/s, timed as the max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+C restatement in oracle/, all host cores) on the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (layers, B per rank, Hq, Hkv, quantized ctx, recent rows)
+    "llama2-32k": (32, 1, 32, 32, 32768, 31),
+    "llama3-gqa-32k": (32, 16, 32, 8, 32768, 31),
+    "llama2-4k-1layer": (1, 1, 32, 32, 4096, 31),
+}
+D, M, NBITS = 128, 64, 8
+METRIC = "decode attention tokens/s at 32K ctx (HBM GB/s of roofline); KV encode tok/s"
+THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg_name):
+    """dram read+write bytes per launch of the decode kernel from a committed
+    `ncu --set full` capture summary (profiles/*decode_ncu.json), else None."""
+    pdir = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(pdir):
+        for f in sorted(os.listdir(pdir)):
+            if f.endswith("decode_ncu.json"):
+                try:
+                    with open(os.path.join(pdir, f)) as fh:
+                        j = json.load(fh)
+                    if j.get("config") == cfg_name:
+                        best = j.get("dram_bytes_per_launch")
+                except Exception:
+                    pass
+    return best
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 4:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), float(parts[2]),
+                                         int(parts[3], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [s for s in self.samples if not (s[3] & 0x1)] or self.samples
+        reasons = set()
+        for s in busy:
+            for bit, name in THROTTLE_BITS.items():
+                if s[3] & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy),
+                "sm_max_mhz": max(s[1] for s in busy),
+                "power_w_max": max(s[2] for s in busy),
+                "samples": len(busy), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+
+def cpu_decode_rate(cfg_name, threads, budget_s, layers_per_rep=1, seed=0):
+    """Time the C restatement of the reference decode (oracle/, fp64, numba-loop
+    equivalent, block_size 8192 as harness.py:161) on `threads` host threads over
+    a bounded sample of the workload; returns (tokens/s, sample description)."""
+    from oracle import pqkv_oracle as O
+    lib = O.c_library()
+    if lib is None:
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+        O._clib = None
+        lib = O.c_library()
+    L, B, Hq, Hkv, n, R = CONFIGS[cfg_name]
+    G = Hq // Hkv
+    heads = B * Hq
+    rng = np.random.default_rng(seed)
+    ck = rng.integers(0, 256, (B * Hkv, n, M), dtype=np.uint8)
+    cv = rng.integers(0, 256, (B * Hkv, n, M), dtype=np.uint8)
+    # GQA: q-head h reads KV head h // G; the C loop takes per-head strides, so
+    # replicate pointers by laying q-heads out in KV-head-major order
+    ck_h = ck if G == 1 else np.repeat(ck, G, axis=0)
+    cv_h = cv if G == 1 else np.repeat(cv, G, axis=0)
+    q = rng.standard_normal((heads, D))
+    kn = rng.standard_normal((heads, D)).astype(np.float32)
+    vn = rng.standard_normal((heads, D)).astype(np.float32)
+    rk = rng.standard_normal((heads, R, D)).astype(np.float32)
+    rv = rng.standard_normal((heads, R, D)).astype(np.float32)
+    cents_k = rng.standard_normal((M, 256, 2)).astype(np.float32)
+    cents_v = rng.standard_normal((M, 256, 2)).astype(np.float32)
+    out = np.empty((heads, D))
+    P = ctypes.c_void_p
+
+    def one_layer():
+        rc = lib.oracle_decode_heads_mt(
+            q.ctypes.data_as(P), kn.ctypes.data_as(P), vn.ctypes.data_as(P),
+            ck_h.ctypes.data_as(P), cv_h.ctypes.data_as(P), n, n, rk.ctypes.data_as(P),
+            rv.ctypes.data_as(P), R, cents_k.ctypes.data_as(P), cents_v.ctypes.data_as(P),
+            M, NBITS, 2, 1.0 / np.sqrt(D), 8192, out.ctypes.data_as(P), heads, threads)
+        assert rc == 0
+
+    one_layer()  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        for _ in range(layers_per_rep):
+            one_layer()
+        times.append((time.perf_counter() - t0) / layers_per_rep)
+        if time.perf_counter() - t_start > budget_s and len(times) >= 3:
+            break
+    per_layer = statistics.median(times)
+    tok_s = B / (per_layer * L)
+    sample = (f"{len(times)} reps x {layers_per_rep} layer(s) of {heads} heads x {n} ctx "
+              f"(median {per_layer * 1e3:.1f} ms/layer, scaled x{L} layers)")
+    return tok_s, sample
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    per_step = []
+    sample = ""
+    for _ in range(args.warmup):
+        cpu_decode_rate(args.config, threads, 0.0)
+    for _ in range(args.steps):
+        v, sample = cpu_decode_rate(args.config, threads, 0.0)
+        per_step.append(v)
+    value = statistics.median(per_step)
+    L, B, Hq, Hkv, n, R = CONFIGS[args.config]
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * B / value, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args.config, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(name, n_gpus):
+    L, B, Hq, Hkv, n, R = CONFIGS[name]
+    return {"workload": name, "layers": L, "batch_per_gpu": B, "global_batch": B * n_gpus,
+            "q_heads": Hq, "kv_heads": Hkv, "head_dim": D, "ctx_quantized": n,
+            "recent_rows": R, "pq": "m64b8 (M=64, nbits=8, dsub=2)",
+            "code_bytes_per_step_per_gpu": 2 * L * B * Hkv * n * M,
+            "parallelism": f"batch-sharded x{n_gpus} (no collective)",
+            "l2": "inputs > L2 (code stream per step >> 126 MB); no flush needed"}
+
+
+# ------------------------------------------------------------------ ours --
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2504_03661_b200 import build as B_
+    B_.build()
+    from paper_2504_03661_b200 import kernels as K
+    from paper_2504_03661_b200 import _native as N
+    from paper_2504_03661_b200.engine import PQDecoder, random_codes
+    from paper_2504_03661_b200.pq_core import PQConfig
+
+    L, B, Hq, Hkv, n, R = CONFIGS[args.config]
+    cfg = PQConfig(D, M, NBITS)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    codes_k = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
+    codes_v = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
+    cbk = [torch.randn((M, 256, 2), generator=g, device=dev) for _ in range(L)]
+    cbv = [K.value_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS)
+           for _ in range(L)]
+    rk = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
+    rv = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
+    n_q = torch.full((B,), n, dtype=torch.int32, device=dev)
+    n_r = torch.full((B,), R, dtype=torch.int32, device=dev)
+    q = torch.randn((L, B, Hq, D), generator=g, device=dev)
+    kc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
+    vc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
+    out = torch.empty((L, B, Hq, D), device=dev)
+    dec = PQDecoder(B, Hq, Hkv, cfg, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for l in range(L):
+            dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv[l], rk[l], rv[l], n_r, kc[l],
+                vc[l], out=out[l])
+
+    # capture one decode step (3 launches per layer) in a CUDA graph
+    with torch.cuda.stream(stream):
+        step()
+        step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    launches_per_step = 3 * L
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed region ------------------------------------
+    for _ in range(args.warmup):
+        graph.replay()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            ev1.record(stream)
+        barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = world * B * 1e3 / ms
+    clocks = clk.summary()
+
+    # ---- dominant kernel: per-launch CUDA-event time on its own stream ------
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(L)]
+    ktimes = []
+    with torch.cuda.stream(stream):
+        for rep in range(max(2, min(args.steps, 5))):
+            for l in range(L):
+                K.build_lut(q[l].view(B * Hq, D), cbk[l], NBITS, 1 / D ** 0.5, out=dec.ws.lut,
+                            stream=stream)
+                kev[l][0].record(stream)
+                K.decode_partials(dec.ws, Hkv, codes_k[l], codes_v[l], n_q, cbv[l],
+                                  stream=stream)
+                kev[l][1].record(stream)
+            stream.synchronize()
+            if rep > 0:
+                ktimes += [a.elapsed_time(b) for a, b in kev]
+    k_ms = statistics.mean(ktimes)
+    bytes_per_launch = 2 * B * Hkv * n * M
+    hbm_peak, peak_kind = peaks()
+    achieved = bytes_per_launch / (k_ms * 1e-3) / 1e9
+    share = k_ms * L / ms
+
+    # ---- end to end through the public API with host buffers --------------
+    q_h = torch.randn((L, B, Hq, D)).pin_memory()
+    k_h = torch.randn((L, B, Hkv, D)).pin_memory()
+    v_h = torch.randn((L, B, Hkv, D)).pin_memory()
+    o_h = torch.empty((L, B, Hq, D)).pin_memory()
+    h2d = (q_h.numel() + k_h.numel() + v_h.numel()) * 4
+    d2h = o_h.numel() * 4
+
+    def e2e_step():
+        q.copy_(q_h, non_blocking=True)
+        kc.copy_(k_h, non_blocking=True)
+        vc.copy_(v_h, non_blocking=True)
+        graph.replay()
+        o_h.copy_(out, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            e2e_step()
+    barrier()
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+            ev1.record(stream)
+            ev1.synchronize()  # the host reads each step's result
+        e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    barrier()
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 codes / f32 accumulate", "data": "synthetic (seeded uniform codes, "
+            "N(0,1) codebooks, queries and recent rows)",
+            "config": config_dict(args.config, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(args.config),
+                         "kernel": "decode_partials_m64b8",
+                         "kernel_ms_per_launch": k_ms,
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "kernel_share_of_step": share},
+            "e2e": {"value": world * B * 1e3 / e2e_ms, "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_2504_03661_b200.engine.PQDecoder (graph-replayed step)"},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "code_stream_gbs_step": 2 * L * B * Hkv * n * M / (ms * 1e-3) / 1e9}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample = cpu_decode_rate(args.config, 1, args.cpu_budget)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": 1, "kind": "port",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama2-32k", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

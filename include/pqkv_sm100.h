@@ -1,0 +1,141 @@
+/*
+ * pqkv_sm100.h -- C ABI of the B200 (sm_100a) product-quantized KV-cache hot
+ * path: KV encode, key lookup tables, quantized-span decode attention and the
+ * log-sum-exp merge of softmax partials.
+ *
+ * Every entry point replaces a function of the reference package `pqkv`
+ * (paths relative to the reference's pkg/src/pqkv/); the citation is on each
+ * declaration.  Conventions:
+ *   - all pointers are DEVICE pointers unless stated otherwise; sizes are in
+ *     elements; no entry point allocates, synchronises or keeps global
+ *     mutable state beyond a per-thread error string;
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*; NULL means
+ *     the legacy default stream) and is asynchronous;
+ *   - the return value is 0 on success, PQKV_EINVAL for a bad argument
+ *     (the reference raises ValueError) and PQKV_ECUDA for a CUDA launch
+ *     error; pqkv_last_error() returns the calling thread's last message.
+ *
+ * Geometry: d = M * dsub, ksub = 2^nbits.  Codes are token-major rows of M
+ * cells (uint8 when nbits <= 8 else uint16), exactly the reference's
+ * CodesMatrix layout (pq_core.py:114-145).  Codebooks are (M, ksub, dsub)
+ * float32, subspace-major (pq_core.py:86-111).
+ */
+#ifndef PQKV_SM100_H
+#define PQKV_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQKV_OK 0
+#define PQKV_EINVAL 1
+#define PQKV_ECUDA 2
+
+#define PQKV_DTYPE_F32 0
+#define PQKV_DTYPE_BF16 1
+#define PQKV_DTYPE_F16 2
+
+/* Floats per softmax-partial record: (m, l, 2 pad, acc[d]) -> d + 4.
+ * Mirrors SoftmaxPartial (attention.py:46-53); empty = (-inf, 0, 0). */
+#define PQKV_PARTIAL_HEADER 4
+
+int pqkv_version(void);
+const char *pqkv_last_error(void);
+
+/* Nearest-centroid encoder, bit-exact with assign_codes (pq_core.py:269-287
+ * on top of _squared_distances :158-168): fp64 d2 = (|x|^2 - 2 x.c) + |c|^2
+ * with numpy's pairwise norms and a sequential x.c, clamped at 0, lowest
+ * index on ties.  x: n rows of d values (row stride ld_x elements, dtype
+ * PQKV_DTYPE_*); codes: n rows of M cells, row stride ld_codes cells. */
+int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
+                const float *centroids, int M, int nbits, void *codes,
+                int64_t ld_codes, void *stream);
+
+/* reconstruct (pq_core.py:290-304): out[t, i*dsub + j] = C[i, codes[t, i], j].
+ * Test/diagnostic helper: the attention path never dequantizes. */
+int pqkv_reconstruct(const void *codes, int64_t n, int64_t ld_codes,
+                     const float *centroids, int d, int M, int nbits,
+                     float *out, void *stream);
+
+/* build_key_lut (attention.py:70-83) for n_heads queries at once:
+ * lut[h, c, i] = scale * <q[h, i*dsub:(i+1)*dsub], C_K[i, c]>, float32,
+ * stored centroid-major ([ksub][M] per head) -- the decode kernel's
+ * shared-memory layout, so the kernel copies it without a transpose. */
+int pqkv_build_lut(const float *q, int64_t n_heads, int d, const float *cb_k,
+                   int M, int nbits, float scale, float *lut, void *stream);
+
+/* One-time re-layout of a value codebook for the m64b8 fast path
+ * (d=128, M=64, nbits=8): out is [2][256][32] float2, i.e. subspace half,
+ * centroid, subspace-within-half.  65536 float32.  Other geometries use the
+ * plain (M, ksub, dsub) codebook and need no call. */
+int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits,
+                                float *out, void *stream);
+
+/* Number of persistent CTAs pqkv_decode_partials uses on the current device
+ * (one per SM for the fast path); needed to size the partials buffer. */
+int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas);
+
+/* Floats needed for the partials workspace: (num_ctas + B*Hq) * (d + 4). */
+int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d);
+
+/* Quantized-span softmax partials: the fused LUT-score + online softmax +
+ * value accumulation of quantized_partial (attention.py:114-166), i.e.
+ * score_codes (_kernels.py:27-34) and the value aggregation
+ * (_kernels.py:37-43 + attention.py:103-111 / :155-157), for every
+ * (batch b, query head hq) over tokens [0, n_q[b]) of KV head
+ * hkv = hq / (Hq / Hkv).  The token space of all heads is split evenly over
+ * num_ctas persistent CTAs; each (CTA, head) overlap emits one partial.
+ *   lut      [B*Hq][ksub][M] float32 from pqkv_build_lut
+ *   codes_k/codes_v  [B][Hkv][ld_tok][M] cells
+ *   n_q      [B] int32 (device): quantized tokens per sequence
+ *   cb_v     fast path: pqkv_prepare_value_codebook output; else (M,ksub,dsub)
+ *   partials pqkv_partials_floats(num_ctas, B, Hq, d) floats */
+int pqkv_decode_partials(const float *lut, int B, int Hq, int Hkv,
+                         const void *codes_k, const void *codes_v,
+                         int64_t ld_tok, const int32_t *n_q, const float *cb_v,
+                         int d, int M, int nbits, int num_ctas,
+                         float *partials, void *stream);
+
+/* Finish one decode step for every (b, hq): merge that head's quantized
+ * partials in a fixed order (merge_partials, attention.py:193-204), add the
+ * dense partial over the full-precision recent rows plus the current token
+ * (dense_partial :169-190, decode_step :264-267) and finalize (:207-211).
+ *   q            [B*Hq][d] float32 (scores use `scale`)
+ *   recent_k/v   [B][Hkv][ld_recent][d] float32, rows [0, n_recent[b])
+ *   n_recent     [B] int32 (device) or NULL (no recent rows)
+ *   k_cur/v_cur  [B][Hkv][d] float32 or NULL (no current token)
+ *   out          [B*Hq][d] float32 (may be NULL)
+ *   lse          [B*Hq] float32 m + log(l) (may be NULL)
+ *   merged       [B*Hq][d+4] merged, un-normalised partial (may be NULL) --
+ *                the record exchanged between ranks for a sequence split.
+ * A head whose merged partial is empty (l == 0) gets NaN outputs (the
+ * reference's finalize raises ValueError; the Python layer checks). */
+int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
+                       int Hkv, int d, const int32_t *n_q, const float *q,
+                       float scale, const float *recent_k,
+                       const float *recent_v, int64_t ld_recent,
+                       const int32_t *n_recent, const float *k_cur,
+                       const float *v_cur, float *out, float *lse,
+                       float *merged, void *stream);
+
+/* Merge n_parts partial records per head in index order (merge_partials,
+ * attention.py:193-204; the cross-GPU log-sum-exp merge of a sequence
+ * split) and optionally finalize.  parts: [n_parts][n_heads][d+4]. */
+int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_heads,
+                        int d, float *out, float *lse, float *merged,
+                        void *stream);
+
+/* Lower seam of the reference (_kernels.py:46-53, 56-65), float32:
+ *   scores[t] = sum_i lut[code[t,i], i]          (lut centroid-major [ksub][M])
+ *   h[i, c]  += p[t] for code[t, i] == c          (h is zeroed first) */
+int pqkv_score_codes(const float *lut, const void *codes, int64_t n, int M,
+                     int nbits, float *scores, void *stream);
+int pqkv_accumulate_mass(const void *codes, const float *p, int64_t n, int M,
+                         int nbits, float *h, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PQKV_SM100_H */

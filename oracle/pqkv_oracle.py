@@ -71,18 +71,17 @@ def subspace_distances(x_sub: np.ndarray, cents: np.ndarray) -> np.ndarray:
     """fp64 expanded-form squared distances, (n, ksub).
 
     Follows pq_core.py:158-168: d2 = (||x||^2 - 2 x.c) + ||c||^2, clamped at 0.
-    Inputs are float32 values promoted to float64, so every product is exact
-    and each dot product / norm is one rounding per sequential addition.
+    Inputs are float32 values promoted to float64, so every product is exact.
+    x.c is a sequential k-loop (OpenBLAS dgemm order, checked bit-for-bit for
+    k in 2..16); the norms use numpy's pairwise row sum.
     """
     X = np.asarray(x_sub, dtype=np.float64)
     C = np.asarray(cents, dtype=np.float64)
     n, dsub = X.shape
-    xx = np.zeros(n)
-    for j in range(dsub):                 # sequential, like a short numpy sum
-        xx = xx + X[:, j] * X[:, j]
-    cc = np.zeros(C.shape[0])
-    for j in range(dsub):
-        cc = cc + C[:, j] * C[:, j]
+    # row norms: numpy's pairwise axis-1 sum (8 accumulators from 8 terms up),
+    # exactly what pq_core.py:163,165 evaluates
+    xx = np.sum(X * X, axis=1)
+    cc = np.sum(C * C, axis=1)
     xc = np.zeros((n, C.shape[0]))
     for j in range(dsub):                 # dgemm k-loop: FMA chain == exact products + sequential adds
         xc = xc + X[:, j : j + 1] * C[None, :, j]

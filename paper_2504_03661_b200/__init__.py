@@ -1,0 +1,22 @@
+"""B200-native (sm_100a) product-quantized KV-cache attention.
+
+Drop-in for the hot path of the reference package ``pqkv`` (MILLION,
+arXiv 2504.03661): codebook load, KV encode and quantized-cache decode
+attention keep the reference's names and semantics; the arithmetic runs in
+hand-written CUDA kernels in ``_lib/libpqkv_sm100.so`` reached through the C
+ABI declared in ``include/pqkv_sm100.h``.  There is no CPU fallback.
+
+The batched serving path (many sequences, heads and layers per launch, GQA,
+sequence split across GPUs) is ``engine``.
+"""
+
+from .pq_core import (PQConfig, PRESETS, Codebook, CodesMatrix, assign_codes, reconstruct,
+                      bits_per_value)
+from .kv_cache import LayerKVCache, CacheSnapshot
+from .attention import (Lut, SoftmaxPartial, Counters, empty_partial, build_key_lut,
+                        score_tokens, quantized_partial, dense_partial, merge_partials, finalize,
+                        decode_step)
+from .fileio import (FormatError, read_codebook, write_codebook, read_cache_dump,
+                     write_cache_dump, dump_cache, read_tensor, write_tensor)
+
+__version__ = "0.1.0"

@@ -1,0 +1,309 @@
+"""Decode-step attention over a PQ KV cache -- drop-in for the reference ``attention``.
+
+Same names, arguments and errors as the reference's ``attention.py``
+(Lut :37-43, SoftmaxPartial :46-53, Counters :56-63, empty_partial :66-67,
+build_key_lut :70-83, score_tokens :86-100, quantized_partial :114-166,
+dense_partial :169-190, merge_partials :193-204, finalize :207-211,
+decode_step :214-287).  The arithmetic runs in libpqkv_sm100.so:
+
+* build_key_lut      -> pqkv_build_lut (float32 table, centroid-major)
+* score_tokens       -> pqkv_score_codes
+* quantized_partial  -> pqkv_decode_partials + pqkv_decode_finish: one fused
+                        kernel (LUT gather, online softmax, value accumulation
+                        in registers from the shared-memory codebook), split
+                        over every SM and merged in a fixed order;
+* dense_partial      -> pqkv_decode_finish (recent rows, no quantized span)
+* decode_step        -> LUT + fused partials + dense/current-token merge +
+                        finalize in three launches, then the cache append.
+
+The reference accumulates in float64 on the CPU; this path accumulates in
+float32 on the GPU.  Outputs agree within the tolerance stated in DESIGN.md
+(1e-5 relative on the oracle cases).  numpy inputs give numpy float64 results
+like the reference; CUDA tensors give CUDA tensors and never synchronise.
+``strategy`` is validated as in the reference; both values select the same
+kernel (the value path never materialises V), and
+``block_size`` only affects the reference's CPU blocking, so it is accepted
+and ignored (the GPU split is chosen per SM count).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_device
+
+__all__ = ["Lut", "SoftmaxPartial", "Counters", "empty_partial", "build_key_lut",
+           "score_tokens", "quantized_partial", "dense_partial", "merge_partials", "finalize",
+           "decode_step"]
+
+_STRATEGIES = ("auto", "gather", "centroid_accumulate")
+
+
+@dataclass
+class Lut:
+    """Scaled query-centroid dot products.  ``table`` is (M, 2^nbits) like the
+    reference; ``device_table`` is the centroid-major (2^nbits, M) float32 copy
+    the kernels read."""
+
+    table: object
+    nbits: int
+    device_table: torch.Tensor | None = None
+
+
+@dataclass
+class SoftmaxPartial:
+    """Online-softmax state (m, l, acc); empty = (-inf, 0, 0)."""
+
+    m: float
+    l: float
+    acc: object
+
+
+@dataclass
+class Counters:
+    lut_lookups: int = 0
+    adds: int = 0
+    code_bytes_read: int = 0
+    dense_bytes_read: int = 0
+
+
+def empty_partial(d: int) -> SoftmaxPartial:
+    return SoftmaxPartial(m=-np.inf, l=0.0, acc=np.zeros(d, dtype=np.float64))
+
+
+def _scale(d: int, scale):
+    return 1.0 / np.sqrt(d) if scale is None else float(scale)
+
+
+def build_key_lut(q_n, cb_K: Codebook, scale: float | None = None) -> Lut:
+    """table[i][c] = scale * dot(q_n subvector i, key centroid c of subspace i)."""
+    cfg = cb_K.config
+    host = not _is_tensor(q_n)
+    q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
+                  torch.float32)
+    if q.shape[0] != cfg.d:
+        raise ValueError(f"query width {q.shape[0]} != codebook d {cfg.d}")
+    cm = K.build_lut(q.view(1, -1), cb_K.device_centroids(q.device), cfg.nbits,
+                     _scale(cfg.d, scale))[0]
+    table = cm.t().double().cpu().numpy().copy() if host else cm.t()
+    return Lut(table=table, nbits=cfg.nbits, device_table=cm)
+
+
+def _device_table(lut: Lut) -> torch.Tensor:
+    if lut.device_table is not None:
+        return lut.device_table
+    t = lut.table
+    t = to_device(np.asarray(t, dtype=np.float32) if not _is_tensor(t) else t, torch.float32)
+    lut.device_table = t.t().contiguous()
+    return lut.device_table
+
+
+def score_tokens(lut: Lut, codes_K: CodesMatrix, counters: Counters | None = None):
+    """scores[t] = sum_i lut[i][codes[t][i]] (keys stay quantized)."""
+    tab = _device_table(lut)
+    ksub, M = tab.shape
+    c = codes_K.codes
+    n = codes_K.n_tokens
+    if n and ksub <= (255 if codes_K.cell_width == 1 else 65535):
+        from .pq_core import _max_code
+        if _max_code(c) >= ksub:
+            raise ValueError("code value out of range for lookup table")
+    if counters is not None:
+        counters.lut_lookups += n * codes_K.M
+        counters.adds += n * codes_K.M
+        counters.code_bytes_read += n * codes_K.M * codes_K.cell_width
+    host = not _is_tensor(c)
+    if n == 0:
+        return np.empty(0, dtype=np.float64) if host else torch.empty(0, device=tab.device)
+    s = K.score_codes(tab, codes_K.device_codes(tab.device), lut.nbits)
+    return s.double().cpu().numpy() if host else s
+
+
+def _n_tensor(n: int, device) -> torch.Tensor:
+    return torch.tensor([n], dtype=torch.int32, device=device)
+
+
+def _partial_from_record(rec: torch.Tensor, host: bool) -> SoftmaxPartial:
+    vals = rec.double().cpu().numpy()
+    m, l = float(vals[0]), float(vals[1])
+    acc = vals[4:].copy() if host else rec[4:].clone()
+    if l == 0.0:
+        m = -np.inf
+    return SoftmaxPartial(m=m, l=l, acc=acc)
+
+
+def quantized_partial(lut: Lut, codes_K: CodesMatrix, codes_V: CodesMatrix, cb_V: Codebook,
+                      strategy: str = "auto", counters: Counters | None = None,
+                      timings: dict | None = None) -> SoftmaxPartial:
+    """Softmax partial over the quantized token span (fused sm_100a kernel)."""
+    if codes_K.n_tokens != codes_V.n_tokens:
+        raise ValueError(f"key/value token counts differ: {codes_K.n_tokens} vs "
+                         f"{codes_V.n_tokens}")
+    cfg = cb_V.config
+    n = codes_K.n_tokens
+    host = not _is_tensor(codes_K.codes)
+    if n == 0:
+        return empty_partial(cfg.d)
+    if strategy not in _STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}")
+    tab = _device_table(lut)
+    dev = tab.device
+    t0 = time.perf_counter()
+    score_tokens(lut, codes_K, counters)  # range check + counters, as the reference
+    if counters is not None:
+        counters.code_bytes_read += n * cfg.M * codes_V.cell_width
+    ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
+    ws.lut.copy_(tab.view(1, *tab.shape))
+    ck = codes_K.device_codes(dev).contiguous().view(1, 1, n, cfg.M)
+    cv = codes_V.device_codes(dev).contiguous().view(1, 1, n, cfg.M)
+    nq = _n_tensor(n, dev)
+    K.decode_partials(ws, 1, ck, cv, nq, cb_V.device_value_layout(dev))
+    merged = torch.empty((1, cfg.d + 4), dtype=torch.float32, device=dev)
+    K.decode_finish(ws, 1, nq, None, 1.0, merged=merged)
+    part = _partial_from_record(merged[0], host)
+    if timings is not None:
+        timings["score"] = timings.get("score", 0.0) + (time.perf_counter() - t0)
+    return part
+
+
+def dense_partial(q_n, K_dense, V_dense, scale: float | None = None,
+                  counters: Counters | None = None) -> SoftmaxPartial:
+    """Standard softmax partial over full-precision rows."""
+    host = not _is_tensor(q_n)
+    q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
+                  torch.float32)
+    d = q.shape[0]
+    Kd = to_device(K_dense if _is_tensor(K_dense) else np.asarray(K_dense, dtype=np.float32),
+                   torch.float32, q.device).reshape(-1, d)
+    Vd = to_device(V_dense if _is_tensor(V_dense) else np.asarray(V_dense, dtype=np.float32),
+                   torch.float32, q.device)
+    if Vd.dim() == 1:
+        Vd = Vd.view(1, -1)
+    if Kd.shape[0] != Vd.shape[0]:
+        raise ValueError(f"K rows {Kd.shape[0]} != V rows {Vd.shape[0]}")
+    if Kd.shape[0] == 0:
+        raise ValueError("dense partial requires at least the current token")
+    r = Kd.shape[0]
+    if counters is not None:
+        counters.dense_bytes_read += 2 * r * d * 4
+    merged = torch.empty((1, d + 4), dtype=torch.float32, device=q.device)
+    K.decode_finish(None, 1, None, q.view(1, d), _scale(d, scale),
+                    recent_k=Kd.contiguous().view(1, 1, r, d),
+                    recent_v=Vd.contiguous().view(1, 1, r, d),
+                    n_recent=_n_tensor(r, q.device), merged=merged, B=1, Hq=1, d=d)
+    return _partial_from_record(merged[0], host)
+
+
+def merge_partials(a: SoftmaxPartial, b: SoftmaxPartial) -> SoftmaxPartial:
+    """Associative, commutative online-softmax merge (attention.py:193-204).
+
+    Device partials merge with pqkv_merge_partials; host partials (the
+    reference's own numpy types) use the same closed form."""
+    if tuple(a.acc.shape) != tuple(b.acc.shape):
+        raise ValueError("partial widths differ")
+    if _is_tensor(a.acc) or _is_tensor(b.acc):
+        dev = a.acc.device if _is_tensor(a.acc) else b.acc.device
+        d = a.acc.shape[0]
+        recs = torch.zeros((2, 1, d + 4), dtype=torch.float32, device=dev)
+        for k, p in enumerate((a, b)):
+            recs[k, 0, 0] = float(p.m) if p.l != 0.0 else 0.0
+            recs[k, 0, 1] = float(p.l)
+            recs[k, 0, 4:] = to_device(p.acc, torch.float32, dev)
+        out = torch.empty((1, d + 4), dtype=torch.float32, device=dev)
+        K.merge_partials(recs, merged=out)
+        return _partial_from_record(out[0], host=False)
+    if a.l == 0.0:
+        return SoftmaxPartial(m=b.m, l=b.l, acc=b.acc.copy())
+    if b.l == 0.0:
+        return SoftmaxPartial(m=a.m, l=a.l, acc=a.acc.copy())
+    m = max(a.m, b.m)
+    wa = np.exp(a.m - m)
+    wb = np.exp(b.m - m)
+    return SoftmaxPartial(m=m, l=a.l * wa + b.l * wb, acc=a.acc * wa + b.acc * wb)
+
+
+def finalize(p: SoftmaxPartial):
+    """Normalized attention output acc / l."""
+    if p.l <= 0.0:
+        raise ValueError("cannot finalize an empty softmax partial")
+    return p.acc / p.l
+
+
+def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
+                scale: float | None = None, strategy: str = "auto", block_size: int = 1024,
+                counters: Counters | None = None, timings: dict | None = None):
+    """One attention decode step against a LayerKVCache, then append (k_n, v_n).
+
+    The snapshot's quantized span is scored through the LUT by the fused
+    kernel; recent rows plus the current token form the dense partial; the
+    current token is never scored against a quantized copy of itself."""
+    cfg = cb_K.config
+    if strategy not in _STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}")
+    if block_size <= 0:
+        raise ValueError("block_size must be positive")
+    sc = _scale(cfg.d, scale)
+    host = not _is_tensor(q_n)
+    snap = cache.snapshot()
+    dev = getattr(cache, "device", None) or default_device()
+    q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
+                  torch.float32, dev)
+    if q.shape[0] != cfg.d:
+        raise ValueError(f"query width {q.shape[0]} != codebook d {cfg.d}")
+    kc = to_device(k_n if _is_tensor(k_n) else np.asarray(k_n, dtype=np.float32),
+                   torch.float32, dev).reshape(-1)
+    vc = to_device(v_n if _is_tensor(v_n) else np.asarray(v_n, dtype=np.float32),
+                   torch.float32, dev).reshape(-1)
+    if kc.shape[0] != cfg.d or vc.shape[0] != cfg.d:
+        raise ValueError(f"k_n/v_n width must be d={cfg.d}")
+
+    t0 = time.perf_counter()
+    n_q = snap.codes_K.n_tokens
+    ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
+    K.build_lut(q.view(1, -1), cb_K.device_centroids(dev), cfg.nbits, sc, out=ws.lut)
+    if timings is not None:
+        t1 = time.perf_counter()
+        timings["lut_build"] = timings.get("lut_build", 0.0) + (t1 - t0)
+        t0 = t1
+    nq_t = _n_tensor(n_q, dev)
+    if n_q:
+        ck = snap.codes_K.device_codes(dev).contiguous().view(1, 1, n_q, cfg.M)
+        cv = snap.codes_V.device_codes(dev).contiguous().view(1, 1, n_q, cfg.M)
+        K.decode_partials(ws, 1, ck, cv, nq_t, cb_V.device_value_layout(dev))
+    if counters is not None:
+        counters.lut_lookups += n_q * cfg.M
+        counters.adds += n_q * cfg.M
+        counters.code_bytes_read += 2 * n_q * cfg.M * cfg.cell_width
+    if timings is not None:
+        t1 = time.perf_counter()
+        timings["score"] = timings.get("score", 0.0) + (t1 - t0)
+        t0 = t1
+    rk, rv = snap.recent_K, snap.recent_V
+    r = int(rk.shape[0])
+    rkd = to_device(rk if _is_tensor(rk) else np.asarray(rk, dtype=np.float32), torch.float32,
+                    dev).contiguous().view(1, 1, r, cfg.d) if r else None
+    rvd = to_device(rv if _is_tensor(rv) else np.asarray(rv, dtype=np.float32), torch.float32,
+                    dev).contiguous().view(1, 1, r, cfg.d) if r else None
+    if counters is not None:
+        counters.dense_bytes_read += 2 * (r + 1) * cfg.d * 4
+    out = torch.empty((1, cfg.d), dtype=torch.float32, device=dev)
+    K.decode_finish(ws, 1, nq_t, q.view(1, -1), sc, recent_k=rkd, recent_v=rvd,
+                    n_recent=_n_tensor(r, dev) if r else None, k_cur=kc.view(1, 1, -1),
+                    v_cur=vc.view(1, 1, -1), out=out)
+    if timings is not None:
+        t1 = time.perf_counter()
+        timings["dense"] = timings.get("dense", 0.0) + (t1 - t0)
+        t0 = t1
+    flush_before = getattr(cache, "inline_flush_seconds", 0.0)
+    cache.append_decode(k_n, v_n)
+    if timings is not None:
+        t1 = time.perf_counter()
+        flush = getattr(cache, "inline_flush_seconds", 0.0) - flush_before
+        timings["flush_wait"] = timings.get("flush_wait", 0.0) + flush
+        timings["append"] = timings.get("append", 0.0) + (t1 - t0 - flush)
+    return out[0].double().cpu().numpy() if host else out[0]

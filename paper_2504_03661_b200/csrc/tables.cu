@@ -1,0 +1,174 @@
+// Small per-step / per-load kernels: key lookup tables, the value-codebook
+// re-layout for the fast path, reconstruct (test helper), the reference's
+// lower-seam kernels (_kernels.py), and the library's error/version plumbing.
+#include <cstdarg>
+
+#include "common.cuh"
+
+namespace pqkv {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    set_error(buf);
+    return code;
+}
+
+namespace {
+
+// build_key_lut (attention.py:70-83): lut[h][c][i] = scale * <q_i, C_K[i, c]>.
+// Block = 32 centroids x all M subspaces of one head, written contiguously
+// (centroid-major, the decode kernel's shared-memory image).
+__global__ void __launch_bounds__(256) build_lut_kernel(const float *__restrict__ q, int d,
+                                                        const float *__restrict__ cb_k, int M,
+                                                        int ksub, float scale,
+                                                        float *__restrict__ lut) {
+    extern __shared__ float q_s[];
+    const int h = blockIdx.y;
+    const int dsub = d / M;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) q_s[j] = q[(int64_t)h * d + j];
+    __syncthreads();
+    const int c0 = blockIdx.x * 32;
+    const int cn = min(32, ksub - c0);
+    float *out = lut + ((int64_t)h * ksub + c0) * M;
+    for (int idx = threadIdx.x; idx < cn * M; idx += blockDim.x) {
+        const int c = c0 + idx / M, i = idx % M;
+        const float *cr = cb_k + ((int64_t)i * ksub + c) * dsub;
+        const float *qi = q_s + i * dsub;
+        float acc = qi[0] * __ldg(cr);
+        for (int j = 1; j < dsub; ++j) acc = fmaf(qi[j], __ldg(cr + j), acc);
+        out[idx] = acc * scale;
+    }
+}
+
+// Value codebook -> [half][c][32] float2 for the m64b8 decode kernel.
+__global__ void prepare_cv_kernel(const float2 *__restrict__ cb_v, float2 *__restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over (i, c)
+    if (idx >= 64 * 256) return;
+    const int i = idx >> 8, c = idx & 255;
+    out[((i >> 5) * 256 + c) * 32 + (i & 31)] = cb_v[idx];
+}
+
+template <typename CT>
+__global__ void reconstruct_kernel(const CT *__restrict__ codes, int64_t n, int64_t ld_codes,
+                                   const float *__restrict__ cents, int d, int M, int ksub,
+                                   float *__restrict__ out) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * d) return;
+    const int64_t t = idx / d;
+    const int j = (int)(idx - t * d);
+    const int dsub = d / M, i = j / dsub, jj = j - i * dsub;
+    const int c = codes[t * ld_codes + i];
+    out[idx] = cents[((int64_t)i * ksub + c) * dsub + jj];
+}
+
+template <typename CT>
+__global__ void score_codes_kernel(const float *__restrict__ lut, const CT *__restrict__ codes,
+                                   int64_t n, int M, float *__restrict__ scores) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float s = 0.f;
+    for (int i = 0; i < M; ++i) s += __ldg(lut + (int64_t)codes[t * M + i] * M + i);
+    scores[t] = s;
+}
+
+template <typename CT>
+__global__ void accumulate_mass_kernel(const CT *__restrict__ codes, const float *__restrict__ p,
+                                       int64_t n, int M, int ksub, float *__restrict__ h) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * M) return;
+    const int64_t t = idx / M;
+    const int i = (int)(idx - t * M);
+    atomicAdd(h + (int64_t)i * ksub + codes[idx], p[t]);
+}
+
+}  // namespace
+}  // namespace pqkv
+
+using namespace pqkv;
+
+extern "C" int pqkv_version(void) { return 1; }
+
+extern "C" const char *pqkv_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int pqkv_build_lut(const float *q, int64_t n_heads, int d, const float *cb_k, int M,
+                              int nbits, float scale, float *lut, void *stream) {
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "pqkv_build_lut: bad geometry");
+    PQKV_CHECK_ARG(n_heads >= 0 && n_heads <= 65535, "pqkv_build_lut: n_heads out of range");
+    if (n_heads == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(q && cb_k && lut, "pqkv_build_lut: null pointer");
+    const int ksub = 1 << nbits;
+    dim3 grid((unsigned)((ksub + 31) / 32), (unsigned)n_heads);
+    build_lut_kernel<<<grid, 256, d * sizeof(float), as_stream(stream)>>>(q, d, cb_k, M, ksub,
+                                                                         scale, lut);
+    return launch_status("pqkv_build_lut");
+}
+
+extern "C" int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits, float *out,
+                                           void *stream) {
+    PQKV_CHECK_ARG(is_fast_geometry(d, M, nbits),
+                   "pqkv_prepare_value_codebook: only the m64b8 (d=128) geometry is re-laid out");
+    PQKV_CHECK_ARG(cb_v && out, "pqkv_prepare_value_codebook: null pointer");
+    prepare_cv_kernel<<<64, 256, 0, as_stream(stream)>>>((const float2 *)cb_v, (float2 *)out);
+    return launch_status("pqkv_prepare_value_codebook");
+}
+
+extern "C" int pqkv_reconstruct(const void *codes, int64_t n, int64_t ld_codes,
+                                const float *centroids, int d, int M, int nbits, float *out,
+                                void *stream) {
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "pqkv_reconstruct: bad geometry");
+    PQKV_CHECK_ARG(n >= 0 && ld_codes >= M, "pqkv_reconstruct: bad sizes");
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(codes && centroids && out, "pqkv_reconstruct: null pointer");
+    const int64_t total = n * d;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    if (nbits <= 8)
+        reconstruct_kernel<uint8_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            (const uint8_t *)codes, n, ld_codes, centroids, d, M, 1 << nbits, out);
+    else
+        reconstruct_kernel<uint16_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            (const uint16_t *)codes, n, ld_codes, centroids, d, M, 1 << nbits, out);
+    return launch_status("pqkv_reconstruct");
+}
+
+extern "C" int pqkv_score_codes(const float *lut, const void *codes, int64_t n, int M, int nbits,
+                                float *scores, void *stream) {
+    PQKV_CHECK_ARG(M > 0 && nbits >= 1 && nbits <= 16 && n >= 0, "pqkv_score_codes: bad args");
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(lut && codes && scores, "pqkv_score_codes: null pointer");
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (nbits <= 8)
+        score_codes_kernel<uint8_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            lut, (const uint8_t *)codes, n, M, scores);
+    else
+        score_codes_kernel<uint16_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            lut, (const uint16_t *)codes, n, M, scores);
+    return launch_status("pqkv_score_codes");
+}
+
+extern "C" int pqkv_accumulate_mass(const void *codes, const float *p, int64_t n, int M,
+                                    int nbits, float *h, void *stream) {
+    PQKV_CHECK_ARG(M > 0 && nbits >= 1 && nbits <= 16 && n >= 0, "pqkv_accumulate_mass: bad args");
+    PQKV_CHECK_ARG(h, "pqkv_accumulate_mass: null output");
+    const int ksub = 1 << nbits;
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(h, 0, sizeof(float) * (size_t)M * ksub, st);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "pqkv_accumulate_mass: %s", cudaGetErrorString(e));
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(codes && p, "pqkv_accumulate_mass: null pointer");
+    const unsigned blocks = (unsigned)((n * M + 255) / 256);
+    if (nbits <= 8)
+        accumulate_mass_kernel<uint8_t><<<blocks, 256, 0, st>>>((const uint8_t *)codes, p, n, M,
+                                                                 ksub, h);
+    else
+        accumulate_mass_kernel<uint16_t><<<blocks, 256, 0, st>>>((const uint16_t *)codes, p, n, M,
+                                                                  ksub, h);
+    return launch_status("pqkv_accumulate_mass");
+}

@@ -1,0 +1,180 @@
+"""Typed torch wrappers over the C ABI (include/pqkv_sm100.h).
+
+This is the B200 counterpart of the reference's lower seam
+(``_kernels.py:46-65``) plus the fused decode entry points.  Every function
+takes CUDA tensors, enqueues on the current (or given) stream and never
+synchronises.  Shapes are validated here, before the call, as the reference
+validates in Python (attention.py:75-76, 129-132; pq_core.py:275-278).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _native as N
+
+
+def _dev_check(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("expected CUDA tensors on the PQ KV-cache path")
+
+
+def _contig(t):
+    return t if t is None or t.is_contiguous() else t.contiguous()
+
+
+def code_dtype(nbits: int) -> torch.dtype:
+    return torch.uint8 if nbits <= 8 else torch.uint16
+
+
+def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tensor | None = None,
+           stream=None) -> torch.Tensor:
+    """Nearest-centroid codes of x (n, d) -> (n, M); bit-exact with assign_codes."""
+    _dev_check(x, centroids)
+    M, ksub, dsub = centroids.shape
+    d = M * dsub
+    if x.dim() != 2 or x.shape[1] != d:
+        raise ValueError(f"X must be (n, {d}), got {tuple(x.shape)}")
+    if x.dtype not in N.DTYPE_CODE:
+        x = x.float()
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    n = x.shape[0]
+    if out is None:
+        out = torch.empty((n, M), dtype=code_dtype(nbits), device=x.device)
+    if out.shape[0] != n or out.shape[1] != M or out.stride(1) != 1:
+        raise ValueError("codes output must be (n, M) with unit column stride")
+    cents = _contig(centroids.float())
+    N.call("pqkv_encode", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0), N.ptr(cents), M,
+           nbits, N.ptr(out), out.stride(0), N.stream_ptr(stream))
+    return out
+
+
+def reconstruct(codes: torch.Tensor, centroids: torch.Tensor, nbits: int, stream=None):
+    _dev_check(codes, centroids)
+    M, ksub, dsub = centroids.shape
+    n = codes.shape[0]
+    out = torch.empty((n, M * dsub), dtype=torch.float32, device=codes.device)
+    if codes.stride(1) != 1:
+        codes = codes.contiguous()
+    N.call("pqkv_reconstruct", N.ptr(codes), n, codes.stride(0), N.ptr(_contig(centroids)),
+           M * dsub, M, nbits, N.ptr(out), N.stream_ptr(stream))
+    return out
+
+
+def build_lut(q: torch.Tensor, cb_k: torch.Tensor, nbits: int, scale: float,
+              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """(H, d) queries -> (H, ksub, M) float32 centroid-major key tables."""
+    _dev_check(q, cb_k)
+    M, ksub, dsub = cb_k.shape
+    q = _contig(q.float().reshape(-1, M * dsub))
+    H = q.shape[0]
+    if out is None:
+        out = torch.empty((H, ksub, M), dtype=torch.float32, device=q.device)
+    N.call("pqkv_build_lut", N.ptr(q), H, M * dsub, N.ptr(_contig(cb_k)), M, nbits, float(scale),
+           N.ptr(out), N.stream_ptr(stream))
+    return out
+
+
+def is_fast_geometry(d: int, M: int, nbits: int) -> bool:
+    return d == 128 and M == 64 and nbits == 8
+
+
+def value_codebook_layout(cb_v: torch.Tensor, nbits: int, stream=None) -> torch.Tensor:
+    """The value codebook as the decode kernel reads it (re-laid out for m64b8)."""
+    M, ksub, dsub = cb_v.shape
+    cb_v = _contig(cb_v.float())
+    if not is_fast_geometry(M * dsub, M, nbits):
+        return cb_v
+    out = torch.empty(M * ksub * dsub, dtype=torch.float32, device=cb_v.device)
+    N.call("pqkv_prepare_value_codebook", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
+           N.stream_ptr(stream))
+    return out
+
+
+class DecodeWorkspace:
+    """Device scratch for one decode launch shape: LUTs and split partials."""
+
+    def __init__(self, B: int, Hq: int, d: int, M: int, nbits: int, device=None,
+                 num_ctas: int | None = None):
+        self.B, self.Hq, self.d, self.M, self.nbits = B, Hq, d, M, nbits
+        self.ksub = 1 << nbits
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        with torch.cuda.device(self.device):
+            self.num_ctas = num_ctas or N.decode_grid(d, M, nbits)
+        nf = N.partials_floats(self.num_ctas, B, Hq, d)
+        self.lut = torch.empty((B * Hq, self.ksub, M), dtype=torch.float32, device=self.device)
+        self.partials = torch.empty(nf, dtype=torch.float32, device=self.device)
+
+
+def decode_partials(ws: DecodeWorkspace, Hkv: int, codes_k, codes_v, n_q, cb_v_layout,
+                    stream=None) -> None:
+    """Fused LUT-score / online-softmax / value accumulation over the quantized span.
+
+    codes_k/codes_v: (B, Hkv, cap, M) cells; n_q: (B,) int32 device tensor.
+    Uses ws.lut (filled by build_lut) and writes ws.partials.
+    """
+    B, Hq = ws.B, ws.Hq
+    if codes_k.shape != codes_v.shape or codes_k.dim() != 4 or codes_k.shape[:2] != (B, Hkv):
+        raise ValueError("codes must be (B, Hkv, cap, M) and K/V shapes must agree")
+    if codes_k.shape[3] != ws.M or not codes_k.is_contiguous() or not codes_v.is_contiguous():
+        raise ValueError("codes must be contiguous (B, Hkv, cap, M)")
+    if Hq % Hkv:
+        raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
+    N.call("pqkv_decode_partials", N.ptr(ws.lut), B, Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v),
+           codes_k.shape[2], N.ptr(n_q), N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, ws.num_ctas,
+           N.ptr(ws.partials), N.stream_ptr(stream))
+
+
+def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, recent_k=None,
+                  recent_v=None, n_recent=None, k_cur=None, v_cur=None, out=None, lse=None,
+                  merged=None, B: int | None = None, Hq: int | None = None, d: int | None = None,
+                  stream=None) -> None:
+    """Merge split partials + dense window + current token, finalize.
+
+    recent_k/v: (B, Hkv, R, d) float32; n_recent: (B,) int32; k_cur/v_cur:
+    (B, Hkv, d) float32; out: (B*Hq, d); lse: (B*Hq,); merged: (B*Hq, d+4).
+    """
+    if ws is not None:
+        B, Hq, d = ws.B, ws.Hq, ws.d
+    ld_recent = 0
+    if recent_k is not None:
+        if recent_k.shape != recent_v.shape or recent_k.dim() != 4:
+            raise ValueError("recent_k/recent_v must both be (B, Hkv, R, d)")
+        ld_recent = recent_k.shape[2]
+    N.call("pqkv_decode_finish", N.ptr(ws.partials) if ws is not None else None,
+           ws.num_ctas if ws is not None else 0, B, Hq, Hkv, d, N.ptr(n_q), N.ptr(q),
+           float(scale), N.ptr(recent_k), N.ptr(recent_v), ld_recent, N.ptr(n_recent),
+           N.ptr(k_cur), N.ptr(v_cur), N.ptr(out), N.ptr(lse), N.ptr(merged),
+           N.stream_ptr(stream))
+
+
+def merge_partials(parts: torch.Tensor, out=None, lse=None, merged=None, stream=None) -> None:
+    """parts (n_parts, n_heads, d+4) -> merged in index order / finalized."""
+    n_parts, n_heads, w = parts.shape
+    N.call("pqkv_merge_partials", N.ptr(_contig(parts)), n_parts, n_heads, w - N.PARTIAL_HEADER,
+           N.ptr(out), N.ptr(lse), N.ptr(merged), N.stream_ptr(stream))
+
+
+def score_codes(lut_cm: torch.Tensor, codes: torch.Tensor, nbits: int, stream=None):
+    """scores[t] = sum_i lut[code[t,i], i] (lut centroid-major (ksub, M))."""
+    n, M = codes.shape
+    out = torch.empty(n, dtype=torch.float32, device=codes.device)
+    N.call("pqkv_score_codes", N.ptr(_contig(lut_cm)), N.ptr(_contig(codes)), n, M, nbits,
+           N.ptr(out), N.stream_ptr(stream))
+    return out
+
+
+def accumulate_mass(codes: torch.Tensor, p: torch.Tensor, nbits: int, stream=None):
+    n, M = codes.shape
+    h = torch.empty((M, 1 << nbits), dtype=torch.float32, device=codes.device)
+    N.call("pqkv_accumulate_mass", N.ptr(_contig(codes)), N.ptr(_contig(p.float())), n, M, nbits,
+           N.ptr(h), N.stream_ptr(stream))
+    return h
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,328 @@
+"""GPU-resident per-layer PQ code store + full-precision recent window.
+
+Drop-in for the reference ``kv_cache.py`` (CacheSnapshot :26-39,
+LayerKVCache :42-302): same constructor, methods, flush trigger
+(``len(recent) >= flush_threshold``, whole batches only, :108-110, :197-215),
+single publication point (``n_q`` bumps after a batch's codes are written,
+:228) and exactly-once snapshots (:269-290).
+
+B200 mapping of the reference's concurrency:
+
+* the code store and the recent rows live in HBM (torch tensors); flushes run
+  the sm_100a encoder (``pqkv_encode``) straight into the store;
+* ``worker="sync"`` enqueues the flush on the caller's stream inline;
+* ``worker="thread"`` (the reference's background flusher thread) runs the
+  encode on a low-priority side stream; the batch stays in the recent window
+  until the side stream's event has completed, and only then is ``n_q``
+  published -- a snapshot therefore still covers every token exactly once;
+* ``worker="manual"`` leaves flushing to ``flush_step`` / ``drain`` (the
+  deterministic test driver of the reference).
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_device
+
+__all__ = ["LayerKVCache", "CacheSnapshot"]
+
+
+@dataclass(frozen=True)
+class CacheSnapshot:
+    """Immutable view: published codes + recent rows, tokens [0, n_total) once."""
+
+    codes_K: CodesMatrix
+    codes_V: CodesMatrix
+    recent_K: object
+    recent_V: object
+    n_q: int
+    n_total: int
+
+
+class LayerKVCache:
+    """KV store for one layer/head with deferred batch quantization on the GPU."""
+
+    def __init__(self, cb_K: Codebook, cb_V: Codebook, recent_capacity: int = 32,
+                 flush_threshold: int = 32, worker: str = "sync", device=None):
+        if cb_K.config != cb_V.config:
+            raise ValueError("key/value codebooks must share one PQConfig")
+        if cb_K.kind != "key" or cb_V.kind != "value":
+            raise ValueError("expected a (key, value) codebook pair")
+        if recent_capacity < 0 or flush_threshold < 1:
+            raise ValueError("recent_capacity >= 0 and flush_threshold >= 1 required")
+        if worker not in ("sync", "thread", "manual"):
+            raise ValueError(f"unknown worker mode {worker!r}")
+        self.cb_K, self.cb_V = cb_K, cb_V
+        self.config = cb_K.config
+        self.recent_capacity = recent_capacity
+        self.flush_threshold = flush_threshold
+        self.worker = worker
+        self.device = torch.device(device) if device is not None else default_device()
+        cfg = self.config
+        cap = 1024
+        self._store_k = torch.zeros((cap, cfg.M), dtype=cfg.torch_code_dtype, device=self.device)
+        self._store_v = torch.zeros_like(self._store_k)
+        self._n_q = 0
+        rcap = max(64, 2 * (recent_capacity + flush_threshold))
+        self._rk = torch.zeros((rcap, cfg.d), dtype=torch.float32, device=self.device)
+        self._rv = torch.zeros_like(self._rk)
+        self._r0 = 0          # first live recent row in _rk/_rv
+        self._rlen = 0        # live recent rows (published + in-flight flushes)
+        self._n_total = 0
+        self._pending: list[tuple[torch.cuda.Event, int]] = []  # in-flight batches, FIFO
+        self._pending_rows = 0
+        self._lock = threading.RLock()
+        self.inline_flush_seconds = 0.0
+        self._side = (torch.cuda.Stream(device=self.device, priority=0)
+                      if worker == "thread" else None)
+        if self._side is not None:
+            lo, _hi = torch.cuda.Stream.priority_range()
+            self._side = torch.cuda.Stream(device=self.device, priority=lo)  # lowest priority
+
+    # -- state queries -----------------------------------------------------
+    @property
+    def n_total(self) -> int:
+        return self._n_total
+
+    @property
+    def n_q(self) -> int:
+        with self._lock:
+            self._publish_completed()
+            return self._n_q
+
+    def recent_len(self) -> int:
+        with self._lock:
+            self._publish_completed()
+            return self._rlen
+
+    def _flush_needed_locked(self) -> bool:
+        return self._rlen - self._pending_rows >= self.flush_threshold
+
+    # -- storage helpers ---------------------------------------------------
+    def _ensure_store(self, n_new: int) -> None:
+        cap = self._store_k.shape[0]
+        if n_new <= cap:
+            return
+        self._wait_pending()
+        cap = max(n_new, 2 * cap)
+        gk = torch.zeros((cap, self.config.M), dtype=self._store_k.dtype, device=self.device)
+        gv = torch.zeros_like(gk)
+        gk[: self._n_q] = self._store_k[: self._n_q]
+        gv[: self._n_q] = self._store_v[: self._n_q]
+        self._store_k, self._store_v = gk, gv
+
+    def _ensure_recent(self, extra: int) -> None:
+        cap = self._rk.shape[0]
+        if self._r0 + self._rlen + extra <= cap:
+            return
+        self._wait_pending()
+        need = self._rlen + extra
+        if need * 2 > cap:
+            cap = max(2 * need, cap)
+        nk = torch.zeros((cap, self.config.d), dtype=torch.float32, device=self.device)
+        nv = torch.zeros_like(nk)
+        nk[: self._rlen] = self._rk[self._r0: self._r0 + self._rlen]
+        nv[: self._rlen] = self._rv[self._r0: self._r0 + self._rlen]
+        self._rk, self._rv, self._r0 = nk, nv, 0
+
+    def _rows(self, x, name: str) -> torch.Tensor:
+        d = self.config.d
+        t = to_device(x if _is_tensor(x) else np.asarray(x, dtype=np.float32), torch.float32,
+                      self.device)
+        return t
+
+    def _check_row(self, x, name: str) -> torch.Tensor:
+        t = self._rows(x, name).reshape(-1)
+        if t.shape[0] != self.config.d:
+            raise ValueError(f"{name} width {t.shape[0]} != d {self.config.d}")
+        return t
+
+    # -- writes --------------------------------------------------------------
+    def prefill_ingest(self, K_rows, V_rows) -> None:
+        """Encode prompt tokens, keeping the trailing min(R, n) rows full precision."""
+        Kt = self._rows(K_rows, "K")
+        Vt = self._rows(V_rows, "V")
+        if Kt.shape != Vt.shape or Kt.dim() != 2 or Kt.shape[1] != self.config.d:
+            raise ValueError(f"bad prefill shapes K{tuple(Kt.shape)} V{tuple(Vt.shape)}")
+        with self._lock:
+            self._publish_completed()
+            if self._n_total != self._rlen + self._n_q:
+                raise RuntimeError("cache in inconsistent state")
+            n = Kt.shape[0]
+            keep = min(self.recent_capacity, n)
+            n_enc = n - keep
+            if n_enc > 0:
+                self._wait_pending()
+                self._ensure_store(self._n_q + n_enc)
+                K.encode(Kt[:n_enc].contiguous(), self.cb_K.device_centroids(self.device),
+                         self.config.nbits, out=self._store_k[self._n_q: self._n_q + n_enc])
+                K.encode(Vt[:n_enc].contiguous(), self.cb_V.device_centroids(self.device),
+                         self.config.nbits, out=self._store_v[self._n_q: self._n_q + n_enc])
+            if keep:
+                self._ensure_recent(keep)
+                a = self._r0 + self._rlen
+                self._rk[a: a + keep] = Kt[n_enc:]
+                self._rv[a: a + keep] = Vt[n_enc:]
+                self._rlen += keep
+            self._n_q += n_enc
+            self._n_total += n
+
+    def append_decode(self, k_n, v_n) -> None:
+        """Append the current token's full-precision KV pair; flush whole
+        batches once the recent window reaches the threshold."""
+        k = self._check_row(k_n, "k_n")
+        v = self._check_row(v_n, "v_n")
+        with self._lock:
+            self._publish_completed()
+            self._ensure_recent(1)
+            a = self._r0 + self._rlen
+            self._rk[a].copy_(k)
+            self._rv[a].copy_(v)
+            self._rlen += 1
+            self._n_total += 1
+            needed = self._flush_needed_locked()
+        if needed and self.worker == "sync":
+            t0 = time.perf_counter()
+            with self._lock:
+                while self._flush_needed_locked():
+                    self._flush_batch_locked(self.flush_threshold)
+            self.inline_flush_seconds += time.perf_counter() - t0
+        elif needed and self.worker == "thread":
+            with self._lock:
+                while self._flush_needed_locked():
+                    self._flush_batch_locked(self.flush_threshold, asynchronous=True)
+
+    def flush_recent(self, batch: int) -> None:
+        """Explicitly encode and publish the oldest `batch` recent entries."""
+        if batch < 0:
+            raise ValueError("batch must be >= 0")
+        with self._lock:
+            self._publish_completed()
+            if batch > self._rlen:
+                raise ValueError(f"batch {batch} exceeds recent length {self._rlen}")
+            if batch > 0:
+                self._wait_pending()
+                self._flush_batch_locked(batch)
+
+    def flush_step(self) -> bool:
+        """Run one scheduled flush if the trigger condition holds."""
+        with self._lock:
+            self._publish_completed()
+            if not self._flush_needed_locked():
+                return False
+            self._flush_batch_locked(self.flush_threshold)
+            return True
+
+    def drain(self) -> None:
+        """Barrier: run/await flushes until no flush is pending."""
+        while self.flush_step():
+            pass
+        with self._lock:
+            self._wait_pending()
+
+    # -- flush machinery -------------------------------------------------------
+    def _flush_batch_locked(self, batch: int, asynchronous: bool = False) -> None:
+        first = self._r0 + self._pending_rows
+        batch = min(batch, self._rlen - self._pending_rows)
+        if batch <= 0:
+            return
+        n0 = self._n_q + self._pending_rows
+        self._ensure_store(n0 + batch)
+        cents_k = self.cb_K.device_centroids(self.device)
+        cents_v = self.cb_V.device_centroids(self.device)
+        nb = self.config.nbits
+        rows_k = self._rk[first: first + batch]
+        rows_v = self._rv[first: first + batch]
+        out_k = self._store_k[n0: n0 + batch]
+        out_v = self._store_v[n0: n0 + batch]
+        if not asynchronous:
+            K.encode(rows_k, cents_k, nb, out=out_k)
+            K.encode(rows_v, cents_v, nb, out=out_v)
+            self._n_q += batch          # single publication point
+            self._r0 += batch
+            self._rlen -= batch
+            return
+        main = torch.cuda.current_stream(self.device)
+        self._side.wait_stream(main)    # the rows were written on the main stream
+        with torch.cuda.stream(self._side):
+            K.encode(rows_k, cents_k, nb, out=out_k, stream=self._side)
+            K.encode(rows_v, cents_v, nb, out=out_v, stream=self._side)
+            ev = torch.cuda.Event()
+            ev.record(self._side)
+        for t in (rows_k, rows_v, out_k, out_v):
+            t.record_stream(self._side)
+        self._pending.append((ev, batch))
+        self._pending_rows += batch
+
+    def _publish_completed(self, block: bool = False) -> None:
+        while self._pending:
+            ev, batch = self._pending[0]
+            if block:
+                ev.synchronize()
+            elif not ev.query():
+                break
+            # make later main-stream readers of the store ordered after the encode
+            torch.cuda.current_stream(self.device).wait_event(ev)
+            self._pending.pop(0)
+            self._pending_rows -= batch
+            self._n_q += batch          # single publication point
+            self._r0 += batch
+            self._rlen -= batch
+
+    def _wait_pending(self) -> None:
+        self._publish_completed(block=True)
+
+    def close(self) -> None:
+        with self._lock:
+            self._wait_pending()
+
+    def load_snapshot(self, snap: CacheSnapshot) -> None:
+        """Restore a previously captured state into an empty cache."""
+        if self._n_total != 0:
+            raise RuntimeError("load_snapshot requires an empty cache")
+        if snap.codes_K.M != self.config.M or snap.codes_K.nbits != self.config.nbits:
+            raise ValueError("snapshot geometry does not match codebooks")
+        with self._lock:
+            n = snap.codes_K.n_tokens
+            self._ensure_store(n)
+            if n:
+                self._store_k[:n] = snap.codes_K.device_codes(self.device)
+                self._store_v[:n] = snap.codes_V.device_codes(self.device)
+            self._n_q = n
+            r = int(snap.recent_K.shape[0])
+            if r:
+                self._ensure_recent(r)
+                self._rk[:r] = self._rows(snap.recent_K, "recent_K").reshape(r, -1)
+                self._rv[:r] = self._rows(snap.recent_V, "recent_V").reshape(r, -1)
+            self._r0, self._rlen = 0, r
+            self._n_total = snap.n_total
+
+    # -- reads -------------------------------------------------------------------
+    def snapshot(self) -> CacheSnapshot:
+        """Consistent view covering every stored token exactly once."""
+        with self._lock:
+            self._publish_completed()
+            n_q = self._n_q
+            rk = self._rk[self._r0: self._r0 + self._rlen].clone()
+            rv = self._rv[self._r0: self._r0 + self._rlen].clone()
+            n_total = self._n_total
+            sk, sv = self._store_k, self._store_v
+        return CacheSnapshot(codes_K=CodesMatrix(codes=sk[:n_q], nbits=self.config.nbits),
+                             codes_V=CodesMatrix(codes=sv[:n_q], nbits=self.config.nbits),
+                             recent_K=rk, recent_V=rv, n_q=n_q, n_total=n_total)
+
+    def memory_usage(self) -> dict[str, int]:
+        """Exact byte accounting of current storage."""
+        with self._lock:
+            self._publish_completed()
+            cell = self.config.cell_width
+            return {"codes_bytes": 2 * self._n_q * self.config.M * cell,
+                    "recent_bytes": 2 * self._rlen * self.config.d * 4,
+                    "codebook_bytes": self.cb_K.nbytes() + self.cb_V.nbytes()}

@@ -1,0 +1,175 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads without a
+GPU, exports every entry point include/pqkv_sm100.h declares, validates
+arguments before touching CUDA, and the Python mirror keeps the reference's
+signatures and errors."""
+
+import inspect
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pqkv_sm100.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(pqkv_\w+)\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2504_03661_b200 import _native as N
+    from paper_2504_03661_b200 import build as B
+    if not os.path.exists(N.library_path()):
+        B.build()
+    return N.load(require_cuda=False)
+
+
+def test_header_symbols_exported(lib):
+    names = _declared()
+    assert len(names) >= 12
+    from paper_2504_03661_b200 import _native as N
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in N.SIGNATURES, f"{name} has no ctypes signature"
+
+
+def test_no_torch_types_in_header():
+    src = open(os.path.join(ROOT, "include", "pqkv_sm100.h")).read()
+    assert "torch" not in src.replace("no torch", "") and "at::" not in src
+    assert 'extern "C"' in src
+
+
+def test_bad_arguments_fail_before_cuda(lib):
+    from paper_2504_03661_b200 import _native as N
+    assert lib.pqkv_version() == 1
+    # d not divisible by M -> EINVAL with a message, no CUDA call needed
+    rc = lib.pqkv_encode(None, 0, 10, 130, 130, None, 64, 8, None, 64, None)
+    assert rc == N.PQKV_EINVAL
+    assert b"geometry" in lib.pqkv_last_error()
+    rc = lib.pqkv_decode_partials(None, 1, 6, 4, None, None, 0, None, None, 128, 64, 8, 1,
+                                  None, None)
+    assert rc == N.PQKV_EINVAL and b"multiple" in lib.pqkv_last_error()
+    rc = lib.pqkv_prepare_value_codebook(None, 128, 32, 8, None, None)
+    assert rc == N.PQKV_EINVAL
+    with pytest.raises(ValueError):
+        N.check(N.PQKV_EINVAL, "x")
+    # n == 0 is a no-op success
+    assert lib.pqkv_encode(None, 0, 0, 128, 128, None, 64, 8, None, 64, None) == 0
+
+
+def test_partials_size(lib):
+    from paper_2504_03661_b200 import _native as N
+    assert N.partials_floats(148, 16, 32, 128) == (148 + 16 * 32) * 132
+
+
+def test_reference_signatures_kept():
+    """Same parameter names/defaults as the reference public API (pqkv/__init__.py)."""
+    import paper_2504_03661_b200 as P
+    exp = {
+        "assign_codes": ["X", "cb"],
+        "reconstruct": ["codes", "cb"],
+        "build_key_lut": ["q_n", "cb_K", "scale"],
+        "score_tokens": ["lut", "codes_K", "counters"],
+        "quantized_partial": ["lut", "codes_K", "codes_V", "cb_V", "strategy", "counters",
+                              "timings"],
+        "dense_partial": ["q_n", "K_dense", "V_dense", "scale", "counters"],
+        "merge_partials": ["a", "b"],
+        "finalize": ["p"],
+        "decode_step": ["q_n", "k_n", "v_n", "cache", "cb_K", "cb_V", "scale", "strategy",
+                        "block_size", "counters", "timings"],
+        "read_codebook": ["path", "config_overrides"],
+    }
+    for name, params in exp.items():
+        got = list(inspect.signature(getattr(P, name)).parameters)
+        assert got == params, (name, got)
+    cache_params = list(inspect.signature(P.LayerKVCache).parameters)
+    assert cache_params[:5] == ["cb_K", "cb_V", "recent_capacity", "flush_threshold", "worker"]
+    for m in ("prefill_ingest", "append_decode", "flush_recent", "flush_step", "drain",
+              "snapshot", "load_snapshot", "memory_usage", "close"):
+        assert hasattr(P.LayerKVCache, m), m
+
+
+def test_pqconfig_validation_matches_reference():
+    import paper_2504_03661_b200 as P
+    with pytest.raises(ValueError):
+        P.PQConfig(d=130, M=64, nbits=8)
+    with pytest.raises(ValueError):
+        P.PQConfig(d=128, M=64, nbits=17)
+    with pytest.raises(ValueError):
+        P.PQConfig(d=0, M=1, nbits=8)
+    c = P.PQConfig(128, 64, 8)
+    assert (c.dsub, c.ksub, c.cell_width) == (2, 256, 1)
+    assert P.PQConfig(128, 32, 12).cell_width == 2
+    assert P.bits_per_value(c) == 4.0
+    assert P.PRESETS == {"m64b8": (64, 8), "m32b12": (32, 12)}
+
+
+def test_codebook_and_codes_validation():
+    import paper_2504_03661_b200 as P
+    cfg = P.PQConfig(8, 4, 2)
+    with pytest.raises(ValueError):
+        P.Codebook(cfg, np.zeros((4, 4, 3), np.float32))
+    bad = np.zeros((4, 4, 2), np.float32)
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        P.Codebook(cfg, bad)
+    with pytest.raises(ValueError):
+        P.Codebook(cfg, np.zeros((4, 4, 2), np.float32), kind="query")
+    with pytest.raises(ValueError):
+        P.CodesMatrix(np.array([[0, 4, 1, 1]], np.uint8), nbits=2)
+    with pytest.raises(ValueError):
+        P.CodesMatrix(np.zeros(4, np.uint8), nbits=2)
+    cm = P.CodesMatrix(np.array([[255, 0]], np.uint8), nbits=8)
+    assert (cm.n_tokens, cm.M, cm.cell_width, cm.nbytes()) == (1, 2, 1, 2)
+
+
+def test_fileio_host_roundtrip(golden, tmp_path):
+    import paper_2504_03661_b200 as P
+    g = golden("fileio")
+    for gi in range(3):
+        p = tmp_path / f"cb{gi}.pqkv"
+        p.write_bytes(g[f"f{gi}_raw"].tobytes())
+        cb = P.read_codebook(p)
+        d, M, nbits, kind = (int(v) for v in g[f"f{gi}_geom"])
+        assert (cb.config.d, cb.config.M, cb.config.nbits) == (d, M, nbits)
+        assert cb.kind == ("key" if kind == 0 else "value")
+        np.testing.assert_array_equal(cb.centroids, g[f"f{gi}_cents"])
+        P.write_codebook(tmp_path / "w.pqkv", cb)
+        assert (tmp_path / "w.pqkv").read_bytes() == p.read_bytes()
+    raw = g["f0_raw"].tobytes()
+    for bad in (b"XXXX" + raw[4:], raw[:-4], raw[:4] + b"\x02" + raw[5:]):
+        (tmp_path / "bad.pqkv").write_bytes(bad)
+        with pytest.raises(P.FormatError):
+            P.read_codebook(tmp_path / "bad.pqkv")
+    assert issubclass(P.FormatError, ValueError)
+
+
+def test_cache_dump_roundtrip_host(tmp_path):
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(0)
+    cfg = P.PQConfig(8, 4, 2)
+    snap = P.CacheSnapshot(P.CodesMatrix(rng.integers(0, 4, (5, 4)).astype(np.uint8), 2),
+                           P.CodesMatrix(rng.integers(0, 4, (5, 4)).astype(np.uint8), 2),
+                           rng.standard_normal((3, 8)).astype(np.float32),
+                           rng.standard_normal((3, 8)).astype(np.float32), 5, 8)
+    P.write_cache_dump(tmp_path / "c.pqkc", snap, cfg)
+    back, cfg2 = P.read_cache_dump(tmp_path / "c.pqkc")
+    assert cfg2 == cfg and back.n_q == 5 and back.n_total == 8
+    np.testing.assert_array_equal(back.codes_K.codes, snap.codes_K.codes)
+    np.testing.assert_array_equal(back.recent_V, snap.recent_V)
+    raw = (tmp_path / "c.pqkc").read_bytes()
+    (tmp_path / "t.pqkc").write_bytes(raw[:-1])
+    with pytest.raises(P.FormatError):
+        P.read_cache_dump(tmp_path / "t.pqkc")
+
+
+def test_shard_tokens_cover_exactly_once():
+    from paper_2504_03661_b200.engine import shard_tokens
+    for n in (0, 1, 7, 131072, 131071):
+        for w in (1, 2, 3, 8):
+            spans = [shard_tokens(n, r, w) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))

@@ -1,0 +1,398 @@
+"""Parity of the sm_100a path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Needs a B200: run with ``-m gpu``.
+
+Tolerances: codes are bit-exact; attention outputs are float32 on the GPU vs
+float64 in the reference, compared at rtol 1e-5 (atol 1e-6) on unit-scale
+data -- the reference's own acceptance bar (test_acceptance.py:41-72).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pqkv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2504_03661_b200._native as N
+    N.load()  # fails loudly if the library is missing
+
+
+def _cb(cents, kind, nbits):
+    import paper_2504_03661_b200 as P
+    M, ksub, dsub = cents.shape
+    return P.Codebook(P.PQConfig(M * dsub, M, nbits), np.asarray(cents, np.float32), kind)
+
+
+# ------------------------------------------------------------------ encode --
+
+def test_encode_golden_geometries(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("encode")
+    gi = 0
+    while f"g{gi}_geom" in g:
+        d, M, nbits = (int(v) for v in g[f"g{gi}_geom"])
+        cb = _cb(g[f"g{gi}_cents"], "key", nbits)
+        got = P.assign_codes(g[f"g{gi}_X"], cb).codes
+        np.testing.assert_array_equal(got, g[f"g{gi}_codes"], err_msg=f"geometry {d, M, nbits}")
+        gi += 1
+
+
+def test_encode_exact_ties_lowest_index(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("encode")
+    cb = _cb(g["tie_cents"], "key", 3)
+    np.testing.assert_array_equal(P.assign_codes(g["tie_X"], cb).codes, g["tie_codes"])
+
+
+def test_encode_trained_codebooks(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("encode")
+    for kind in ("k", "v"):
+        cb = _cb(g[f"trained_cents_{kind}"], "key", 8)
+        np.testing.assert_array_equal(P.assign_codes(g[f"trained_X_{kind}"], cb).codes,
+                                      g[f"trained_codes_{kind}"])
+
+
+def test_encode_large_m64b8_vs_c_oracle():
+    """32K vectors of the BASELINE geometry, bit-exact against the C oracle."""
+    from paper_2504_03661_b200 import kernels as K
+    if O.c_library() is None:
+        pytest.skip("oracle C library not built")
+    rng = np.random.default_rng(5)
+    cents = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    X = (rng.standard_normal((32768, 128)) * 1.3).astype(np.float32)
+    got = K.encode(torch.from_numpy(X).cuda(), torch.from_numpy(cents).cuda(), 8).cpu().numpy()
+    want = O.c_assign_codes(X, cents, 8)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_encode_half_inputs(dtype):
+    """bf16/f16 rows are upcast exactly; codes equal the oracle on the upcast values."""
+    from paper_2504_03661_b200 import kernels as K
+    rng = np.random.default_rng(6)
+    cents = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    X = torch.from_numpy(rng.standard_normal((2048, 128)).astype(np.float32)).to(dtype)
+    got = K.encode(X.cuda(), torch.from_numpy(cents).cuda(), 8).cpu().numpy()
+    want = O.assign_codes(X.float().numpy(), cents, 8)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_encode_strided_output_rows():
+    """Encoding straight into a slice of a larger code store (the cache flush path)."""
+    from paper_2504_03661_b200 import kernels as K
+    rng = np.random.default_rng(7)
+    cents = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    X = rng.standard_normal((100, 128)).astype(np.float32)
+    store = torch.full((300, 64), 7, dtype=torch.uint8, device="cuda")
+    K.encode(torch.from_numpy(X).cuda(), torch.from_numpy(cents).cuda(), 8, out=store[50:150])
+    s = store.cpu().numpy()
+    np.testing.assert_array_equal(s[50:150], O.assign_codes(X, cents, 8))
+    assert (s[:50] == 7).all() and (s[150:] == 7).all()
+
+
+def test_reconstruct_matches_oracle():
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(8)
+    for (d, M, nbits) in [(128, 64, 8), (8, 4, 2), (128, 32, 12)]:
+        cfg = P.PQConfig(d, M, nbits)
+        cents = rng.standard_normal((M, cfg.ksub, cfg.dsub)).astype(np.float32)
+        codes = rng.integers(0, cfg.ksub, (77, M)).astype(cfg.code_dtype)
+        cb = P.Codebook(cfg, cents, "value")
+        got = P.reconstruct(P.CodesMatrix(codes, nbits), cb)
+        np.testing.assert_array_equal(got, O.reconstruct(codes, cents))
+
+
+# -------------------------------------------------------------- attention --
+
+def test_lut_matches_golden(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("attention")
+    for ci in range(int(g["ncases"])):
+        d, M, nbits = (int(v) for v in g[f"c{ci}_params"][:3])
+        lut = P.build_key_lut(g[f"c{ci}_q"][0], _cb(g[f"c{ci}_cents_k"], "key", nbits))
+        np.testing.assert_allclose(lut.table, g[f"c{ci}_lut0"], rtol=2e-6, atol=2e-6)
+
+
+def test_quantized_partial_matches_golden(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("attention")
+    seen = 0
+    for ci in range(int(g["ncases"])):
+        if f"c{ci}_qp" not in g:
+            continue
+        d, M, nbits = (int(v) for v in g[f"c{ci}_params"][:3])
+        ck, cv = _cb(g[f"c{ci}_cents_k"], "key", nbits), _cb(g[f"c{ci}_cents_v"], "value", nbits)
+        lut = P.build_key_lut(g[f"c{ci}_q"][0], ck)
+        p = P.quantized_partial(lut, P.CodesMatrix(g[f"c{ci}_snap0_codes_k"], nbits),
+                                P.CodesMatrix(g[f"c{ci}_snap0_codes_v"], nbits), cv)
+        want = g[f"c{ci}_qp"]
+        assert p.m == pytest.approx(want[0], rel=RTOL, abs=ATOL)
+        np.testing.assert_allclose(P.finalize(p), want[2:] / want[1], rtol=RTOL, atol=ATOL)
+        seen += 1
+    assert seen >= 5
+
+
+@pytest.mark.parametrize("ci", range(10))
+def test_decode_step_replay_matches_reference(golden, ci):
+    """Replay the reference's decode_step streams through the GPU cache."""
+    import paper_2504_03661_b200 as P
+    g = golden("attention")
+    d, M, nbits, R, R_f, npre, steps, bs = (int(x) for x in g[f"c{ci}_params"])
+    ck, cv = _cb(g[f"c{ci}_cents_k"], "key", nbits), _cb(g[f"c{ci}_cents_v"], "value", nbits)
+    cache = P.LayerKVCache(ck, cv, recent_capacity=R, flush_threshold=R_f, worker="sync")
+    snap0 = P.CacheSnapshot(P.CodesMatrix(g[f"c{ci}_snap0_codes_k"], nbits),
+                            P.CodesMatrix(g[f"c{ci}_snap0_codes_v"], nbits),
+                            g[f"c{ci}_snap0_recent_k"], g[f"c{ci}_snap0_recent_v"],
+                            int(g[f"c{ci}_nq"][0]),
+                            int(g[f"c{ci}_nq"][0]) + g[f"c{ci}_snap0_recent_k"].shape[0])
+    cache.load_snapshot(snap0)
+    outs = []
+    for s in range(steps):
+        assert cache.n_q == g[f"c{ci}_nq"][s]
+        outs.append(P.decode_step(g[f"c{ci}_q"][s], g[f"c{ci}_steps_k"][s],
+                                  g[f"c{ci}_steps_v"][s], cache, ck, cv, block_size=bs))
+    np.testing.assert_allclose(np.stack(outs), g[f"c{ci}_out"], rtol=RTOL, atol=ATOL)
+    fin = cache.snapshot()
+    np.testing.assert_array_equal(fin.codes_K.codes.cpu().numpy(), g[f"c{ci}_final_codes_k"])
+    np.testing.assert_array_equal(fin.codes_V.codes.cpu().numpy(), g[f"c{ci}_final_codes_v"])
+
+
+def test_dense_merge_finalize_golden(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("attention")
+    q, Kd, Vd = g["merge_q"], g["merge_K"], g["merge_V"]
+    a = P.dense_partial(q, Kd[:13], Vd[:13])
+    b = P.dense_partial(q, Kd[13:], Vd[13:])
+    np.testing.assert_allclose([a.m, a.l, *a.acc], g["merge_a"], rtol=RTOL, atol=ATOL)
+    ab = P.merge_partials(a, b)
+    np.testing.assert_allclose(P.finalize(ab), g["merge_final"], rtol=RTOL, atol=ATOL)
+    # device partials merge on the GPU
+    da = P.SoftmaxPartial(a.m, a.l, torch.from_numpy(a.acc).float().cuda())
+    db = P.SoftmaxPartial(b.m, b.l, torch.from_numpy(b.acc).float().cuda())
+    dab = P.merge_partials(da, db)
+    np.testing.assert_allclose(P.finalize(dab).cpu().numpy(), g["merge_final"], rtol=RTOL,
+                               atol=ATOL)
+    with pytest.raises(ValueError):
+        P.dense_partial(q, Kd[:0], Vd[:0])
+    with pytest.raises(ValueError):
+        P.finalize(P.empty_partial(8))
+
+
+def test_empty_cache_first_step_returns_v1():
+    """test_attention.py:207-215: with nothing cached the output is v_n."""
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(3)
+    cfg = P.PQConfig(128, 64, 8)
+    ck = P.Codebook(cfg, rng.standard_normal((64, 256, 2)).astype(np.float32), "key")
+    cv = P.Codebook(cfg, rng.standard_normal((64, 256, 2)).astype(np.float32), "value")
+    cache = P.LayerKVCache(ck, cv)
+    v = rng.standard_normal(128).astype(np.float32)
+    out = P.decode_step(rng.standard_normal(128), rng.standard_normal(128), v, cache, ck, cv)
+    np.testing.assert_allclose(out, v, rtol=1e-6, atol=1e-6)
+
+
+# ------------------------------------------------------------- batched path --
+
+def _oracle_heads(q, ck_codes, cv_codes, n_q, rk, rv, n_r, kcur, vcur, cents_k, cents_v, G):
+    """Per (b, hq) oracle: snapshot -> LUT -> quantized + dense partials -> finalize."""
+    B, Hq, d = q.shape
+    out = np.zeros((B, Hq, d))
+    for b in range(B):
+        for h in range(Hq):
+            kv = h // G
+            n = n_q[b]
+            out[b, h] = O.decode_from_snapshot(
+                q[b, h], kcur[b, kv], vcur[b, kv], ck_codes[b, kv, :n], cv_codes[b, kv, :n],
+                rk[b, kv, :n_r[b]], rv[b, kv, :n_r[b]], cents_k, cents_v, block_size=1 << 30)
+    return out
+
+
+def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None):
+    from paper_2504_03661_b200 import kernels as K
+    from paper_2504_03661_b200.engine import PQDecoder
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(seed)
+    cfg = P.PQConfig(128, 64, 8)
+    cents_k = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    cents_v = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    q = rng.standard_normal((B, Hq, 128)).astype(np.float32)
+    codes_k = rng.integers(0, 256, (B, Hkv, cap, 64), dtype=np.uint8)
+    codes_v = rng.integers(0, 256, (B, Hkv, cap, 64), dtype=np.uint8)
+    rk = rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)
+    rv = rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)
+    kc = rng.standard_normal((B, Hkv, 128)).astype(np.float32)
+    vc = rng.standard_normal((B, Hkv, 128)).astype(np.float32)
+    dev = torch.device("cuda")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    dec = PQDecoder(B, Hq, Hkv, cfg, num_ctas=num_ctas)
+    cbk = t(cents_k)
+    cbv = K.value_codebook_layout(t(cents_v), 8)
+    out = dec(t(q), t(codes_k), t(codes_v), t(np.array(n_q, np.int32)), cbk, cbv, t(rk), t(rv),
+              t(np.array(n_r, np.int32)), t(kc), t(vc))
+    want = _oracle_heads(q, codes_k, codes_v, n_q, rk, rv, n_r, kc, vc, cents_k, cents_v,
+                         Hq // Hkv)
+    return out.cpu().numpy(), want
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
+    (1, 4, 4, 3000, [3000], [31]),                    # MHA, multi-CTA per head
+    (2, 8, 2, 5000, [4999, 1234], [5, 32]),           # GQA 4:1, ragged lengths
+    (3, 2, 1, 700, [0, 1, 7], [0, 3, 0]),             # empty / tiny quantized spans
+    (1, 1, 1, 100000, [100000], [0]),                 # long single head
+])
+def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
+    got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_batched_decoder_more_ctas_than_tokens():
+    got, want = _batched_case(2, 2, 2, 64, [40, 9], [1, 2], num_ctas=300)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_batched_decoder_config2_layer_vs_c_oracle():
+    """One Llama-2-7B layer at 32K context (BASELINE config 2 shape), all 32
+    heads, against the float64 C oracle."""
+    from paper_2504_03661_b200 import kernels as K
+    from paper_2504_03661_b200.engine import PQDecoder
+    import paper_2504_03661_b200 as P
+    if O.c_library() is None:
+        pytest.skip("oracle C library not built")
+    rng = np.random.default_rng(11)
+    H, n, R = 32, 32768, 31
+    cents_k = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    cents_v = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    q = rng.standard_normal((1, H, 128)).astype(np.float32)
+    ck = rng.integers(0, 256, (1, H, n, 64), dtype=np.uint8)
+    cv = rng.integers(0, 256, (1, H, n, 64), dtype=np.uint8)
+    rk = rng.standard_normal((1, H, R, 128)).astype(np.float32)
+    rv = rng.standard_normal((1, H, R, 128)).astype(np.float32)
+    kc = rng.standard_normal((1, H, 128)).astype(np.float32)
+    vc = rng.standard_normal((1, H, 128)).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    dec = PQDecoder(1, H, H, P.PQConfig(128, 64, 8))
+    out = dec(t(q), t(ck), t(cv), t(np.array([n], np.int32)), t(cents_k),
+              K.value_codebook_layout(t(cents_v), 8), t(rk), t(rv),
+              t(np.array([R], np.int32)), t(kc), t(vc)).cpu().numpy()[0]
+    lib = O.c_library()
+    want = np.empty((H, 128))
+    import ctypes
+    P_ = ctypes.c_void_p
+    qd = np.ascontiguousarray(q[0], np.float64)
+    rc = lib.oracle_decode_heads_mt(
+        qd.ctypes.data_as(P_), kc[0].ctypes.data_as(P_), vc[0].ctypes.data_as(P_),
+        ck[0].ctypes.data_as(P_), cv[0].ctypes.data_as(P_), n, n,
+        rk[0].ctypes.data_as(P_), rv[0].ctypes.data_as(P_), R,
+        cents_k.ctypes.data_as(P_), cents_v.ctypes.data_as(P_), 64, 8, 2,
+        1.0 / np.sqrt(128.0), 8192, want.ctypes.data_as(P_), H, 8)
+    assert rc == 0
+    np.testing.assert_allclose(out, want, rtol=RTOL, atol=ATOL)
+
+
+def test_sequence_split_merge_equals_full():
+    """Sequence split (config 4 pattern) on one GPU: W token ranges decoded to
+    partial records, merged in rank order == the unsplit decode."""
+    from paper_2504_03661_b200 import kernels as K
+    from paper_2504_03661_b200.engine import PQDecoder, shard_tokens
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(12)
+    B, Hq, Hkv, n, W = 2, 8, 2, 20000, 4
+    cfg = P.PQConfig(128, 64, 8)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    cbk = t(rng.standard_normal((64, 256, 2)).astype(np.float32))
+    cbv = K.value_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8)
+    q = t(rng.standard_normal((B, Hq, 128)).astype(np.float32))
+    ck = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+    cv = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+    rk = t(rng.standard_normal((B, Hkv, 16, 128)).astype(np.float32))
+    rv = t(rng.standard_normal((B, Hkv, 16, 128)).astype(np.float32))
+    nr = t(np.array([16, 3], np.int32))
+    kc = t(rng.standard_normal((B, Hkv, 128)).astype(np.float32))
+    vc = t(rng.standard_normal((B, Hkv, 128)).astype(np.float32))
+    dec = PQDecoder(B, Hq, Hkv, cfg)
+    full = dec(q, ck, cv, t(np.array([n, n], np.int32)), cbk, cbv, rk, rv, nr, kc, vc)
+    recs = []
+    for r in range(W):
+        a, b = shard_tokens(n, r, W)
+        tail = r == W - 1
+        rec = torch.empty((B * Hq, 132), device="cuda")
+        dec(q, ck[:, :, a:b].contiguous(), cv[:, :, a:b].contiguous(),
+            t(np.array([b - a] * B, np.int32)), cbk, cbv, rk if tail else None,
+            rv if tail else None, nr if tail else None, kc if tail else None,
+            vc if tail else None, merged=rec, finalize=False)
+        recs.append(rec)
+    out = torch.empty_like(full)
+    K.merge_partials(torch.stack(recs), out=out)
+    np.testing.assert_allclose(out.cpu().numpy(), full.cpu().numpy(), rtol=2e-6, atol=1e-6)
+
+
+# ------------------------------------------------------------------- cache --
+
+def test_cache_sequences_match_reference(golden):
+    import paper_2504_03661_b200 as P
+    g = golden("cache")
+    for tr in range(int(g["ntrials"])):
+        R, R_f, npre, n = (int(x) for x in g[f"t{tr}_params"])
+        ck, cv = _cb(g["cents_k"], "key", 2), _cb(g["cents_v"], "value", 2)
+        c = P.LayerKVCache(ck, cv, recent_capacity=R, flush_threshold=R_f)
+        K_, V_ = g[f"t{tr}_K"], g[f"t{tr}_V"]
+        if npre:
+            c.prefill_ingest(K_[:npre], V_[:npre])
+        for t_ in range(npre, npre + n):
+            c.append_decode(K_[t_], V_[t_])
+        s = c.snapshot()
+        np.testing.assert_array_equal(s.codes_K.codes.cpu().numpy(), g[f"t{tr}_codes_k"])
+        np.testing.assert_array_equal(s.codes_V.codes.cpu().numpy(), g[f"t{tr}_codes_v"])
+        np.testing.assert_array_equal(s.recent_K.cpu().numpy(), g[f"t{tr}_recent_k"])
+        assert (s.n_q, s.n_total) == tuple(int(v) for v in g[f"t{tr}_nq"])
+
+
+@pytest.mark.parametrize("worker", ["thread", "manual"])
+def test_async_worker_bit_identical_to_sync(worker):
+    """C4 (test_acceptance.py:134-199): any flush schedule drains to the sync state,
+    and every snapshot covers each token exactly once."""
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(21)
+    cfg = P.PQConfig(128, 64, 8)
+    ck = P.Codebook(cfg, rng.standard_normal((64, 256, 2)).astype(np.float32), "key")
+    cv = P.Codebook(cfg, rng.standard_normal((64, 256, 2)).astype(np.float32), "value")
+    Kr = rng.standard_normal((700, 128)).astype(np.float32)
+    Vr = rng.standard_normal((700, 128)).astype(np.float32)
+    sync = P.LayerKVCache(ck, cv, 16, 8, "sync")
+    other = P.LayerKVCache(ck, cv, 16, 8, worker)
+    for c in (sync, other):
+        c.prefill_ingest(Kr[:300], Vr[:300])
+    for t_ in range(300, 700):
+        sync.append_decode(Kr[t_], Vr[t_])
+        other.append_decode(Kr[t_], Vr[t_])
+        if worker == "manual" and rng.random() < 0.3:
+            other.flush_step()
+        s = other.snapshot()
+        assert s.n_q + s.recent_K.shape[0] == s.n_total == t_ + 1
+    other.drain()
+    a, b = sync.snapshot(), other.snapshot()
+    assert (a.n_q, a.n_total) == (b.n_q, b.n_total)
+    np.testing.assert_array_equal(a.codes_K.codes.cpu().numpy(), b.codes_K.codes.cpu().numpy())
+    np.testing.assert_array_equal(a.codes_V.codes.cpu().numpy(), b.codes_V.codes.cpu().numpy())
+    np.testing.assert_array_equal(a.recent_K.cpu().numpy(), b.recent_K.cpu().numpy())
+
+
+def test_codebook_file_to_device(golden, tmp_path):
+    import paper_2504_03661_b200 as P
+    g = golden("fileio")
+    raw = g["f0_raw"].tobytes()
+    p = tmp_path / "cb.pqkv"
+    p.write_bytes(raw)
+    cb = P.read_codebook(p)
+    np.testing.assert_array_equal(cb.device_centroids().cpu().numpy(), g["f0_cents"])
+    P.write_codebook(tmp_path / "back.pqkv", cb)
+    assert (tmp_path / "back.pqkv").read_bytes() == raw
