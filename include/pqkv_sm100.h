@@ -44,14 +44,30 @@ extern "C" {
 int pqkv_version(void);
 const char *pqkv_last_error(void);
 
+/* Code layouts.  PQKV rows: token-major rows of M cells in subspace order,
+ * the reference's CodesMatrix.  Decode layout (m64b8 only): the same rows
+ * with each 16-byte quarter q of token t stored rotated, subspace i at byte
+ * 16q + ((i - r) & 15), r = ((l & 15) + (l >> 4)) & 15, l = 4 (t & 7) + q;
+ * the decode kernel's lanes then read their bytes in register order and still
+ * hit 32 distinct shared-memory banks per step.  t counts rows from the start
+ * of the buffer handed to the decode kernel.  A per-row bijection. */
+
 /* Nearest-centroid encoder, bit-exact with assign_codes (pq_core.py:269-287
  * on top of _squared_distances :158-168): fp64 d2 = (|x|^2 - 2 x.c) + |c|^2
  * with numpy's pairwise norms and a sequential x.c, clamped at 0, lowest
  * index on ties.  x: n rows of d values (row stride ld_x elements, dtype
- * PQKV_DTYPE_*); codes: n rows of M cells, row stride ld_codes cells. */
+ * PQKV_DTYPE_*); codes: n rows of M cells, row stride ld_codes cells.
+ * rot_base < 0 writes the row layout; rot_base >= 0 writes the decode layout
+ * with row 0 being token index rot_base of the destination buffer. */
 int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
                 const float *centroids, int M, int nbits, void *codes,
-                int64_t ld_codes, void *stream);
+                int64_t ld_codes, int64_t rot_base, void *stream);
+
+/* Convert n rows between the row layout and the decode layout (to_decode = 1:
+ * rows -> decode, 0: decode -> rows); row 0 is token index t_first. */
+int pqkv_relayout_codes(const void *src, int64_t ld_src, void *dst,
+                        int64_t ld_dst, int64_t n, int64_t t_first,
+                        int to_decode, int d, int M, int nbits, void *stream);
 
 /* reconstruct (pq_core.py:290-304): out[t, i*dsub + j] = C[i, codes[t, i], j].
  * Test/diagnostic helper: the attention path never dequantizes. */
@@ -66,10 +82,16 @@ int pqkv_reconstruct(const void *codes, int64_t n, int64_t ld_codes,
 int pqkv_build_lut(const float *q, int64_t n_heads, int d, const float *cb_k,
                    int M, int nbits, float scale, float *lut, void *stream);
 
-/* One-time re-layout of a value codebook for the m64b8 fast path
- * (d=128, M=64, nbits=8): out is [2][256][32] float2, i.e. subspace half,
- * centroid, subspace-within-half.  65536 float32.  Other geometries use the
- * plain (M, ksub, dsub) codebook and need no call. */
+/* One-time re-layouts of a layer's codebooks for the m64b8 fast path
+ * (d=128, M=64, nbits=8), done at codebook load:
+ *   key:   [256][64] float2 (centroid-major; the in-kernel LUT build reads it
+ *          with coalesced 16-byte loads)
+ *   value: [2][256][32] float2 (subspace half, centroid, subspace-in-half;
+ *          the shared-memory image the value gather reads conflict-free)
+ * Each output is 65536 float32.  Other geometries use the plain
+ * (M, ksub, dsub) codebooks and need no call. */
+int pqkv_prepare_key_codebook(const float *cb_k, int d, int M, int nbits,
+                              float *out, void *stream);
 int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits,
                                 float *out, void *stream);
 
@@ -82,21 +104,35 @@ int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d);
 
 /* Quantized-span softmax partials: the fused LUT-score + online softmax +
  * value accumulation of quantized_partial (attention.py:114-166), i.e.
- * score_codes (_kernels.py:27-34) and the value aggregation
- * (_kernels.py:37-43 + attention.py:103-111 / :155-157), for every
- * (batch b, query head hq) over tokens [0, n_q[b]) of KV head
+ * build_key_lut (:70-83), score_codes (_kernels.py:27-34) and the value
+ * aggregation (_kernels.py:37-43 + attention.py:103-111 / :155-157), for
+ * every (batch b, query head hq) over tokens [0, n_q[b]) of KV head
  * hkv = hq / (Hq / Hkv).  The token space of all heads is split evenly over
  * num_ctas persistent CTAs; each (CTA, head) overlap emits one partial.
- *   lut      [B*Hq][ksub][M] float32 from pqkv_build_lut
- *   codes_k/codes_v  [B][Hkv][ld_tok][M] cells
+ *   q        [B*Hq][d] float32 queries, scores scaled by `scale`
+ *   cb_k     fast path: pqkv_prepare_key_codebook output (the LUT is built
+ *            in shared memory by the decode kernel itself);
+ *            other geometries: the plain (M, ksub, dsub) codebook
+ *   lut_ws   other geometries: [B*Hq][ksub][M] float32 scratch that receives
+ *            the tables (pqkv_build_lut); unused (may be NULL) on the fast path
+ *   codes_k/codes_v  [B][Hkv][ld_tok][M] cells; fast path: decode layout
  *   n_q      [B] int32 (device): quantized tokens per sequence
  *   cb_v     fast path: pqkv_prepare_value_codebook output; else (M,ksub,dsub)
  *   partials pqkv_partials_floats(num_ctas, B, Hq, d) floats */
-int pqkv_decode_partials(const float *lut, int B, int Hq, int Hkv,
+int pqkv_decode_partials(const float *q, float scale, const float *cb_k,
+                         float *lut_ws, int B, int Hq, int Hkv,
                          const void *codes_k, const void *codes_v,
                          int64_t ld_tok, const int32_t *n_q, const float *cb_v,
                          int d, int M, int nbits, int num_ctas,
                          float *partials, void *stream);
+
+/* Same, from precomputed tables lut [B*Hq][ksub][M] (pqkv_build_lut) -- the
+ * quantized_partial(lut, ...) form of the reference API. */
+int pqkv_decode_partials_lut(const float *lut, int B, int Hq, int Hkv,
+                             const void *codes_k, const void *codes_v,
+                             int64_t ld_tok, const int32_t *n_q,
+                             const float *cb_v, int d, int M, int nbits,
+                             int num_ctas, float *partials, void *stream);
 
 /* Finish one decode step for every (b, hq): merge that head's quantized
  * partials in a fixed order (merge_partials, attention.py:193-204), add the

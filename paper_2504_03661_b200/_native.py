@@ -28,13 +28,18 @@ _F = ctypes.c_float
 SIGNATURES = {
     "pqkv_version": (_I, []),
     "pqkv_last_error": (ctypes.c_char_p, []),
-    "pqkv_encode": (_I, [_P, _I, _I64, _I, _I64, _P, _I, _I, _P, _I64, _P]),
+    "pqkv_encode": (_I, [_P, _I, _I64, _I, _I64, _P, _I, _I, _P, _I64, _I64, _P]),
+    "pqkv_relayout_codes": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P]),
     "pqkv_reconstruct": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
     "pqkv_build_lut": (_I, [_P, _I64, _I, _P, _I, _I, _F, _P, _P]),
     "pqkv_prepare_value_codebook": (_I, [_P, _I, _I, _I, _P, _P]),
     "pqkv_decode_grid": (_I, [_I, _I, _I, ctypes.POINTER(_I)]),
     "pqkv_partials_floats": (_I64, [_I, _I, _I, _I]),
-    "pqkv_decode_partials": (_I, [_P, _I, _I, _I, _P, _P, _I64, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "pqkv_prepare_key_codebook": (_I, [_P, _I, _I, _I, _P, _P]),
+    "pqkv_decode_partials": (_I, [_P, _F, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _I, _I, _I,
+                                  _I, _P, _P]),
+    "pqkv_decode_partials_lut": (_I, [_P, _I, _I, _I, _P, _P, _I64, _P, _P, _I, _I, _I, _I, _P,
+                                      _P]),
     "pqkv_decode_finish": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _F, _P, _P, _I64, _P, _P, _P,
                                 _P, _P, _P, _P]),
     "pqkv_merge_partials": (_I, [_P, _I, _I64, _I, _P, _P, _P, _P]),

@@ -6,15 +6,17 @@ build_key_lut :70-83, score_tokens :86-100, quantized_partial :114-166,
 dense_partial :169-190, merge_partials :193-204, finalize :207-211,
 decode_step :214-287).  The arithmetic runs in libpqkv_sm100.so:
 
-* build_key_lut      -> pqkv_build_lut (float32 table, centroid-major)
+* build_key_lut      -> pqkv_build_lut (float32 table, centroid-major; the
+                        decode kernel builds the same table in shared memory)
 * score_tokens       -> pqkv_score_codes
 * quantized_partial  -> pqkv_decode_partials + pqkv_decode_finish: one fused
                         kernel (LUT gather, online softmax, value accumulation
                         in registers from the shared-memory codebook), split
                         over every SM and merged in a fixed order;
 * dense_partial      -> pqkv_decode_finish (recent rows, no quantized span)
-* decode_step        -> LUT + fused partials + dense/current-token merge +
-                        finalize in three launches, then the cache append.
+* decode_step        -> fused partials (LUT built in shared memory) +
+                        dense/current-token merge + finalize in two launches,
+                        then the cache append.
 
 The reference accumulates in float64 on the CPU; this path accumulates in
 float32 on the GPU.  Outputs agree within the tolerance stated in DESIGN.md
@@ -124,6 +126,13 @@ def score_tokens(lut: Lut, codes_K: CodesMatrix, counters: Counters | None = Non
     return s.double().cpu().numpy() if host else s
 
 
+def _decode_codes(codes: torch.Tensor, cfg) -> torch.Tensor:
+    """Reference row-layout codes -> the layout the decode kernel reads."""
+    if K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits):
+        return K.relayout(codes, to_decode=True)
+    return codes.contiguous()
+
+
 def _n_tensor(n: int, device) -> torch.Tensor:
     return torch.tensor([n], dtype=torch.int32, device=device)
 
@@ -158,11 +167,11 @@ def quantized_partial(lut: Lut, codes_K: CodesMatrix, codes_V: CodesMatrix, cb_V
     if counters is not None:
         counters.code_bytes_read += n * cfg.M * codes_V.cell_width
     ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
-    ws.lut.copy_(tab.view(1, *tab.shape))
-    ck = codes_K.device_codes(dev).contiguous().view(1, 1, n, cfg.M)
-    cv = codes_V.device_codes(dev).contiguous().view(1, 1, n, cfg.M)
+    ck = _decode_codes(codes_K.device_codes(dev), cfg).view(1, 1, n, cfg.M)
+    cv = _decode_codes(codes_V.device_codes(dev), cfg).view(1, 1, n, cfg.M)
     nq = _n_tensor(n, dev)
-    K.decode_partials(ws, 1, ck, cv, nq, cb_V.device_value_layout(dev))
+    K.decode_partials_lut(ws, 1, tab.view(1, *tab.shape), ck, cv, nq,
+                          cb_V.device_value_layout(dev))
     merged = torch.empty((1, cfg.d + 4), dtype=torch.float32, device=dev)
     K.decode_finish(ws, 1, nq, None, 1.0, merged=merged)
     part = _partial_from_record(merged[0], host)
@@ -249,8 +258,16 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         raise ValueError("block_size must be positive")
     sc = _scale(cfg.d, scale)
     host = not _is_tensor(q_n)
-    snap = cache.snapshot()
     dev = getattr(cache, "device", None) or default_device()
+    if hasattr(cache, "raw_snapshot"):       # this package's GPU cache: no copies
+        ck_raw, cv_raw, rk, rv, n_q, _ = cache.raw_snapshot()
+        ck_raw, cv_raw = ck_raw.contiguous(), cv_raw.contiguous()
+    else:                                    # any object with the reference snapshot()
+        snap = cache.snapshot()
+        n_q = snap.codes_K.n_tokens
+        ck_raw = _decode_codes(snap.codes_K.device_codes(dev), cfg) if n_q else None
+        cv_raw = _decode_codes(snap.codes_V.device_codes(dev), cfg) if n_q else None
+        rk, rv = snap.recent_K, snap.recent_V
     q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
                   torch.float32, dev)
     if q.shape[0] != cfg.d:
@@ -263,18 +280,13 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         raise ValueError(f"k_n/v_n width must be d={cfg.d}")
 
     t0 = time.perf_counter()
-    n_q = snap.codes_K.n_tokens
     ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
-    K.build_lut(q.view(1, -1), cb_K.device_centroids(dev), cfg.nbits, sc, out=ws.lut)
-    if timings is not None:
-        t1 = time.perf_counter()
-        timings["lut_build"] = timings.get("lut_build", 0.0) + (t1 - t0)
-        t0 = t1
     nq_t = _n_tensor(n_q, dev)
-    if n_q:
-        ck = snap.codes_K.device_codes(dev).contiguous().view(1, 1, n_q, cfg.M)
-        cv = snap.codes_V.device_codes(dev).contiguous().view(1, 1, n_q, cfg.M)
-        K.decode_partials(ws, 1, ck, cv, nq_t, cb_V.device_value_layout(dev))
+    if n_q:  # the LUT is built inside the fused kernel (lut_build time is part of "score")
+        ck = ck_raw.view(1, 1, n_q, cfg.M)
+        cv = cv_raw.view(1, 1, n_q, cfg.M)
+        K.decode_partials(ws, 1, q.view(1, -1), sc, cb_K.device_key_layout(dev), ck, cv, nq_t,
+                          cb_V.device_value_layout(dev))
     if counters is not None:
         counters.lut_lookups += n_q * cfg.M
         counters.adds += n_q * cfg.M
@@ -283,7 +295,6 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         t1 = time.perf_counter()
         timings["score"] = timings.get("score", 0.0) + (t1 - t0)
         t0 = t1
-    rk, rv = snap.recent_K, snap.recent_V
     r = int(rk.shape[0])
     rkd = to_device(rk if _is_tensor(rk) else np.asarray(rk, dtype=np.float32), torch.float32,
                     dev).contiguous().view(1, 1, r, cfg.d) if r else None

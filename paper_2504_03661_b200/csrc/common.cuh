@@ -41,6 +41,24 @@ inline bool is_fast_geometry(int d, int M, int nbits) {
     return d == 128 && M == 64 && nbits == 8;
 }
 
+// ---------------------------------------------------------- decode layout ---
+// m64b8 decode layout of a 64-byte code row: the decode kernel's lane
+// (slot s = t & 7, quarter q) reads bytes [16q, 16q+16) and processes them in
+// the order j = 0..15 against subspace 16q + ((j + r) & 15), where
+// r = ((lane & 15) + (lane >> 4)) & 15 for lane = 4s + q.  Storing subspace i
+// of token t at byte 16q + ((i - r) & 15) lets every lane take its bytes in
+// register order while the 32 lanes of a warp still hit 32 distinct
+// subspaces (= shared-memory banks) at every step -- no in-register
+// rotation.  A bijection per row, so uniform random codes stay uniform.
+__host__ __device__ __forceinline__ int decode_lane_rot(int lane) {
+    return ((lane & 15) + (lane >> 4)) & 15;
+}
+__host__ __device__ __forceinline__ int decode_layout_pos(int i, int slot) {
+    const int q = i >> 4;
+    const int r = decode_lane_rot(4 * slot + q);
+    return 16 * q + (((i & 15) - r) & 15);
+}
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 

@@ -16,14 +16,16 @@
 //   * shared memory: the head's key LUT, centroid-major [256][64] fp32
 //     (64 KiB), and the value codebook as two [256][32] float2 halves
 //     (128 KiB, loaded once per CTA);
-//   * a warp handles 8 tokens per step: lane = (token slot, 16-subspace
-//     quarter) and loads the 16 K-code and 16 V-code bytes of its quarter with
-//     one 128-bit load each (coalesced: the warp reads 2 x 512 contiguous B);
-//   * each lane rotates its 16 code bytes by a lane constant r so that at
-//     every unrolled step the 32 lanes touch 32 distinct subspaces mod 32:
-//     the LUT gather (bank = subspace mod 32) and the 64-bit codebook gather
-//     (8-byte slot = subspace mod 16 per half-warp) are bank-conflict free
-//     for ANY code values;
+//   * a warp handles 16 tokens per step (two independent 8-token halves, one
+//     merged softmax update): lane = (token slot, 16-subspace quarter) loads
+//     the 16 K-code and 16 V-code bytes of its quarter with one 128-bit load
+//     each (coalesced: the warp reads 4 x 512 contiguous B);
+//   * codes are stored in the decode layout (common.cuh): each quarter is
+//     pre-rotated by its lane constant r, so at every unrolled step the 32
+//     lanes touch 32 distinct subspaces mod 32 without any in-register
+//     shuffling: the LUT gather (bank = subspace mod 32) and the 64-bit
+//     codebook gather (8-byte slot = subspace mod 16 per half-warp) are
+//     bank-conflict free for ANY code values;
 //   * one PRMT per code byte forms the shared-memory byte address
 //     (code << 8 | lane offset | half << 16);
 //   * the 4 lanes of a token combine their partial scores with 2 shuffles;
@@ -31,6 +33,8 @@
 //     value accumulators (its quarter's 16 subspaces x dsub 2);
 //   * epilogue: slot partials are rescaled to the CTA max and summed through
 //     shared memory into one (m, l, acc[128]) record per segment.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pqkv {
@@ -44,8 +48,7 @@ constexpr int M = 64, KSUB = 256, D = 128;
 constexpr int WARPS = 16, NT = WARPS * 32;
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
-constexpr int SMEM_BYTES = LUT_BYTES + CV_BYTES + (2 * WARPS + 4 * D) * 4;
-constexpr int PREFETCH = 2;  // groups in flight per warp beyond the current one
+constexpr int SMEM_BYTES = LUT_BYTES + CV_BYTES + (2 * WARPS + 4 * D) * 4 + 16;
 
 __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
     uint4 r;
@@ -93,48 +96,154 @@ __device__ __forceinline__ float2 unpack2(unsigned long long v) {
     return r;
 }
 
-// rotate the 16 bytes (w0..w3) so that out.byte[j] = in.byte[(j + r) & 15]
-__device__ __forceinline__ void rotate16(const uint4 in, int r, uint32_t (&o)[4]) {
-    uint32_t w0 = in.x, w1 = in.y, w2 = in.z, w3 = in.w;
-    if (r & 4) {
-        const uint32_t t = w0;
-        w0 = w1; w1 = w2; w2 = w3; w3 = t;
-    }
-    if (r & 8) {
-        uint32_t t = w0; w0 = w2; w2 = t;
-        t = w1; w1 = w3; w3 = t;
-    }
-    const uint32_t sh = (uint32_t)(r & 3) * 8u;
-    o[0] = __funnelshift_r(w0, w1, sh);
-    o[1] = __funnelshift_r(w1, w2, sh);
-    o[2] = __funnelshift_r(w2, w3, sh);
-    o[3] = __funnelshift_r(w3, w0, sh);
-}
-
 // PRMT selector for rotated byte j: [offset byte (j&1) of b, code byte (j&3)
 // of a, byte 2 of b, byte 3 of b]
 __device__ __forceinline__ constexpr uint32_t sel_for(int j) {
     return (uint32_t)(4 + (j & 1)) | ((uint32_t)(j & 3) << 4) | (6u << 8) | (7u << 12);
 }
 
+// ---- TMA bulk copy (global -> shared) completing on an mbarrier ------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar), "r"(phase)
+        : "memory");
+}
+
+// One unit = 16 tokens [16u, 16u + 16) of a head: lane slot s takes tokens
+// 16u + s (A) and 16u + 8 + s (B), one 128-bit K load and one V load each.
+// The codes are in the decode layout (common.cuh), so the lane uses its bytes
+// in register order.
+struct Unit {
+    uint4 ka, va, kb, vb;
+};
+
+__device__ __forceinline__ void load_unit(Unit &U, const uint8_t *kbase, const uint8_t *vbase,
+                                          int u, int slot, int lo, int hi) {
+    const int ta = u * 16 + slot, tb = ta + 8;
+    if (ta >= lo && ta < hi) {
+        U.ka = ld_stream(kbase + (int64_t)ta * M);
+        U.va = ld_stream(vbase + (int64_t)ta * M);
+    }
+    if (tb >= lo && tb < hi) {
+        U.kb = ld_stream(kbase + (int64_t)tb * M);
+        U.vb = ld_stream(vbase + (int64_t)tb * M);
+    }
+}
+
+struct SlotState {
+    float m, l;
+    unsigned long long acc[16];  // float2 per (rotated) subspace of this lane's quarter
+};
+
+__device__ __forceinline__ float lut_score(const uint4 k, const uint32_t (&packK)[8]) {
+    const uint32_t w[4] = {k.x, k.y, k.z, k.w};
+    float sp[4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float x = lds_lut(__byte_perm(w[j >> 2], packK[j >> 1], sel_for(j)));
+        if (j < 4)
+            sp[j] = x;
+        else
+            sp[j & 3] += x;
+    }
+    return (sp[0] + sp[1]) + (sp[2] + sp[3]);
+}
+
+template <bool kMask>
+__device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
+                                             const uint32_t (&packK)[8],
+                                             const uint32_t (&packV)[8], bool okA, bool okB) {
+    float sa = lut_score(U.ka, packK);
+    float sb = lut_score(U.kb, packK);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+    sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+    sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+    if (kMask) {
+        if (!okA && !okB) return;
+        if (!okA) sa = -INFINITY;
+        if (!okB) sb = -INFINITY;
+    }
+    const float mx = fmaxf(sa, sb);
+    if (mx > S.m) {
+        const float f = fast_exp2((S.m - mx) * kLog2e);
+        S.l *= f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) fmul2(S.acc[k], f);
+        S.m = mx;
+    }
+    const float pa = fast_exp2((sa - S.m) * kLog2e);
+    const float pb = fast_exp2((sb - S.m) * kLog2e);
+    S.l += pa + pb;
+    const uint32_t wa[4] = {U.va.x, U.va.y, U.va.z, U.va.w};
+    const uint32_t wb[4] = {U.vb.x, U.vb.y, U.vb.z, U.vb.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const unsigned long long ca = lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+        const unsigned long long cb = lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+        ffma2(S.acc[j], pa, ca);
+        ffma2(S.acc[j], pb, cb);
+    }
+}
+
+// kLutFromQ: build each head's LUT in shared memory from q and the
+// centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
+// otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
+template <bool kLutFromQ>
 __global__ void __launch_bounds__(NT, 1)
-    decode_partials_m64b8(const float *__restrict__ lut_g, int B, int Hq, int Hkv,
-                          const uint8_t *__restrict__ codes_k, const uint8_t *__restrict__ codes_v,
-                          int64_t ld_tok, const int32_t *__restrict__ n_q,
-                          const float *__restrict__ cv_g, int num_ctas,
-                          float *__restrict__ parts) {
+    decode_partials_m64b8(const float *__restrict__ q_g, float scale,
+                          const float *__restrict__ ck_g, const float *__restrict__ lut_g, int B,
+                          int Hq, int Hkv, const uint8_t *__restrict__ codes_k,
+                          const uint8_t *__restrict__ codes_v, int64_t ld_tok,
+                          const int32_t *__restrict__ n_q, const float *__restrict__ cv_g,
+                          int num_ctas, float *__restrict__ parts) {
     extern __shared__ __align__(128) unsigned char smem[];
     float *lut_s = reinterpret_cast<float *>(smem);
     float *red_m = reinterpret_cast<float *>(smem + LUT_BYTES + CV_BYTES);
     float *red_l = red_m + WARPS;
     float(*colsum)[D] = reinterpret_cast<float(*)[D]>(red_l + WARPS);
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(colsum[4]);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_lut)
     const uint32_t cta_byte = sbase & 0xFF000000u;
+    const uint32_t bar_cv = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t bar_lut = (uint32_t)__cvta_generic_to_shared(&bars[1]);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q4 = lane & 3, slot = lane >> 2;
-    const int r = ((lane & 15) + (lane >> 4)) & 15;
+    const int r = decode_lane_rot(lane);
+
+    // value codebook: one TMA bulk copy per CTA, overlapped with the first
+    // segment's code prefetch and LUT build
+    if (tid == 0) {
+        mbar_init(bar_cv, 1);
+        mbar_init(bar_lut, 1);
+        mbar_expect_tx(bar_cv, CV_BYTES);
+#pragma unroll
+        for (int c = 0; c < CV_BYTES / 16384; ++c)
+            bulk_g2s(sbase + LUT_BYTES + c * 16384, reinterpret_cast<const char *>(cv_g) + c * 16384,
+                     16384, bar_cv);
+    }
 
     // lane-constant address bytes (see header comment)
     uint32_t packK[8], packV[8];
@@ -152,19 +261,13 @@ __global__ void __launch_bounds__(NT, 1)
         packV[jp] = pv | ((uint32_t)(q4 >> 1) << 16) | cta_byte;
     }
 
-    // value codebook: once per CTA (already in the [half][c][32] layout)
-    {
-        const float4 *src = reinterpret_cast<const float4 *>(cv_g);
-        float4 *dst = reinterpret_cast<float4 *>(smem + LUT_BYTES);
-#pragma unroll 4
-        for (int k = tid; k < CV_BYTES / 16; k += NT) dst[k] = __ldg(src + k);
-    }
-
     const FlatMap fm = flat_map(n_q, B, Hq, num_ctas);
     const int cta = blockIdx.x;
     int64_t pos = (int64_t)cta * fm.chunk;
     const int64_t end = min(pos + fm.chunk, fm.total);
     const int group = Hq / Hkv;
+    bool cv_ready = false;
+    uint32_t lut_phase = 0;
 
     while (pos < end) {
         int bh, t0, len;
@@ -172,85 +275,82 @@ __global__ void __launch_bounds__(NT, 1)
         const int n = (int)min((int64_t)(len - t0), end - pos);
         const int b = bh / Hq, hq = bh - b * Hq, hkv = hq / group;
 
+        const int64_t head_off = ((int64_t)b * Hkv + hkv) * ld_tok * M;
+        const uint8_t *kbase = codes_k + head_off + q4 * 16;
+        const uint8_t *vbase = codes_v + head_off + q4 * 16;
+        const int lo = t0, hi = t0 + n;           // token range of this segment
+        const int u0 = lo >> 4, u1 = (hi + 15) >> 4;  // 16-token units (absolute)
+
+        // code prefetch first: these loads fly while the LUT is built
+        Unit U0, U1;
+        U0.ka = U0.va = U0.kb = U0.vb = make_uint4(0, 0, 0, 0);
+        U1 = U0;
+        load_unit(U0, kbase, vbase, u0 + warp, slot, lo, hi);
+        load_unit(U1, kbase, vbase, u0 + warp + WARPS, slot, lo, hi);
+
         __syncthreads();  // previous segment's epilogue is done with lut_s
-        {
-            const float4 *src = reinterpret_cast<const float4 *>(lut_g + (int64_t)bh * KSUB * M);
-            float4 *dst = reinterpret_cast<float4 *>(smem);
-#pragma unroll 4
-            for (int k = tid; k < LUT_BYTES / 16; k += NT) dst[k] = __ldg(src + k);
+        if (kLutFromQ) {
+            // lut[c][i] = scale * (q[2i] C[c][i].x + q[2i+1] C[c][i].y); thread owns
+            // subspaces i0, i0+1 (i0 = 2*(tid & 31)) of centroids c = tid/32 + 16k
+            const float4 qq = __ldg(reinterpret_cast<const float4 *>(q_g + (int64_t)bh * D) +
+                                    (tid & 31));
+            const float4 *src = reinterpret_cast<const float4 *>(ck_g);
+            float4 cc[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                float2 o;
+                o.x = scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
+                o.y = scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
+                reinterpret_cast<float2 *>(lut_s)[tid + k * NT] = o;
+            }
+        } else if (tid == 0) {
+            mbar_expect_tx(bar_lut, LUT_BYTES);
+#pragma unroll
+            for (int c = 0; c < LUT_BYTES / 16384; ++c)
+                bulk_g2s(sbase + c * 16384,
+                         reinterpret_cast<const char *>(lut_g + (int64_t)bh * KSUB * M) + c * 16384,
+                         16384, bar_lut);
+        }
+        if (!kLutFromQ) {
+            mbar_wait(bar_lut, lut_phase);
+            lut_phase ^= 1u;
+        }
+        if (!cv_ready) {
+            mbar_wait(bar_cv, 0);
+            cv_ready = true;
         }
         __syncthreads();
 
-        const int64_t head_off = ((int64_t)b * Hkv + hkv) * ld_tok * M;
-        const uint8_t *kb = codes_k + head_off + (int64_t)t0 * M + q4 * 16;
-        const uint8_t *vb = codes_v + head_off + (int64_t)t0 * M + q4 * 16;
-        const int ngroups = (n + 7) >> 3;
-
-        float m = -INFINITY, l = 0.f;
-        unsigned long long acc[16];  // float2 per rotated subspace
+        SlotState S;
+        S.m = -INFINITY;
+        S.l = 0.f;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = 0ull;
+        for (int k = 0; k < 16; ++k) S.acc[k] = 0ull;
 
-        uint4 kr[PREFETCH + 1], vr[PREFETCH + 1];
-        bool ok[PREFETCH + 1];
-#pragma unroll
-        for (int s = 0; s <= PREFETCH; ++s) {
-            const int t = (warp + s * WARPS) * 8 + slot;
-            ok[s] = t < n;
-            kr[s] = ok[s] ? ld_stream(kb + (int64_t)t * M) : make_uint4(0, 0, 0, 0);
-            vr[s] = ok[s] ? ld_stream(vb + (int64_t)t * M) : make_uint4(0, 0, 0, 0);
-        }
-
-        for (int g = warp; g < ngroups; g += WARPS) {
-            const uint4 kc = kr[0], vc = vr[0];
-            const bool valid = ok[0];
-#pragma unroll
-            for (int s = 0; s < PREFETCH; ++s) {
-                kr[s] = kr[s + 1];
-                vr[s] = vr[s + 1];
-                ok[s] = ok[s + 1];
-            }
-            {
-                const int t = (g + (PREFETCH + 1) * WARPS) * 8 + slot;
-                ok[PREFETCH] = t < n;
-                kr[PREFETCH] = ok[PREFETCH] ? ld_stream(kb + (int64_t)t * M) : make_uint4(0, 0, 0, 0);
-                vr[PREFETCH] = ok[PREFETCH] ? ld_stream(vb + (int64_t)t * M) : make_uint4(0, 0, 0, 0);
-            }
-
-            uint32_t RK[4], RV[4];
-            rotate16(kc, r, RK);
-            rotate16(vc, r, RV);
-
-            float sp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t a = __byte_perm(RK[j >> 2], packK[j >> 1], sel_for(j));
-                sp[j & 3] += lds_lut(a);
-            }
-            float s = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-
-            if (valid) {
-                if (s > m) {
-                    const float f = fast_exp2((m - s) * kLog2e);
-                    l *= f;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) fmul2(acc[k], f);
-                    m = s;
-                }
-                const float p = fast_exp2((s - m) * kLog2e);
-                l += p;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t a = __byte_perm(RV[j >> 2], packV[j >> 1], sel_for(j));
-                    ffma2(acc[j], p, lds_cv(a));
-                }
-            }
+        // static 2-unit (32-token) register ring per warp: no register moves, a
+        // pending load is only waited for when its unit is processed
+        int u = u0 + warp;
+        while (true) {
+#define PQKV_STEP(UX)                                                                   \
+    if (u >= u1) break;                                                                 \
+    if ((u << 4) >= lo && (u << 4) + 16 <= hi) {                                        \
+        process_unit<false>(UX, S, packK, packV, true, true);                           \
+    } else {                                                                            \
+        const int ta = (u << 4) + slot;                                                 \
+        process_unit<true>(UX, S, packK, packV, ta >= lo && ta < hi,                    \
+                           ta + 8 >= lo && ta + 8 < hi);                                \
+    }                                                                                   \
+    load_unit(UX, kbase, vbase, u + 2 * WARPS, slot, lo, hi);                           \
+    u += WARPS;
+            PQKV_STEP(U0)
+            PQKV_STEP(U1)
+#undef PQKV_STEP
         }
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
-        float mw = m;
+        float mw = S.m;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
         if (lane == 0) red_m[warp] = mw;
@@ -258,16 +358,16 @@ __global__ void __launch_bounds__(NT, 1)
         float Mx = red_m[0];
 #pragma unroll
         for (int w = 1; w < WARPS; ++w) Mx = fmaxf(Mx, red_m[w]);
-        const float f = (m == -INFINITY) ? 0.f : fast_exp2((m - Mx) * kLog2e);
-        float lw = (q4 == 0) ? l * f : 0.f;
+        const float f = (S.m == -INFINITY) ? 0.f : fast_exp2((S.m - Mx) * kLog2e);
+        float lw = (q4 == 0) ? S.l * f : 0.f;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
         if (lane == 0) red_l[warp] = lw;
         float *rows = lut_s + (warp * 8 + slot) * D;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const int i = 16 * q4 + ((j + r) & 15);
-            const float2 a = unpack2(acc[j]);
+            const int i = 16 * q4 + ((j + r) & 15);  // decode layout: byte j <-> this subspace
+            const float2 a = unpack2(S.acc[j]);
             rows[2 * i] = a.x * f;
             rows[2 * i + 1] = a.y * f;
         }
@@ -295,6 +395,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         pos += n;
     }
+    if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight
 }
 }  // namespace fast
 
@@ -433,6 +534,13 @@ __device__ __forceinline__ void merge_into(float &m, float &l, float (&acc)[FMAX
     m = mm;
 }
 
+constexpr int DCH_MAX = 32;  // dense rows staged per chunk (fewer for wide heads)
+inline int dense_chunk(int d) { return std::max(1, std::min(DCH_MAX, 12000 / (2 * d))); }
+
+// One CTA per (b, hq).  Every global load of a phase is issued before any is
+// consumed (records in batches of 8, dense rows staged to shared memory with
+// coalesced 16-byte loads), so the kernel pays a few memory latencies, not one
+// per record / row.
 __global__ void __launch_bounds__(FT)
     decode_finish_kernel(const float *__restrict__ parts, int num_ctas, int B, int Hq, int Hkv,
                          int d, const int32_t *__restrict__ n_q, const float *__restrict__ q,
@@ -440,10 +548,11 @@ __global__ void __launch_bounds__(FT)
                          const float *__restrict__ recent_v, int64_t ld_recent,
                          const int32_t *__restrict__ n_recent, const float *__restrict__ k_cur,
                          const float *__restrict__ v_cur, float *__restrict__ out,
-                         float *__restrict__ lse, float *__restrict__ merged) {
-    extern __shared__ float sc[];  // dense scores, ld_recent + 1
-    __shared__ float dense_acc_dummy;
-    (void)dense_acc_dummy;
+                         float *__restrict__ lse, float *__restrict__ merged, int DCH) {
+    extern __shared__ float fsm[];
+    float *ks = fsm;             // [DCH][d]
+    float *vs = fsm + DCH * d;   // [DCH][d]
+    float *sc = vs + DCH * d;    // [DCH]
     const int bh = blockIdx.x;
     const int b = bh / Hq, hq = bh - b * Hq, hkv = hq / (Hq / Hkv);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -453,64 +562,113 @@ __global__ void __launch_bounds__(FT)
 #pragma unroll
     for (int k = 0; k < FMAXD / FT; ++k) acc[k] = 0.f;
 
-    // 1. quantized partials of this head, in CTA order (deterministic)
+    // 1. quantized partials of this head, merged in CTA order (deterministic)
     if (parts != nullptr && n_q != nullptr) {
         const FlatMap fm = flat_map(n_q, B, Hq, num_ctas);
         int len;
         const int64_t s0 = head_start(n_q, Hq, bh, &len);
         if (len > 0) {
             const int64_t c_first = s0 / fm.chunk, c_last = (s0 + len - 1) / fm.chunk;
-            for (int64_t c = c_first; c <= c_last; ++c) {
-                const float *rec = parts + (c + bh) * (int64_t)(d + kPS);
-                merge_into(m, l, acc, rec[0], rec[1], rec + kPS, d);
+            for (int64_t c0 = c_first; c0 <= c_last; c0 += 8) {
+                const int cnt = (int)min((int64_t)8, c_last - c0 + 1);
+                float rm[8], rl[8], ra[8][FMAXD / FT];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (k < cnt) {
+                        const float *rec = parts + (c0 + k + bh) * (int64_t)(d + kPS);
+                        rm[k] = rec[0];
+                        rl[k] = rec[1];
+#pragma unroll
+                        for (int e = 0; e < FMAXD / FT; ++e) {
+                            const int j = tid + e * FT;
+                            ra[k][e] = (j < d) ? rec[kPS + j] : 0.f;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (k >= cnt || rl[k] == 0.f) continue;
+                    if (l == 0.f) {
+                        m = rm[k];
+                        l = rl[k];
+#pragma unroll
+                        for (int e = 0; e < FMAXD / FT; ++e) acc[e] = ra[k][e];
+                        continue;
+                    }
+                    const float mm = fmaxf(m, rm[k]);
+                    const float wa = expf(m - mm), wb = expf(rm[k] - mm);
+                    l = l * wa + rl[k] * wb;
+#pragma unroll
+                    for (int e = 0; e < FMAXD / FT; ++e) acc[e] = acc[e] * wa + ra[k][e] * wb;
+                    m = mm;
+                }
             }
         }
     }
 
-    // 2. dense partial over recent rows [0, n_recent[b]) + current token
+    // 2. dense partial over recent rows [0, n_recent[b]) + the current token
     const int nr = (n_recent != nullptr && recent_k != nullptr) ? max(n_recent[b], 0) : 0;
     const int rows = nr + (k_cur != nullptr ? 1 : 0);
-    if (rows > 0) {
-        const float *qh = q + (int64_t)bh * d;
-        const int64_t rbase = ((int64_t)b * Hkv + hkv) * ld_recent * d;
-        for (int row = warp; row < rows; row += FT / 32) {
-            const float *kr = row < nr ? recent_k + rbase + (int64_t)row * d
-                                       : k_cur + ((int64_t)b * Hkv + hkv) * d;
+    const float *qh = q + (int64_t)bh * d;
+    const int64_t rbase = ((int64_t)b * Hkv + hkv) * ld_recent * d;
+    const int64_t cbase = ((int64_t)b * Hkv + hkv) * d;
+    const bool vec4 = (d % 4) == 0;
+    for (int r0 = 0; r0 < rows; r0 += DCH) {
+        const int cn = min(DCH, rows - r0);
+        __syncthreads();  // previous chunk fully consumed
+        if (vec4) {
+            const int d4 = d / 4;
+            for (int idx = tid; idx < cn * d4; idx += FT) {
+                const int rr = idx / d4, jj = idx - rr * d4, row = r0 + rr;
+                const float4 *kr = reinterpret_cast<const float4 *>(
+                    row < nr ? recent_k + rbase + (int64_t)row * d : k_cur + cbase);
+                const float4 *vr = reinterpret_cast<const float4 *>(
+                    row < nr ? recent_v + rbase + (int64_t)row * d : v_cur + cbase);
+                reinterpret_cast<float4 *>(ks)[rr * d4 + jj] = __ldg(kr + jj);
+                reinterpret_cast<float4 *>(vs)[rr * d4 + jj] = __ldg(vr + jj);
+            }
+        } else {
+            for (int idx = tid; idx < cn * d; idx += FT) {
+                const int rr = idx / d, jj = idx - rr * d, row = r0 + rr;
+                ks[idx] = row < nr ? recent_k[rbase + (int64_t)row * d + jj] : k_cur[cbase + jj];
+                vs[idx] = row < nr ? recent_v[rbase + (int64_t)row * d + jj] : v_cur[cbase + jj];
+            }
+        }
+        __syncthreads();
+        for (int rr = warp; rr < cn; rr += FT / 32) {
             float dot = 0.f;
-            for (int j = lane; j < d; j += 32) dot = fmaf(qh[j], kr[j], dot);
+            for (int j = lane; j < d; j += 32) dot = fmaf(__ldg(qh + j), ks[rr * d + j], dot);
+#pragma unroll
             for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-            if (lane == 0) sc[row] = scale * dot;
+            if (lane == 0) sc[rr] = scale * dot;
         }
         __syncthreads();
         float md = -INFINITY;
-        for (int row = 0; row < rows; ++row) md = fmaxf(md, sc[row]);
+        for (int rr = 0; rr < cn; ++rr) md = fmaxf(md, sc[rr]);
         float ld = 0.f;
         float dacc[FMAXD / FT];
 #pragma unroll
-        for (int k = 0; k < FMAXD / FT; ++k) dacc[k] = 0.f;
-        for (int row = 0; row < rows; ++row) {
-            const float p = expf(sc[row] - md);
+        for (int e = 0; e < FMAXD / FT; ++e) dacc[e] = 0.f;
+        for (int rr = 0; rr < cn; ++rr) {
+            const float p = expf(sc[rr] - md);
             ld += p;
-            const float *vr = row < nr ? recent_v + rbase + (int64_t)row * d
-                                       : v_cur + ((int64_t)b * Hkv + hkv) * d;
 #pragma unroll
-            for (int k = 0; k < FMAXD / FT; ++k) {
-                const int j = tid + k * FT;
-                if (j < d) dacc[k] = fmaf(p, vr[j], dacc[k]);
+            for (int e = 0; e < FMAXD / FT; ++e) {
+                const int j = tid + e * FT;
+                if (j < d) dacc[e] = fmaf(p, vs[rr * d + j], dacc[e]);
             }
         }
-        // merge the dense partial (register-resident) into (m, l, acc)
         if (l == 0.f) {
             m = md;
             l = ld;
 #pragma unroll
-            for (int k = 0; k < FMAXD / FT; ++k) acc[k] = dacc[k];
+            for (int e = 0; e < FMAXD / FT; ++e) acc[e] = dacc[e];
         } else {
             const float mm = fmaxf(m, md);
             const float wa = expf(m - mm), wb = expf(md - mm);
             l = l * wa + ld * wb;
 #pragma unroll
-            for (int k = 0; k < FMAXD / FT; ++k) acc[k] = acc[k] * wa + dacc[k] * wb;
+            for (int e = 0; e < FMAXD / FT; ++e) acc[e] = acc[e] * wa + dacc[e] * wb;
             m = mm;
         }
     }
@@ -598,43 +756,89 @@ extern "C" int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d) {
     return ((int64_t)num_ctas + (int64_t)B * Hq) * (int64_t)(d + kPS);
 }
 
-extern "C" int pqkv_decode_partials(const float *lut, int B, int Hq, int Hkv, const void *codes_k,
-                                    const void *codes_v, int64_t ld_tok, const int32_t *n_q,
-                                    const float *cb_v, int d, int M, int nbits, int num_ctas,
-                                    float *partials, void *stream) {
-    PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "pqkv_decode_partials: bad geometry");
+static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int M, int nbits,
+                             int num_ctas, int64_t ld_tok) {
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "%s: bad geometry", fn);
     PQKV_CHECK_ARG(B >= 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0,
-                   "pqkv_decode_partials: Hq must be a positive multiple of Hkv");
-    PQKV_CHECK_ARG(num_ctas > 0 && num_ctas <= (1 << 20), "pqkv_decode_partials: bad num_ctas");
-    PQKV_CHECK_ARG(ld_tok >= 0, "pqkv_decode_partials: bad ld_tok");
-    PQKV_CHECK_ARG(d <= GMAXD, "pqkv_decode_partials: d > %d unsupported", GMAXD);
-    if (B == 0) return PQKV_OK;
-    PQKV_CHECK_ARG(lut && codes_k && codes_v && n_q && cb_v && partials,
-                   "pqkv_decode_partials: null pointer");
-    cudaStream_t st = as_stream(stream);
-    if (is_fast_geometry(d, M, nbits)) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(fast::decode_partials_m64b8,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 fast::SMEM_BYTES);
-            if (e != cudaSuccess)
-                return fail(PQKV_ECUDA, "pqkv_decode_partials: %s", cudaGetErrorString(e));
-            attr_set = true;
-        }
-        fast::decode_partials_m64b8<<<num_ctas, fast::NT, fast::SMEM_BYTES, st>>>(
-            lut, B, Hq, Hkv, (const uint8_t *)codes_k, (const uint8_t *)codes_v, ld_tok, n_q, cb_v,
-            num_ctas, partials);
-    } else if (nbits <= 8) {
+                   "%s: Hq must be a positive multiple of Hkv", fn);
+    PQKV_CHECK_ARG(num_ctas > 0 && num_ctas <= (1 << 20), "%s: bad num_ctas", fn);
+    PQKV_CHECK_ARG(ld_tok >= 0, "%s: bad ld_tok", fn);
+    PQKV_CHECK_ARG(d <= GMAXD, "%s: d > %d unsupported", fn, GMAXD);
+    return PQKV_OK;
+}
+
+template <bool kLutFromQ>
+static int launch_fast(const float *q, float scale, const float *ck, const float *lut, int B,
+                       int Hq, int Hkv, const void *codes_k, const void *codes_v, int64_t ld_tok,
+                       const int32_t *n_q, const float *cb_v, int num_ctas, float *partials,
+                       cudaStream_t st) {
+    static bool attr_set = false;
+    auto kern = fast::decode_partials_m64b8<kLutFromQ>;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             fast::SMEM_BYTES);
+        if (e != cudaSuccess)
+            return fail(PQKV_ECUDA, "pqkv_decode_partials: %s", cudaGetErrorString(e));
+        attr_set = true;
+    }
+    kern<<<num_ctas, fast::NT, fast::SMEM_BYTES, st>>>(
+        q, scale, ck, lut, B, Hq, Hkv, (const uint8_t *)codes_k, (const uint8_t *)codes_v, ld_tok,
+        n_q, cb_v, num_ctas, partials);
+    return launch_status("pqkv_decode_partials");
+}
+
+static int launch_generic(const float *lut, int B, int Hq, int Hkv, const void *codes_k,
+                          const void *codes_v, int64_t ld_tok, const int32_t *n_q,
+                          const float *cb_v, int d, int M, int nbits, int num_ctas,
+                          float *partials, cudaStream_t st) {
+    if (nbits <= 8)
         decode_partials_generic<uint8_t><<<num_ctas, GT, 0, st>>>(
             lut, B, Hq, Hkv, (const uint8_t *)codes_k, (const uint8_t *)codes_v, ld_tok, n_q, cb_v,
             d, M, 1 << nbits, num_ctas, partials);
-    } else {
+    else
         decode_partials_generic<uint16_t><<<num_ctas, GT, 0, st>>>(
             lut, B, Hq, Hkv, (const uint16_t *)codes_k, (const uint16_t *)codes_v, ld_tok, n_q,
             cb_v, d, M, 1 << nbits, num_ctas, partials);
-    }
     return launch_status("pqkv_decode_partials");
+}
+
+extern "C" int pqkv_decode_partials(const float *q, float scale, const float *cb_k, float *lut_ws,
+                                    int B, int Hq, int Hkv, const void *codes_k,
+                                    const void *codes_v, int64_t ld_tok, const int32_t *n_q,
+                                    const float *cb_v, int d, int M, int nbits, int num_ctas,
+                                    float *partials, void *stream) {
+    int rc = check_decode_args("pqkv_decode_partials", B, Hq, Hkv, d, M, nbits, num_ctas, ld_tok);
+    if (rc) return rc;
+    if (B == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
+                   "pqkv_decode_partials: null pointer");
+    cudaStream_t st = as_stream(stream);
+    if (is_fast_geometry(d, M, nbits))
+        return launch_fast<true>(q, scale, cb_k, nullptr, B, Hq, Hkv, codes_k, codes_v, ld_tok,
+                                 n_q, cb_v, num_ctas, partials, st);
+    PQKV_CHECK_ARG(lut_ws != nullptr, "pqkv_decode_partials: this geometry needs lut_ws");
+    rc = pqkv_build_lut(q, (int64_t)B * Hq, d, cb_k, M, nbits, scale, lut_ws, stream);
+    if (rc) return rc;
+    return launch_generic(lut_ws, B, Hq, Hkv, codes_k, codes_v, ld_tok, n_q, cb_v, d, M, nbits,
+                          num_ctas, partials, st);
+}
+
+extern "C" int pqkv_decode_partials_lut(const float *lut, int B, int Hq, int Hkv,
+                                        const void *codes_k, const void *codes_v, int64_t ld_tok,
+                                        const int32_t *n_q, const float *cb_v, int d, int M,
+                                        int nbits, int num_ctas, float *partials, void *stream) {
+    int rc = check_decode_args("pqkv_decode_partials_lut", B, Hq, Hkv, d, M, nbits, num_ctas,
+                               ld_tok);
+    if (rc) return rc;
+    if (B == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(lut && codes_k && codes_v && n_q && cb_v && partials,
+                   "pqkv_decode_partials_lut: null pointer");
+    cudaStream_t st = as_stream(stream);
+    if (is_fast_geometry(d, M, nbits))
+        return launch_fast<false>(nullptr, 0.f, nullptr, lut, B, Hq, Hkv, codes_k, codes_v, ld_tok,
+                                  n_q, cb_v, num_ctas, partials, st);
+    return launch_generic(lut, B, Hq, Hkv, codes_k, codes_v, ld_tok, n_q, cb_v, d, M, nbits,
+                          num_ctas, partials, st);
 }
 
 extern "C" int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq, int Hkv,
@@ -655,10 +859,11 @@ extern "C" int pqkv_decode_finish(const float *partials, int num_ctas, int B, in
                    "pqkv_decode_finish: partials need n_q and num_ctas");
     PQKV_CHECK_ARG(q != nullptr || (k_cur == nullptr && recent_k == nullptr),
                    "pqkv_decode_finish: dense rows need q");
-    const size_t smem = sizeof(float) * (size_t)(ld_recent + 1);
+    const int dch = dense_chunk(d);
+    const size_t smem = sizeof(float) * (size_t)(2 * dch * d + dch);
     decode_finish_kernel<<<B * Hq, FT, smem, as_stream(stream)>>>(
         partials, num_ctas, B, Hq, Hkv, d, n_q, q, scale, recent_k, recent_v, ld_recent, n_recent,
-        k_cur, v_cur, out, lse, merged);
+        k_cur, v_cur, out, lse, merged, dch);
     return launch_status("pqkv_decode_finish");
 }
 

@@ -22,6 +22,14 @@
 namespace pqkv {
 namespace {
 
+// Destination cell of code (row v, subspace i): the reference row layout, or
+// (rot_base >= 0, m64b8 only) the decode layout in which each 16-byte quarter
+// of a row is stored rotated by its decode lane's constant (see common.cuh).
+__device__ __forceinline__ int64_t code_cell(int64_t v, int i, int64_t ld_codes, int64_t rot_base) {
+    if (rot_base < 0) return v * ld_codes + i;
+    return v * ld_codes + decode_layout_pos(i, (int)((rot_base + v) & 7));
+}
+
 template <typename TX>
 __device__ __forceinline__ double load_x(const TX *p);
 template <>
@@ -66,7 +74,7 @@ template <typename TX, typename CT, int DSUB>
 __global__ void __launch_bounds__(256) encode_staged(const TX *__restrict__ x, int64_t n,
                                                      int64_t ld_x, const float *__restrict__ cents,
                                                      int ksub, CT *__restrict__ codes,
-                                                     int64_t ld_codes) {
+                                                     int64_t ld_codes, int64_t rot_base) {
     extern __shared__ double sm[];
     double *c_s = sm;                      // [ksub][DSUB]
     double *cc_s = sm + (size_t)ksub * DSUB;  // [ksub]
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(256) encode_staged(const TX *__restrict__ x, i
             arg = c;
         }
     }
-    codes[v * ld_codes + i] = (CT)arg;
+    codes[code_cell(v, i, ld_codes, rot_base)] = (CT)arg;
 }
 
 // Any dsub: operands read from global memory (L1-resident per subspace).
@@ -110,7 +118,7 @@ template <typename TX, typename CT>
 __global__ void __launch_bounds__(256) encode_generic(const TX *__restrict__ x, int64_t n,
                                                       int64_t ld_x, const float *__restrict__ cents,
                                                       int ksub, int dsub, CT *__restrict__ codes,
-                                                      int64_t ld_codes) {
+                                                      int64_t ld_codes, int64_t rot_base) {
     const int i = blockIdx.y;
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
@@ -140,12 +148,12 @@ __global__ void __launch_bounds__(256) encode_generic(const TX *__restrict__ x, 
             arg = c;
         }
     }
-    codes[v * ld_codes + i] = (CT)arg;
+    codes[code_cell(v, i, ld_codes, rot_base)] = (CT)arg;
 }
 
 template <typename TX, typename CT, int DSUB>
 int launch_staged(const void *x, int64_t n, int64_t ld_x, const float *cents, int M, int ksub,
-                  void *codes, int64_t ld_codes, cudaStream_t st) {
+                  void *codes, int64_t ld_codes, int64_t rot_base, cudaStream_t st) {
     const size_t smem = (size_t)ksub * (DSUB + 1) * sizeof(double);
     auto k = encode_staged<TX, CT, DSUB>;
     if (smem > 48 * 1024) {
@@ -154,37 +162,40 @@ int launch_staged(const void *x, int64_t n, int64_t ld_x, const float *cents, in
         if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
     }
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)M);
-    k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes);
+    k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes,
+                               rot_base);
     return launch_status("pqkv_encode");
 }
 
 template <typename TX, typename CT>
 int dispatch_encode(const void *x, int64_t n, int d, int64_t ld_x, const float *cents, int M,
-                    int nbits, void *codes, int64_t ld_codes, cudaStream_t st) {
+                    int nbits, void *codes, int64_t ld_codes, int64_t rot_base, cudaStream_t st) {
     const int ksub = 1 << nbits, dsub = d / M;
     const size_t staged_smem = (size_t)ksub * (dsub + 1) * sizeof(double);
     if (staged_smem <= 160 * 1024) {
         switch (dsub) {
-            case 1: return launch_staged<TX, CT, 1>(x, n, ld_x, cents, M, ksub, codes, ld_codes, st);
-            case 2: return launch_staged<TX, CT, 2>(x, n, ld_x, cents, M, ksub, codes, ld_codes, st);
-            case 4: return launch_staged<TX, CT, 4>(x, n, ld_x, cents, M, ksub, codes, ld_codes, st);
-            case 8: return launch_staged<TX, CT, 8>(x, n, ld_x, cents, M, ksub, codes, ld_codes, st);
-            case 16: return launch_staged<TX, CT, 16>(x, n, ld_x, cents, M, ksub, codes, ld_codes, st);
+            case 1: return launch_staged<TX, CT, 1>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
+            case 2: return launch_staged<TX, CT, 2>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
+            case 4: return launch_staged<TX, CT, 4>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
+            case 8: return launch_staged<TX, CT, 8>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
+            case 16: return launch_staged<TX, CT, 16>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
             default: break;
         }
     }
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)M);
     encode_generic<TX, CT><<<grid, 256, 0, st>>>((const TX *)x, n, ld_x, cents, ksub, dsub,
-                                                  (CT *)codes, ld_codes);
+                                                  (CT *)codes, ld_codes, rot_base);
     return launch_status("pqkv_encode");
 }
 
 template <typename TX>
 int dispatch_cell(const void *x, int64_t n, int d, int64_t ld_x, const float *cents, int M,
-                  int nbits, void *codes, int64_t ld_codes, cudaStream_t st) {
+                  int nbits, void *codes, int64_t ld_codes, int64_t rot_base, cudaStream_t st) {
     if (nbits <= 8)
-        return dispatch_encode<TX, uint8_t>(x, n, d, ld_x, cents, M, nbits, codes, ld_codes, st);
-    return dispatch_encode<TX, uint16_t>(x, n, d, ld_x, cents, M, nbits, codes, ld_codes, st);
+        return dispatch_encode<TX, uint8_t>(x, n, d, ld_x, cents, M, nbits, codes, ld_codes,
+                                            rot_base, st);
+    return dispatch_encode<TX, uint16_t>(x, n, d, ld_x, cents, M, nbits, codes, ld_codes,
+                                         rot_base, st);
 }
 
 }  // namespace
@@ -194,7 +205,7 @@ using namespace pqkv;
 
 extern "C" int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
                            const float *centroids, int M, int nbits, void *codes,
-                           int64_t ld_codes, void *stream) {
+                           int64_t ld_codes, int64_t rot_base, void *stream) {
     PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "pqkv_encode: bad geometry d=%d M=%d nbits=%d", d,
                    M, nbits);
     PQKV_CHECK_ARG(n >= 0, "pqkv_encode: n must be >= 0");
@@ -202,15 +213,19 @@ extern "C" int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t
     if (n == 0) return PQKV_OK;
     PQKV_CHECK_ARG(x && centroids && codes, "pqkv_encode: null pointer");
     PQKV_CHECK_ARG(n <= (int64_t)65535 * 256 * 1024, "pqkv_encode: n too large");
+    PQKV_CHECK_ARG(rot_base < 0 || is_fast_geometry(d, M, nbits),
+                   "pqkv_encode: the decode layout exists only for m64b8 (d=128, M=64, nbits=8)");
     cudaStream_t st = as_stream(stream);
     switch (x_dtype) {
         case PQKV_DTYPE_F32:
-            return dispatch_cell<float>(x, n, d, ld_x, centroids, M, nbits, codes, ld_codes, st);
+            return dispatch_cell<float>(x, n, d, ld_x, centroids, M, nbits, codes, ld_codes,
+                                        rot_base, st);
         case PQKV_DTYPE_BF16:
             return dispatch_cell<__nv_bfloat16>(x, n, d, ld_x, centroids, M, nbits, codes,
-                                                ld_codes, st);
+                                                ld_codes, rot_base, st);
         case PQKV_DTYPE_F16:
-            return dispatch_cell<__half>(x, n, d, ld_x, centroids, M, nbits, codes, ld_codes, st);
+            return dispatch_cell<__half>(x, n, d, ld_x, centroids, M, nbits, codes, ld_codes,
+                                         rot_base, st);
         default:
             return fail(PQKV_EINVAL, "pqkv_encode: unknown dtype %d", x_dtype);
     }

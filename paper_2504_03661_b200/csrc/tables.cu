@@ -56,6 +56,29 @@ __global__ void prepare_cv_kernel(const float2 *__restrict__ cb_v, float2 *__res
     out[((i >> 5) * 256 + c) * 32 + (i & 31)] = cb_v[idx];
 }
 
+// Key codebook -> centroid-major [c][i] float2 for the in-kernel LUT build.
+__global__ void prepare_ck_kernel(const float2 *__restrict__ cb_k, float2 *__restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over (i, c)
+    if (idx >= 64 * 256) return;
+    const int i = idx >> 8, c = idx & 255;
+    out[c * 64 + i] = cb_k[idx];
+}
+
+// Reference row layout <-> m64b8 decode layout (common.cuh), one byte per thread.
+__global__ void relayout_kernel(const uint8_t *__restrict__ src, int64_t ld_src,
+                                uint8_t *__restrict__ dst, int64_t ld_dst, int64_t n,
+                                int64_t t_first, int to_decode) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * 64) return;
+    const int64_t v = idx >> 6;
+    const int i = (int)(idx & 63);
+    const int pos = decode_layout_pos(i, (int)((t_first + v) & 7));
+    if (to_decode)
+        dst[v * ld_dst + pos] = src[v * ld_src + i];
+    else
+        dst[v * ld_dst + i] = src[v * ld_src + pos];
+}
+
 template <typename CT>
 __global__ void reconstruct_kernel(const CT *__restrict__ codes, int64_t n, int64_t ld_codes,
                                    const float *__restrict__ cents, int d, int M, int ksub,
@@ -118,6 +141,29 @@ extern "C" int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int 
     PQKV_CHECK_ARG(cb_v && out, "pqkv_prepare_value_codebook: null pointer");
     prepare_cv_kernel<<<64, 256, 0, as_stream(stream)>>>((const float2 *)cb_v, (float2 *)out);
     return launch_status("pqkv_prepare_value_codebook");
+}
+
+extern "C" int pqkv_prepare_key_codebook(const float *cb_k, int d, int M, int nbits, float *out,
+                                         void *stream) {
+    PQKV_CHECK_ARG(is_fast_geometry(d, M, nbits),
+                   "pqkv_prepare_key_codebook: only the m64b8 (d=128) geometry is re-laid out");
+    PQKV_CHECK_ARG(cb_k && out, "pqkv_prepare_key_codebook: null pointer");
+    prepare_ck_kernel<<<64, 256, 0, as_stream(stream)>>>((const float2 *)cb_k, (float2 *)out);
+    return launch_status("pqkv_prepare_key_codebook");
+}
+
+extern "C" int pqkv_relayout_codes(const void *src, int64_t ld_src, void *dst, int64_t ld_dst,
+                                   int64_t n, int64_t t_first, int to_decode, int d, int M,
+                                   int nbits, void *stream) {
+    PQKV_CHECK_ARG(is_fast_geometry(d, M, nbits),
+                   "pqkv_relayout_codes: the decode layout exists only for m64b8");
+    PQKV_CHECK_ARG(n >= 0 && t_first >= 0 && ld_src >= M && ld_dst >= M,
+                   "pqkv_relayout_codes: bad sizes");
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(src && dst && src != dst, "pqkv_relayout_codes: null or aliased pointers");
+    relayout_kernel<<<(unsigned)((n * 64 + 255) / 256), 256, 0, as_stream(stream)>>>(
+        (const uint8_t *)src, ld_src, (uint8_t *)dst, ld_dst, n, t_first, to_decode);
+    return launch_status("pqkv_relayout_codes");
 }
 
 extern "C" int pqkv_reconstruct(const void *codes, int64_t n, int64_t ld_codes,

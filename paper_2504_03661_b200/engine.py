@@ -3,21 +3,22 @@
 The reference decodes one head of one sequence per call (attention.py:214,
 a per-head Python loop in harness.py:195-201).  Here one call covers a whole
 layer: every sequence b < B and query head hq < Hq, with GQA (query head hq
-reads KV head hq // (Hq // Hkv)).  Three launches per layer:
+reads KV head hq // (Hq // Hkv)).  Two launches per layer:
 
-1. ``pqkv_build_lut``        B*Hq key tables (build_key_lut, attention.py:70-83)
-2. ``pqkv_decode_partials``  one persistent CTA per SM streams the codes of all
+1. ``pqkv_decode_partials``  one persistent CTA per SM builds each head's key
+                             LUT in shared memory (build_key_lut,
+                             attention.py:70-83) and streams the codes of all
                              heads (quantized_partial, attention.py:114-166)
-3. ``pqkv_decode_finish``    per head: fixed-order merge of the split partials,
+2. ``pqkv_decode_finish``    per head: fixed-order merge of the split partials,
                              dense partial over recent rows + current token,
                              finalize (attention.py:169-211, 264-274)
 
-All three run on one stream with device-resident lengths, so a whole decode
+Both run on one stream with device-resident lengths, so a whole decode
 step (all layers) can be captured in a CUDA graph and replayed.
 
 Multi-GPU: head/batch sharding needs no collective -- each
 rank runs ``PQDecoder`` on its own heads.  A sequence split (128K context)
-runs the same three launches on each rank's token range with
+runs the same launches on each rank's token range with
 ``merged=`` records instead of a finalized output, all-gathers the
 (d + 4)-float records and merges them in rank order
 (``sequence_parallel_decode``), the cross-GPU form of merge_partials.
@@ -50,11 +51,12 @@ class PQDecoder:
     def num_ctas(self) -> int:
         return self.ws.num_ctas
 
-    def __call__(self, q, codes_k, codes_v, n_q, cb_k, cb_v_layout, recent_k=None,
+    def __call__(self, q, codes_k, codes_v, n_q, cb_k_layout, cb_v_layout, recent_k=None,
                  recent_v=None, n_recent=None, k_cur=None, v_cur=None, out=None, lse=None,
                  merged=None, scale: float | None = None, stream=None, finalize: bool = True):
         """q (B, Hq, d) f32; codes (B, Hkv, cap, M); n_q (B,) int32 device;
-        cb_k (M, ksub, dsub) f32 device; cb_v_layout from value_codebook_layout;
+        cb_k_layout / cb_v_layout from kernels.key/value_codebook_layout (or
+        Codebook.device_key_layout / device_value_layout);
         recent (B, Hkv, R, d) f32 + n_recent (B,) int32; k_cur/v_cur (B, Hkv, d).
         Returns out (B, Hq, d) f32 (or only fills lse / merged)."""
         cfg = self.config
@@ -65,15 +67,15 @@ class PQDecoder:
         qf = q if (q.dtype == torch.float32 and q.is_contiguous()) else q.float().contiguous()
         if out is None and finalize:
             out = torch.empty((B, Hq, d), dtype=torch.float32, device=q.device)
-        K.build_lut(qf.view(B * Hq, d), cb_k, cfg.nbits, sc, out=self.ws.lut, stream=stream)
-        K.decode_partials(self.ws, self.Hkv, codes_k, codes_v, n_q, cb_v_layout, stream=stream)
+        K.decode_partials(self.ws, self.Hkv, qf.view(B * Hq, d), sc, cb_k_layout, codes_k,
+                          codes_v, n_q, cb_v_layout, stream=stream)
         K.decode_finish(self.ws, self.Hkv, n_q, qf, sc, recent_k=recent_k, recent_v=recent_v,
                         n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
                         merged=merged, stream=stream)
         return out
 
 
-def sequence_parallel_decode(decoder: PQDecoder, group, q, codes_k, codes_v, n_q, cb_k,
+def sequence_parallel_decode(decoder: PQDecoder, group, q, codes_k, codes_v, n_q, cb_k_layout,
                              cb_v_layout, recent_k=None, recent_v=None, n_recent=None,
                              k_cur=None, v_cur=None, scale: float | None = None, out=None):
     """Context-parallel decode: this rank holds a contiguous token range of
@@ -85,7 +87,7 @@ def sequence_parallel_decode(decoder: PQDecoder, group, q, codes_k, codes_v, n_q
 
     B, Hq, d = decoder.B, decoder.Hq, decoder.config.d
     rec = torch.empty((B * Hq, d + 4), dtype=torch.float32, device=q.device)
-    decoder(q, codes_k, codes_v, n_q, cb_k, cb_v_layout, recent_k, recent_v, n_recent, k_cur,
+    decoder(q, codes_k, codes_v, n_q, cb_k_layout, cb_v_layout, recent_k, recent_v, n_recent, k_cur,
             v_cur, merged=rec, scale=scale, finalize=False)
     gathered = gather_partials(rec, group)
     if out is None:

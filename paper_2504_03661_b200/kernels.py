@@ -31,8 +31,11 @@ def code_dtype(nbits: int) -> torch.dtype:
 
 
 def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tensor | None = None,
-           stream=None) -> torch.Tensor:
-    """Nearest-centroid codes of x (n, d) -> (n, M); bit-exact with assign_codes."""
+           stream=None, layout: str = "rows", t_first: int = 0) -> torch.Tensor:
+    """Nearest-centroid codes of x (n, d) -> (n, M); bit-exact with assign_codes.
+
+    layout="rows" is the reference CodesMatrix order; layout="decode" (m64b8)
+    writes the decode kernel's layout with row 0 at token index t_first."""
     _dev_check(x, centroids)
     M, ksub, dsub = centroids.shape
     d = M * dsub
@@ -48,8 +51,37 @@ def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tens
     if out.shape[0] != n or out.shape[1] != M or out.stride(1) != 1:
         raise ValueError("codes output must be (n, M) with unit column stride")
     cents = _contig(centroids.float())
+    rot = _rot_base(layout, t_first)
     N.call("pqkv_encode", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0), N.ptr(cents), M,
-           nbits, N.ptr(out), out.stride(0), N.stream_ptr(stream))
+           nbits, N.ptr(out), out.stride(0), rot, N.stream_ptr(stream))
+    return out
+
+
+def _rot_base(layout: str, t_first: int) -> int:
+    if layout == "rows":
+        return -1
+    if layout == "decode":
+        if t_first < 0:
+            raise ValueError("t_first must be >= 0")
+        return int(t_first)
+    raise ValueError(f"unknown code layout {layout!r}")
+
+
+def relayout(codes: torch.Tensor, to_decode: bool, t_first: int = 0, out=None, stream=None):
+    """Rows <-> decode layout of an (..., n, 64) uint8 m64b8 code buffer; row
+    index counts from t_first along the token axis (dim -2)."""
+    _dev_check(codes)
+    if codes.shape[-1] != 64 or codes.dtype != torch.uint8:
+        raise ValueError("the decode layout exists only for m64b8 uint8 codes")
+    src = codes.contiguous()
+    out = torch.empty_like(src) if out is None else out
+    lead = src.numel() // (src.shape[-2] * 64) if src.numel() else 0
+    n = src.shape[-2]
+    s2 = src.view(lead, n, 64) if lead else src
+    o2 = out.view(lead, n, 64) if lead else out
+    for h in range(lead):
+        N.call("pqkv_relayout_codes", N.ptr(s2[h]), 64, N.ptr(o2[h]), 64, n, t_first,
+               1 if to_decode else 0, 128, 64, 8, N.stream_ptr(stream))
     return out
 
 
@@ -83,6 +115,18 @@ def is_fast_geometry(d: int, M: int, nbits: int) -> bool:
     return d == 128 and M == 64 and nbits == 8
 
 
+def key_codebook_layout(cb_k: torch.Tensor, nbits: int, stream=None) -> torch.Tensor:
+    """The key codebook as the decode kernel reads it (centroid-major for m64b8)."""
+    M, ksub, dsub = cb_k.shape
+    cb_k = _contig(cb_k.float())
+    if not is_fast_geometry(M * dsub, M, nbits):
+        return cb_k
+    out = torch.empty(M * ksub * dsub, dtype=torch.float32, device=cb_k.device)
+    N.call("pqkv_prepare_key_codebook", N.ptr(cb_k), M * dsub, M, nbits, N.ptr(out),
+           N.stream_ptr(stream))
+    return out
+
+
 def value_codebook_layout(cb_v: torch.Tensor, nbits: int, stream=None) -> torch.Tensor:
     """The value codebook as the decode kernel reads it (re-laid out for m64b8)."""
     M, ksub, dsub = cb_v.shape
@@ -106,27 +150,45 @@ class DecodeWorkspace:
         with torch.cuda.device(self.device):
             self.num_ctas = num_ctas or N.decode_grid(d, M, nbits)
         nf = N.partials_floats(self.num_ctas, B, Hq, d)
-        self.lut = torch.empty((B * Hq, self.ksub, M), dtype=torch.float32, device=self.device)
         self.partials = torch.empty(nf, dtype=torch.float32, device=self.device)
+        # the fast path builds its tables in shared memory; other geometries
+        # need a global LUT scratch
+        self.lut = None if is_fast_geometry(d, M, nbits) else torch.empty(
+            (B * Hq, self.ksub, M), dtype=torch.float32, device=self.device)
 
 
-def decode_partials(ws: DecodeWorkspace, Hkv: int, codes_k, codes_v, n_q, cb_v_layout,
-                    stream=None) -> None:
-    """Fused LUT-score / online-softmax / value accumulation over the quantized span.
-
-    codes_k/codes_v: (B, Hkv, cap, M) cells; n_q: (B,) int32 device tensor.
-    Uses ws.lut (filled by build_lut) and writes ws.partials.
-    """
+def _check_codes(ws: DecodeWorkspace, Hkv: int, codes_k, codes_v):
     B, Hq = ws.B, ws.Hq
-    if codes_k.shape != codes_v.shape or codes_k.dim() != 4 or codes_k.shape[:2] != (B, Hkv):
+    if codes_k.shape != codes_v.shape or codes_k.dim() != 4 or tuple(codes_k.shape[:2]) != (B, Hkv):
         raise ValueError("codes must be (B, Hkv, cap, M) and K/V shapes must agree")
     if codes_k.shape[3] != ws.M or not codes_k.is_contiguous() or not codes_v.is_contiguous():
         raise ValueError("codes must be contiguous (B, Hkv, cap, M)")
     if Hq % Hkv:
         raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
-    N.call("pqkv_decode_partials", N.ptr(ws.lut), B, Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v),
-           codes_k.shape[2], N.ptr(n_q), N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, ws.num_ctas,
-           N.ptr(ws.partials), N.stream_ptr(stream))
+
+
+def decode_partials(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout, codes_k,
+                    codes_v, n_q, cb_v_layout, stream=None) -> None:
+    """Fused LUT build / score / online softmax / value accumulation over the
+    quantized span of every (b, hq).  q: (B*Hq, d) float32; codes (B, Hkv, cap,
+    M); n_q (B,) int32 device; codebooks from key/value_codebook_layout."""
+    _check_codes(ws, Hkv, codes_k, codes_v)
+    N.call("pqkv_decode_partials", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
+           ws.B, ws.Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q),
+           N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, ws.num_ctas, N.ptr(ws.partials),
+           N.stream_ptr(stream))
+
+
+def decode_partials_lut(ws: DecodeWorkspace, Hkv: int, lut, codes_k, codes_v, n_q, cb_v_layout,
+                        stream=None) -> None:
+    """Same from precomputed tables lut (B*Hq, ksub, M) (the Lut-taking API)."""
+    _check_codes(ws, Hkv, codes_k, codes_v)
+    lut = _contig(lut)
+    if tuple(lut.shape) != (ws.B * ws.Hq, ws.ksub, ws.M):
+        raise ValueError("lut must be (B*Hq, ksub, M)")
+    N.call("pqkv_decode_partials_lut", N.ptr(lut), ws.B, ws.Hq, Hkv, N.ptr(codes_k),
+           N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q), N.ptr(cb_v_layout), ws.d, ws.M,
+           ws.nbits, ws.num_ctas, N.ptr(ws.partials), N.stream_ptr(stream))
 
 
 def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, recent_k=None,

@@ -64,6 +64,10 @@ class LayerKVCache:
         self.recent_capacity = recent_capacity
         self.flush_threshold = flush_threshold
         self.worker = worker
+        # m64b8 stores codes in the decode kernel's layout (include/pqkv_sm100.h);
+        # snapshots convert back to the reference row layout
+        self._layout = "decode" if K.is_fast_geometry(cb_K.config.d, cb_K.config.M,
+                                                      cb_K.config.nbits) else "rows"
         self.device = torch.device(device) if device is not None else default_device()
         cfg = self.config
         cap = 1024
@@ -162,9 +166,11 @@ class LayerKVCache:
                 self._wait_pending()
                 self._ensure_store(self._n_q + n_enc)
                 K.encode(Kt[:n_enc].contiguous(), self.cb_K.device_centroids(self.device),
-                         self.config.nbits, out=self._store_k[self._n_q: self._n_q + n_enc])
+                         self.config.nbits, out=self._store_k[self._n_q: self._n_q + n_enc],
+                         layout=self._layout, t_first=self._n_q)
                 K.encode(Vt[:n_enc].contiguous(), self.cb_V.device_centroids(self.device),
-                         self.config.nbits, out=self._store_v[self._n_q: self._n_q + n_enc])
+                         self.config.nbits, out=self._store_v[self._n_q: self._n_q + n_enc],
+                         layout=self._layout, t_first=self._n_q)
             if keep:
                 self._ensure_recent(keep)
                 a = self._r0 + self._rlen
@@ -243,8 +249,8 @@ class LayerKVCache:
         out_k = self._store_k[n0: n0 + batch]
         out_v = self._store_v[n0: n0 + batch]
         if not asynchronous:
-            K.encode(rows_k, cents_k, nb, out=out_k)
-            K.encode(rows_v, cents_v, nb, out=out_v)
+            K.encode(rows_k, cents_k, nb, out=out_k, layout=self._layout, t_first=n0)
+            K.encode(rows_v, cents_v, nb, out=out_v, layout=self._layout, t_first=n0)
             self._n_q += batch          # single publication point
             self._r0 += batch
             self._rlen -= batch
@@ -252,8 +258,10 @@ class LayerKVCache:
         main = torch.cuda.current_stream(self.device)
         self._side.wait_stream(main)    # the rows were written on the main stream
         with torch.cuda.stream(self._side):
-            K.encode(rows_k, cents_k, nb, out=out_k, stream=self._side)
-            K.encode(rows_v, cents_v, nb, out=out_v, stream=self._side)
+            K.encode(rows_k, cents_k, nb, out=out_k, stream=self._side, layout=self._layout,
+                     t_first=n0)
+            K.encode(rows_v, cents_v, nb, out=out_v, stream=self._side, layout=self._layout,
+                     t_first=n0)
             ev = torch.cuda.Event()
             ev.record(self._side)
         for t in (rows_k, rows_v, out_k, out_v):
@@ -293,8 +301,12 @@ class LayerKVCache:
             n = snap.codes_K.n_tokens
             self._ensure_store(n)
             if n:
-                self._store_k[:n] = snap.codes_K.device_codes(self.device)
-                self._store_v[:n] = snap.codes_V.device_codes(self.device)
+                ck = snap.codes_K.device_codes(self.device)
+                cv = snap.codes_V.device_codes(self.device)
+                if self._layout == "decode":
+                    ck, cv = K.relayout(ck, True), K.relayout(cv, True)
+                self._store_k[:n] = ck
+                self._store_v[:n] = cv
             self._n_q = n
             r = int(snap.recent_K.shape[0])
             if r:
@@ -305,17 +317,29 @@ class LayerKVCache:
             self._n_total = snap.n_total
 
     # -- reads -------------------------------------------------------------------
-    def snapshot(self) -> CacheSnapshot:
-        """Consistent view covering every stored token exactly once."""
+    def raw_snapshot(self):
+        """(codes_k, codes_v, recent_K, recent_V, n_q, n_total) with the code
+        store in its on-device layout ("decode" for m64b8) -- what decode_step
+        hands to the kernel without a layout round trip."""
         with self._lock:
             self._publish_completed()
             n_q = self._n_q
             rk = self._rk[self._r0: self._r0 + self._rlen].clone()
             rv = self._rv[self._r0: self._r0 + self._rlen].clone()
-            n_total = self._n_total
-            sk, sv = self._store_k, self._store_v
-        return CacheSnapshot(codes_K=CodesMatrix(codes=sk[:n_q], nbits=self.config.nbits),
-                             codes_V=CodesMatrix(codes=sv[:n_q], nbits=self.config.nbits),
+            return (self._store_k[:n_q], self._store_v[:n_q], rk, rv, n_q, self._n_total)
+
+    @property
+    def code_layout(self) -> str:
+        return self._layout
+
+    def snapshot(self) -> CacheSnapshot:
+        """Consistent view covering every stored token exactly once (codes in
+        the reference row layout)."""
+        ck, cv, rk, rv, n_q, n_total = self.raw_snapshot()
+        if self._layout == "decode" and n_q:
+            ck, cv = K.relayout(ck, False), K.relayout(cv, False)
+        return CacheSnapshot(codes_K=CodesMatrix(codes=ck, nbits=self.config.nbits),
+                             codes_V=CodesMatrix(codes=cv, nbits=self.config.nbits),
                              recent_K=rk, recent_V=rv, n_q=n_q, n_total=n_total)
 
     def memory_usage(self) -> dict[str, int]:

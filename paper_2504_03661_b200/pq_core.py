@@ -128,6 +128,14 @@ class Codebook:
             self._dev[key] = to_device(self.centroids, torch.float32, dev).contiguous()
         return self._dev[key]
 
+    def device_key_layout(self, device=None) -> torch.Tensor:
+        """Key codebook as the decode kernel reads it (pqkv_prepare_key_codebook)."""
+        dev = torch.device(device) if device is not None else default_device()
+        key = ("k", str(dev))
+        if key not in self._dev:
+            self._dev[key] = K.key_codebook_layout(self.device_centroids(dev), self.config.nbits)
+        return self._dev[key]
+
     def device_value_layout(self, device=None) -> torch.Tensor:
         """Value codebook as the decode kernel reads it (pqkv_prepare_value_codebook)."""
         dev = torch.device(device) if device is not None else default_device()

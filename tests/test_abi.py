@@ -46,18 +46,20 @@ def test_bad_arguments_fail_before_cuda(lib):
     from paper_2504_03661_b200 import _native as N
     assert lib.pqkv_version() == 1
     # d not divisible by M -> EINVAL with a message, no CUDA call needed
-    rc = lib.pqkv_encode(None, 0, 10, 130, 130, None, 64, 8, None, 64, None)
+    rc = lib.pqkv_encode(None, 0, 10, 130, 130, None, 64, 8, None, 64, -1, None)
     assert rc == N.PQKV_EINVAL
     assert b"geometry" in lib.pqkv_last_error()
-    rc = lib.pqkv_decode_partials(None, 1, 6, 4, None, None, 0, None, None, 128, 64, 8, 1,
-                                  None, None)
+    rc = lib.pqkv_decode_partials(None, 0.1, None, None, 1, 6, 4, None, None, 0, None, None,
+                                  128, 64, 8, 1, None, None)
     assert rc == N.PQKV_EINVAL and b"multiple" in lib.pqkv_last_error()
     rc = lib.pqkv_prepare_value_codebook(None, 128, 32, 8, None, None)
     assert rc == N.PQKV_EINVAL
     with pytest.raises(ValueError):
         N.check(N.PQKV_EINVAL, "x")
     # n == 0 is a no-op success
-    assert lib.pqkv_encode(None, 0, 0, 128, 128, None, 64, 8, None, 64, None) == 0
+    assert lib.pqkv_encode(None, 0, 0, 128, 128, None, 64, 8, None, 64, -1, None) == 0
+    # the decode layout exists only for m64b8
+    assert lib.pqkv_encode(None, 0, 5, 64, 64, None, 32, 8, None, 32, 0, None) == N.PQKV_EINVAL
 
 
 def test_partials_size(lib):

@@ -99,6 +99,22 @@ def test_encode_strided_output_rows():
     assert (s[:50] == 7).all() and (s[150:] == 7).all()
 
 
+@pytest.mark.parametrize("t_first", [0, 3, 1000])
+def test_encode_decode_layout_is_relayout_of_rows(t_first):
+    """The decode layout written by the encoder == relayout(row layout), and
+    relayout round-trips."""
+    from paper_2504_03661_b200 import kernels as K
+    rng = np.random.default_rng(9)
+    cents = torch.from_numpy(rng.standard_normal((64, 256, 2)).astype(np.float32)).cuda()
+    X = torch.from_numpy(rng.standard_normal((333, 128)).astype(np.float32)).cuda()
+    rows = K.encode(X, cents, 8)
+    dec = K.encode(X, cents, 8, layout="decode", t_first=t_first)
+    assert torch.equal(dec, K.relayout(rows, True, t_first=t_first))
+    assert torch.equal(K.relayout(dec, False, t_first=t_first), rows)
+    if t_first % 8:
+        assert not torch.equal(dec, K.relayout(rows, True, t_first=0))
+
+
 def test_reconstruct_matches_oracle():
     import paper_2504_03661_b200 as P
     rng = np.random.default_rng(8)
@@ -234,9 +250,10 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None):
     dev = torch.device("cuda")
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     dec = PQDecoder(B, Hq, Hkv, cfg, num_ctas=num_ctas)
-    cbk = t(cents_k)
+    cbk = K.key_codebook_layout(t(cents_k), 8)
     cbv = K.value_codebook_layout(t(cents_v), 8)
-    out = dec(t(q), t(codes_k), t(codes_v), t(np.array(n_q, np.int32)), cbk, cbv, t(rk), t(rv),
+    dk, dv = K.relayout(t(codes_k), True), K.relayout(t(codes_v), True)  # decode layout
+    out = dec(t(q), dk, dv, t(np.array(n_q, np.int32)), cbk, cbv, t(rk), t(rv),
               t(np.array(n_r, np.int32)), t(kc), t(vc))
     want = _oracle_heads(q, codes_k, codes_v, n_q, rk, rv, n_r, kc, vc, cents_k, cents_v,
                          Hq // Hkv)
@@ -280,7 +297,8 @@ def test_batched_decoder_config2_layer_vs_c_oracle():
     vc = rng.standard_normal((1, H, 128)).astype(np.float32)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     dec = PQDecoder(1, H, H, P.PQConfig(128, 64, 8))
-    out = dec(t(q), t(ck), t(cv), t(np.array([n], np.int32)), t(cents_k),
+    out = dec(t(q), K.relayout(t(ck), True), K.relayout(t(cv), True), t(np.array([n], np.int32)),
+              K.key_codebook_layout(t(cents_k), 8),
               K.value_codebook_layout(t(cents_v), 8), t(rk), t(rv),
               t(np.array([R], np.int32)), t(kc), t(vc)).cpu().numpy()[0]
     lib = O.c_library()
@@ -308,11 +326,12 @@ def test_sequence_split_merge_equals_full():
     B, Hq, Hkv, n, W = 2, 8, 2, 20000, 4
     cfg = P.PQConfig(128, 64, 8)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
-    cbk = t(rng.standard_normal((64, 256, 2)).astype(np.float32))
+    cbk = K.key_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8)
     cbv = K.value_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8)
     q = t(rng.standard_normal((B, Hq, 128)).astype(np.float32))
-    ck = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
-    cv = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+    ckr = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))   # row layout
+    cvr = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+    ck, cv = K.relayout(ckr, True), K.relayout(cvr, True)
     rk = t(rng.standard_normal((B, Hkv, 16, 128)).astype(np.float32))
     rv = t(rng.standard_normal((B, Hkv, 16, 128)).astype(np.float32))
     nr = t(np.array([16, 3], np.int32))
@@ -325,7 +344,8 @@ def test_sequence_split_merge_equals_full():
         a, b = shard_tokens(n, r, W)
         tail = r == W - 1
         rec = torch.empty((B * Hq, 132), device="cuda")
-        dec(q, ck[:, :, a:b].contiguous(), cv[:, :, a:b].contiguous(),
+        # each rank stores its own shard; the decode layout counts from its row 0
+        dec(q, K.relayout(ckr[:, :, a:b], True), K.relayout(cvr[:, :, a:b], True),
             t(np.array([b - a] * B, np.int32)), cbk, cbv, rk if tail else None,
             rv if tail else None, nr if tail else None, kc if tail else None,
             vc if tail else None, merged=rec, finalize=False)
