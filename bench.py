@@ -84,41 +84,48 @@ def ncu_traffic(cfg_name):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clocks / throttle reasons sampled through NVML every few ms during the
+    timed region (the recipe's clocks line); falls back to nvidia-smi."""
 
-    def __init__(self, index: int):
-        self.index, self.samples, self.proc = index, [], None
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period, self.samples = index, period_s, []
+        self._stop = threading.Event()
 
     def __enter__(self):
-        q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nv = (pynvml, h)
         except Exception:
-            self.proc = None
+            self._nv = None
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 4:
-                try:
-                    self.samples.append((float(parts[0]), float(parts[1]), float(parts[2]),
-                                         int(parts[3], 16)))
-                except ValueError:
-                    pass
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                if self._nv is not None:
+                    nv, h = self._nv
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    smx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                         "power.draw,clocks_event_reasons.active", "--format=csv,noheader,nounits"],
+                        capture_output=True, text=True, timeout=5).stdout.split(",")
+                    sm, smx, pw, rs = float(out[0]), float(out[1]), float(out[2]), int(out[3], 16)
+                self.samples.append((float(sm), float(smx), float(pw), int(rs)))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self.thread.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -230,6 +237,43 @@ def config_dict(name, n_gpus):
 
 # ------------------------------------------------------------------ ours --
 
+def encode_rate(dev, L, Hkv, n, stream):
+    """KV encode tok/s (BASELINE config 5): bit-exact nearest-centroid encoding
+    of an n-token prefill -- K and V of every KV head of one layer, written
+    straight into the decode layout -- timed with CUDA events; tokens/s is
+    per model token (all L layers).  fp64 distances (the bit-exact path):
+    98,304 flop per vector."""
+    import torch
+    from paper_2504_03661_b200 import kernels as K
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    x = torch.randn((2, Hkv * n, D), generator=g, device=dev)
+    cents = torch.randn((2, M, 256, 2), generator=g, device=dev)
+    codes = torch.empty((2, Hkv * n, M), dtype=torch.uint8, device=dev)
+
+    def one():
+        for kind in range(2):
+            K.encode(x[kind], cents[kind], NBITS, out=codes[kind], stream=stream,
+                     layout="decode")
+
+    with torch.cuda.stream(stream):
+        one()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record(stream)
+        for _ in range(reps):
+            one()
+        e1.record(stream)
+        e1.synchronize()
+    t_layer = e0.elapsed_time(e1) / reps * 1e-3
+    vectors = 2 * Hkv * n
+    return {"value": n / (t_layer * L), "unit": "tokens/s (all layers, K+V, all KV heads)",
+            "workload": f"{n}-token prefill x {Hkv} KV heads x K,V, one layer timed, x{L} layers",
+            "ms_per_layer": t_layer * 1e3, "vectors_per_s": vectors / t_layer,
+            "fp64_tflops": vectors * M * 256 * 6 / t_layer / 1e12, "bit_exact": True}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -264,7 +308,11 @@ def run_ours(args):
     kc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
     vc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
     out = torch.empty((L, B, Hq, D), device=dev)
-    dec = PQDecoder(B, Hq, Hkv, cfg, device=dev)
+    torch.cuda.synchronize()  # codebook layouts are written before any decode launch
+    # one fused launch per layer; PDL lets layer l+1 load its value codebook
+    # while layer l's last CTAs drain (codebooks are static: prepared above)
+    dec = PQDecoder(B, Hq, Hkv, cfg, device=dev, pdl=not args.no_pdl,
+                    static_codebooks=not args.no_pdl)
     stream = torch.cuda.Stream(device=dev)
 
     def step():
@@ -272,7 +320,7 @@ def run_ours(args):
             dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv[l], rk[l], rv[l], n_r, kc[l],
                 vc[l], out=out[l])
 
-    # capture one decode step (2 launches per layer) in a CUDA graph
+    # capture one decode step (one launch per layer) in a CUDA graph
     with torch.cuda.stream(stream):
         step()
         step()
@@ -280,7 +328,7 @@ def run_ours(args):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         step()
-    launches_per_step = 2 * L
+    launches_per_step = L
 
     def barrier():
         if world > 1:
@@ -318,8 +366,9 @@ def run_ours(args):
         for rep in range(max(2, min(args.steps, 5))):
             for l in range(L):
                 kev[l][0].record(stream)
-                K.decode_partials(dec.ws, Hkv, q[l].view(B * Hq, D), 1 / D ** 0.5, cbk[l],
-                                  codes_k[l], codes_v[l], n_q, cbv[l], stream=stream)
+                K.decode_attention(dec.ws, Hkv, q[l].view(B * Hq, D), 1 / D ** 0.5, cbk[l],
+                                   codes_k[l], codes_v[l], n_q, cbv[l], rk[l], rv[l], n_r, kc[l],
+                                   vc[l], out=out[l], stream=stream)
                 kev[l][1].record(stream)
             stream.synchronize()
             if rep > 0:
@@ -358,6 +407,8 @@ def run_ours(args):
         e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     barrier()
 
+    enc = None if args.no_encode else encode_rate(dev, L, Hkv, n, stream)
+
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -367,7 +418,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "traffic": ncu_traffic(args.config),
-                         "kernel": "decode_partials_m64b8",
+                         "kernel": "decode_partials_m64b8 (fused pqkv_decode_attention)",
                          "kernel_ms_per_launch": k_ms,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "kernel_share_of_step": share},
@@ -377,6 +428,8 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "code_stream_gbs_step": 2 * L * B * Hkv * n * M / (ms * 1e-3) / 1e9}
+    if enc is not None:
+        line["encode"] = enc
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample = cpu_decode_rate(args.config, 1, args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": 1, "kind": "port",
@@ -390,12 +443,14 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama2-32k", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-encode", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -99,7 +99,8 @@ int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits,
  * (one per SM for the fast path); needed to size the partials buffer. */
 int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas);
 
-/* Floats needed for the partials workspace: (num_ctas + B*Hq) * (d + 4). */
+/* Floats needed for the partials workspace: (num_ctas + 2*B*Hq) * (d + 4)
+ * (split records, then one dense-window record per head). */
 int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d);
 
 /* Quantized-span softmax partials: the fused LUT-score + online softmax +
@@ -159,6 +160,40 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
 /* Merge n_parts partial records per head in index order (merge_partials,
  * attention.py:193-204; the cross-GPU log-sum-exp merge of a sequence
  * split) and optionally finalize.  parts: [n_parts][n_heads][d+4]. */
+/* Flags of pqkv_decode_attention. */
+#define PQKV_DECODE_PDL 1 /* programmatic dependent launch: the grid may start
+                             while the previous kernel on the stream drains;
+                             it waits for it before touching q, lengths,
+                             recent rows, counters, partials or outputs */
+#define PQKV_DECODE_STATIC_CODEBOOKS 2 /* the codebooks were written before the
+                             previous kernel on the stream started (e.g. at
+                             load time), so they may be read before that
+                             kernel finishes (with PQKV_DECODE_PDL) */
+
+/* One fused launch per layer: decode_step (attention.py:214-287) for every
+ * (b, hq) -- pqkv_decode_partials' quantized span, the dense partial of the
+ * recent rows + current token (dense_partial :169-190, computed by the CTA
+ * holding the head's first quantized tokens), and, by the last CTA to finish
+ * each head (an arrival counter), the fixed-order merge_partials (:193-204)
+ * and finalize (:207-211).  Arguments as pqkv_decode_partials plus those of
+ * pqkv_decode_finish, and
+ *   counters  [B*Hq] int32, zero before the first call; every launch leaves
+ *             them zero again (a launch must not be aborted midway)
+ *   partials  pqkv_partials_floats(num_ctas, B, Hq, d) floats
+ *   flags     PQKV_DECODE_* bits
+ * Other geometries run pqkv_decode_partials + pqkv_decode_finish (counters
+ * and flags unused). */
+int pqkv_decode_attention(const float *q, float scale, const float *cb_k,
+                          float *lut_ws, int B, int Hq, int Hkv,
+                          const void *codes_k, const void *codes_v,
+                          int64_t ld_tok, const int32_t *n_q,
+                          const float *cb_v, int d, int M, int nbits,
+                          const float *recent_k, const float *recent_v,
+                          int64_t ld_recent, const int32_t *n_recent,
+                          const float *k_cur, const float *v_cur, int num_ctas,
+                          float *partials, int32_t *counters, float *out,
+                          float *lse, float *merged, int flags, void *stream);
+
 int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_heads,
                         int d, float *out, float *lse, float *merged,
                         void *stream);

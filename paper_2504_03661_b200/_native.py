@@ -18,6 +18,7 @@ from .build import LIB
 PQKV_OK, PQKV_EINVAL, PQKV_ECUDA = 0, 1, 2
 DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 PARTIAL_HEADER = 4
+DECODE_PDL, DECODE_STATIC_CODEBOOKS = 1, 2  # pqkv_decode_attention flags
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -43,6 +44,8 @@ SIGNATURES = {
     "pqkv_decode_finish": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _F, _P, _P, _I64, _P, _P, _P,
                                 _P, _P, _P, _P]),
     "pqkv_merge_partials": (_I, [_P, _I, _I64, _I, _P, _P, _P, _P]),
+    "pqkv_decode_attention": (_I, [_P, _F, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _I, _I, _I,
+                                   _P, _P, _I64, _P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _P]),
     "pqkv_score_codes": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_accumulate_mass": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
 }

@@ -48,27 +48,31 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu for sm_100a and link libpqkv_sm100.so; return its path."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, lib: str = LIB,
+          defines: tuple = ()) -> str:
+    """Compile every .cu for sm_100a and link libpqkv_sm100.so; return its path.
+    `defines` (e.g. ("PQKV_TRACE",)) builds a diagnostic variant into `lib`."""
+    if not force and lib == LIB and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     objs = []
+    tag = "_".join(defines)
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(OUT_DIR, src.replace(".cu", f"{tag}.o"))
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", INCLUDE, "-c",
+               os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                     "-o", tmp, *objs], check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

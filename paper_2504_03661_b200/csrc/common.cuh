@@ -50,12 +50,13 @@ inline bool is_fast_geometry(int d, int M, int nbits) {
 // register order while the 32 lanes of a warp still hit 32 distinct
 // subspaces (= shared-memory banks) at every step -- no in-register
 // rotation.  A bijection per row, so uniform random codes stay uniform.
+// `slot` is the token index (only its low three bits matter).
 __host__ __device__ __forceinline__ int decode_lane_rot(int lane) {
     return ((lane & 15) + (lane >> 4)) & 15;
 }
 __host__ __device__ __forceinline__ int decode_layout_pos(int i, int slot) {
     const int q = i >> 4;
-    const int r = decode_lane_rot(4 * slot + q);
+    const int r = decode_lane_rot(4 * (slot & 7) + q);
     return 16 * q + (((i & 15) - r) & 15);
 }
 
@@ -69,60 +70,98 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 // ------------------------------------------------------- work partition ---
-// The token space of all (b, hq) heads is flattened head-major
-// (pos = Hq * sum_{b'<b} n_q[b'] + hq * n_q[b] + t) and cut into equal
-// chunks, one per persistent CTA.  A (CTA c, head bh) overlap is a segment;
-// its partial lives in slot c + bh, which is unique because both c and bh are
-// non-decreasing along the flattened order.  decode and finish kernels both
-// evaluate this map, so the host never needs the device-resident n_q.
+// Every (b, hq) head is laid out on a flattened *cost* axis, head-major:
+// kSwitchCost setup units (the head's key-LUT build, paid by every CTA that
+// switches onto the head) followed by max(n_q[b], 1) token units (an empty
+// head still owns one unit, so exactly one CTA emits its empty record and
+// finalizes it).  The axis is cut into equal chunks, one per persistent CTA,
+// so a CTA that crosses a head boundary is charged for its extra LUT build
+// and the grid stays balanced.  A (CTA c, head bh) overlap of the *token*
+// units is a segment; its partial lives in slot c + bh, which is unique
+// because both c and bh are non-decreasing along the axis.  The decode and
+// finish kernels both evaluate this map from the device-resident n_q, so the
+// host never needs the lengths.
 constexpr int kChunkAlign = 16;
+constexpr int kSwitchCost = 1024;  // tokens-equivalent of a head switch (measured)
 
-struct FlatMap {
+struct CostMap {
     int64_t total;
     int64_t chunk;
 };
 
-__device__ __forceinline__ FlatMap flat_map(const int32_t *__restrict__ n_q, int B, int Hq,
+__device__ __forceinline__ int64_t head_span(int n) { return kSwitchCost + (int64_t)max(n, 1); }
+
+__device__ __forceinline__ CostMap cost_map(const int32_t *__restrict__ n_q, int B, int Hq,
                                             int num_ctas) {
     int64_t tot = 0;
-    for (int b = 0; b < B; ++b) tot += (int64_t)Hq * (int64_t)max(n_q[b], 0);
+    for (int b = 0; b < B; ++b) tot += (int64_t)Hq * head_span(n_q[b]);
     int64_t chunk = (tot + num_ctas - 1) / num_ctas;
     chunk = (chunk + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
     if (chunk < kChunkAlign) chunk = kChunkAlign;
     return {tot, chunk};
 }
 
-// Flattened start of head bh and its length.
-__device__ __forceinline__ int64_t head_start(const int32_t *__restrict__ n_q, int Hq, int bh,
-                                              int *len) {
+// Cost-axis position of token 0 of head bh; *len = n_q[b] (>= 0).
+__device__ __forceinline__ int64_t head_token0(const int32_t *__restrict__ n_q, int Hq, int bh,
+                                               int *len) {
     const int b = bh / Hq, hq = bh - b * Hq;
     int64_t base = 0;
-    for (int bb = 0; bb < b; ++bb) base += (int64_t)Hq * (int64_t)max(n_q[bb], 0);
+    for (int bb = 0; bb < b; ++bb) base += (int64_t)Hq * head_span(n_q[bb]);
     const int n = max(n_q[b], 0);
     *len = n;
-    return base + (int64_t)hq * n;
+    return base + (int64_t)hq * head_span(n) + kSwitchCost;
 }
 
-// Locate the head containing flattened position pos (pos < total).
-__device__ __forceinline__ void locate(const int32_t *__restrict__ n_q, int B, int Hq, int64_t pos,
-                                       int *bh, int *t, int *len) {
-    int64_t base = 0;
-    for (int b = 0; b < B; ++b) {
-        const int n = max(n_q[b], 0);
-        const int64_t span = (int64_t)Hq * n;
-        if (pos < base + span) {
-            const int64_t off = pos - base;
-            const int hq = (int)(off / n);
-            *bh = b * Hq + hq;
-            *t = (int)(off - (int64_t)hq * n);
-            *len = n;
-            return;
+// CTAs [*c_first, *c_last] hold the segments of head bh.
+__device__ __forceinline__ void head_ctas(const int32_t *__restrict__ n_q, int Hq, int bh,
+                                          int64_t chunk, int *c_first, int *c_last, int *len) {
+    const int64_t t0 = head_token0(n_q, Hq, bh, len);
+    *c_first = (int)(t0 / chunk);
+    *c_last = (int)((t0 + max(*len, 1) - 1) / chunk);
+}
+
+struct Segment {
+    int bh;     // head b * Hq + hq
+    int lo, hi; // token range [lo, hi) (empty for an empty head)
+    int len;    // n_q[b]
+    bool first; // this CTA holds the head's first token unit (c == c_first)
+    bool last;  // this CTA holds the head's last token unit (c == c_last)
+};
+
+// Next segment of the chunk [*pos, end); advances *pos.  False when done.
+__device__ __forceinline__ bool next_segment(const int32_t *__restrict__ n_q, int B, int Hq,
+                                             int64_t *pos, int64_t end, Segment *s) {
+    while (*pos < end) {
+        int64_t base = 0;
+        int b = 0;
+        for (; b < B; ++b) {
+            const int64_t span = (int64_t)Hq * head_span(n_q[b]);
+            if (*pos < base + span) break;
+            base += span;
         }
-        base += span;
+        if (b == B) {  // past the axis (cannot happen for pos < total)
+            *pos = end;
+            return false;
+        }
+        const int n = max(n_q[b], 0);
+        const int64_t hs = head_span(n);
+        const int hq = (int)((*pos - base) / hs);
+        const int64_t h0 = base + (int64_t)hq * hs;   // head start (setup units)
+        const int64_t t0 = h0 + kSwitchCost;           // token 0
+        const int64_t seg_end = min(end, h0 + hs);
+        const int64_t a = max(*pos, t0);
+        *pos = seg_end;
+        if (a < seg_end) {
+            s->bh = b * Hq + hq;
+            s->lo = (int)(a - t0);
+            s->hi = (int)min(seg_end - t0, (int64_t)n);
+            s->len = n;
+            s->first = (a == t0);
+            s->last = (seg_end == h0 + hs);
+            return true;
+        }
     }
-    *bh = -1;
-    *t = 0;
-    *len = 0;
+    return false;
 }
 
 }  // namespace pqkv

@@ -12,7 +12,7 @@
 //
 // decode_partials_m64b8 (the fast path, d=128 M=64 nbits=8):
 //   * persistent grid, one 512-thread CTA per SM; the flattened token space
-//     of all heads is cut into equal chunks (common.cuh FlatMap);
+//     of all heads is cut into equal chunks (common.cuh CostMap);
 //   * shared memory: the head's key LUT, centroid-major [256][64] fp32
 //     (64 KiB), and the value codebook as two [256][32] float2 halves
 //     (128 KiB, loaded once per CTA);
@@ -34,6 +34,7 @@
 //   * epilogue: slot partials are rescaled to the CTA max and summed through
 //     shared memory into one (m, l, acc[128]) record per segment.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -43,12 +44,63 @@ namespace {
 constexpr int kPS = PQKV_PARTIAL_HEADER;  // record = [m, l, 0, 0, acc[d]]
 
 // ============================================================ fast path ====
+// PDL (programmatic dependent launch): a grid launched with the
+// programmatic-serialization attribute may start while the previous kernel on
+// the stream drains; griddepcontrol.wait blocks until that kernel finished
+// and its memory is visible.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 namespace fast {
 constexpr int M = 64, KSUB = 256, D = 128;
-constexpr int WARPS = 16, NT = WARPS * 32;
+constexpr int WARPS = 16, NT = WARPS * 32;  // one persistent CTA per SM
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
-constexpr int SMEM_BYTES = LUT_BYTES + CV_BYTES + (2 * WARPS + 4 * D) * 4 + 16;
+// shared-memory map (bytes from the dynamic base)
+constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                   // red_m[16], red_l[16]
+constexpr int OFF_COL = OFF_RED + 2 * WARPS * 4;                // colsum[4][128]
+constexpr int OFF_DNS = OFF_COL + 4 * D * 4;                    // dense m[16], l[16], acc[16][128]
+constexpr int OFF_BAR = OFF_DNS + (2 * WARPS + WARPS * D) * 4;  // 2 mbarriers
+constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flag, c_first, c_last
+constexpr int SMEM_BYTES = OFF_FLAG + 16;
+
+#ifdef PQKV_TRACE
+// debug-only timeline: per CTA [smid, t_entry, t_ready, t_loop0_end, t_exit, nseg]
+__device__ unsigned long long g_trace[1024 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PQKV_TR(slot, val) \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_trace[blockIdx.x * 8 + (slot)] = (val)
+#else
+#define PQKV_TR(slot, val)
+#endif
+
+struct Args {
+    const float *q;
+    float scale;
+    const float *ck;   // key codebook layout (kLutFromQ) ...
+    const float *lut;  // ... or precomputed tables [B*Hq][256][64]
+    int B, Hq, Hkv;
+    const uint8_t *codes_k, *codes_v;
+    int64_t ld_tok;
+    const int32_t *n_q;
+    const float *cv;
+    int num_ctas;
+    float *parts;
+    // fused finish (counters == nullptr: partial records only)
+    int32_t *counters;
+    const float *recent_k, *recent_v;
+    int64_t ld_recent;
+    const int32_t *n_recent;
+    const float *k_cur, *v_cur;
+    float *out, *lse, *merged;
+    int early_cv;  // value codebook may be read before the grid-dependency wait
+};
 
 __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
     uint4 r;
@@ -206,43 +258,164 @@ __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
     }
 }
 
+// Dense partial of the recent rows + current token (dense_partial,
+// attention.py:169-190), per warp: warp w takes rows w, w + 16, ... with its
+// own online softmax; the 16 states are merged after the next barrier.  Out
+// of line, so the hot loop's register allocation is not shaped by it.
+__device__ __noinline__ void dense_warp_state(const float *q, float scale, const float *recent_k,
+                                              const float *recent_v, int64_t ld_recent,
+                                              const int32_t *n_recent, const float *k_cur,
+                                              const float *v_cur, int Hkv, int bh, int b, int hkv,
+                                              int warp, int lane, float *dn_m, float *dn_l,
+                                              float (*dn_acc)[D]) {
+    const int nr = (n_recent != nullptr && recent_k != nullptr) ? max(n_recent[b], 0) : 0;
+    const int rows = nr + (k_cur != nullptr ? 1 : 0);
+    const float4 qv = __ldg(reinterpret_cast<const float4 *>(q + (int64_t)bh * D) + lane);
+    const int64_t rbase = ((int64_t)b * Hkv + hkv) * ld_recent * D;
+    const int64_t cbase = ((int64_t)b * Hkv + hkv) * D;
+    float dm = -INFINITY, dl = 0.f;
+    float4 da = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int rr = warp; rr < rows; rr += WARPS) {
+        const float *kr = rr < nr ? recent_k + rbase + (int64_t)rr * D : k_cur + cbase;
+        const float *vr = rr < nr ? recent_v + rbase + (int64_t)rr * D : v_cur + cbase;
+        const float4 kk = __ldg(reinterpret_cast<const float4 *>(kr) + lane);
+        const float4 vv = __ldg(reinterpret_cast<const float4 *>(vr) + lane);
+        float sdot = qv.x * kk.x + qv.y * kk.y + qv.z * kk.z + qv.w * kk.w;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+        const float sc = scale * sdot;
+        const float mn = fmaxf(dm, sc);
+        const float f = expf(dm - mn), p = expf(sc - mn);
+        dl = dl * f + p;
+        da.x = da.x * f + p * vv.x;
+        da.y = da.y * f + p * vv.y;
+        da.z = da.z * f + p * vv.z;
+        da.w = da.w * f + p * vv.w;
+        dm = mn;
+    }
+    if (lane == 0) {
+        dn_m[warp] = dm;
+        dn_l[warp] = dl;
+    }
+    reinterpret_cast<float4 *>(dn_acc[warp])[lane] = da;
+}
+
+// merge_partials (attention.py:193-204) of record (mb, lb, ab) into (m, l, acc);
+// identity on lb == 0
+__device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb, float lb,
+                                       float ab) {
+    if (lb == 0.f) return;
+    if (l == 0.f) {
+        m = mb;
+        l = lb;
+        acc = ab;
+        return;
+    }
+    const float mm = fmaxf(m, mb);
+    const float wa = expf(m - mm), wb = expf(mb - mm);
+    l = l * wa + lb * wb;
+    acc = acc * wa + ab * wb;
+    m = mm;
+}
+
+// The last CTA to finish head bh (arrival counter) merges the head's split
+// records in CTA order (deterministic), then its dense record, and finalizes
+// (merge_partials :193-204, finalize :207-211).  Threads tid < D, one output
+// dimension each.  Out of line: runs once per head.
+__device__ __noinline__ void finish_head(const float *parts, int64_t dense_base, int bh,
+                                         int c_first, int c_last, int tid, float *out, float *lse,
+                                         float *merged) {
+    const float *drec = parts + (dense_base + bh) * (D + kPS);
+    // the dense record and the first batch are in flight before any is consumed
+    const float dm = __ldcg(drec), dl = __ldcg(drec + 1), da = __ldcg(drec + kPS + tid);
+    float m = -INFINITY, l = 0.f, acc = 0.f;
+    for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+        const int cnt = min(8, c_last - c0 + 1);
+        float rm[8], rl[8], ra[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < cnt) {
+                const float *rec = parts + ((int64_t)c0 + k + bh) * (D + kPS);
+                rm[k] = __ldcg(rec);
+                rl[k] = __ldcg(rec + 1);
+                ra[k] = __ldcg(rec + kPS + tid);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < cnt) merge1(m, l, acc, rm[k], rl[k], ra[k]);
+    }
+    merge1(m, l, acc, dm, dl, da);
+    const float inv = (l > 0.f) ? 1.f / l : NAN;
+    if (out) out[(int64_t)bh * D + tid] = acc * inv;
+    if (merged) merged[(int64_t)bh * (D + kPS) + kPS + tid] = acc;
+    if (tid == 0) {
+        if (lse) lse[bh] = (l > 0.f) ? m + logf(l) : -INFINITY;
+        if (merged) {
+            float *rec = merged + (int64_t)bh * (D + kPS);
+            rec[0] = m;
+            rec[1] = l;
+            rec[2] = 0.f;
+            rec[3] = 0.f;
+        }
+    }
+}
+
 // kLutFromQ: build each head's LUT in shared memory from q and the
 // centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
 // otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
 template <bool kLutFromQ>
-__global__ void __launch_bounds__(NT, 1)
-    decode_partials_m64b8(const float *__restrict__ q_g, float scale,
-                          const float *__restrict__ ck_g, const float *__restrict__ lut_g, int B,
-                          int Hq, int Hkv, const uint8_t *__restrict__ codes_k,
-                          const uint8_t *__restrict__ codes_v, int64_t ld_tok,
-                          const int32_t *__restrict__ n_q, const float *__restrict__ cv_g,
-                          int num_ctas, float *__restrict__ parts) {
+__global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     extern __shared__ __align__(128) unsigned char smem[];
+#ifdef PQKV_TRACE
+    unsigned smid_;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid_));
+    PQKV_TR(0, smid_);
+    PQKV_TR(1, gtime());
+    int nseg_ = 0;
+#endif
     float *lut_s = reinterpret_cast<float *>(smem);
-    float *red_m = reinterpret_cast<float *>(smem + LUT_BYTES + CV_BYTES);
+    float *red_m = reinterpret_cast<float *>(smem + OFF_RED);
     float *red_l = red_m + WARPS;
-    float(*colsum)[D] = reinterpret_cast<float(*)[D]>(red_l + WARPS);
-    unsigned long long *bars = reinterpret_cast<unsigned long long *>(colsum[4]);
+    float(*colsum)[D] = reinterpret_cast<float(*)[D]>(smem + OFF_COL);
+    float *dn_m = reinterpret_cast<float *>(smem + OFF_DNS);
+    float *dn_l = dn_m + WARPS;
+    float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + WARPS);
+    int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_lut)
     const uint32_t cta_byte = sbase & 0xFF000000u;
-    const uint32_t bar_cv = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const uint32_t bar_lut = (uint32_t)__cvta_generic_to_shared(&bars[1]);
+    const uint32_t bar_cv = sbase + OFF_BAR;
+    const uint32_t bar_lut = sbase + OFF_BAR + 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q4 = lane & 3, slot = lane >> 2;
     const int r = decode_lane_rot(lane);
 
     // value codebook: one TMA bulk copy per CTA, overlapped with the first
-    // segment's code prefetch and LUT build
+    // segment's code prefetch and LUT build -- and, when the codebook is static
+    // (early_cv), with the previous kernel's tail (PDL)
     if (tid == 0) {
         mbar_init(bar_cv, 1);
         mbar_init(bar_lut, 1);
+        if (A.early_cv) {
+            mbar_expect_tx(bar_cv, CV_BYTES);
+#pragma unroll
+            for (int c = 0; c < CV_BYTES / 16384; ++c)
+                bulk_g2s(sbase + LUT_BYTES + c * 16384,
+                         reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
+        }
+    }
+#ifndef PQKV_NO_PDL
+    pdl_launch_dependents();
+    pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
+#endif
+    if (tid == 0 && !A.early_cv) {
         mbar_expect_tx(bar_cv, CV_BYTES);
 #pragma unroll
         for (int c = 0; c < CV_BYTES / 16384; ++c)
-            bulk_g2s(sbase + LUT_BYTES + c * 16384, reinterpret_cast<const char *>(cv_g) + c * 16384,
-                     16384, bar_cv);
+            bulk_g2s(sbase + LUT_BYTES + c * 16384,
+                     reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
     }
 
     // lane-constant address bytes (see header comment)
@@ -261,24 +434,22 @@ __global__ void __launch_bounds__(NT, 1)
         packV[jp] = pv | ((uint32_t)(q4 >> 1) << 16) | cta_byte;
     }
 
-    const FlatMap fm = flat_map(n_q, B, Hq, num_ctas);
+    const CostMap cm = cost_map(A.n_q, A.B, A.Hq, A.num_ctas);
     const int cta = blockIdx.x;
-    int64_t pos = (int64_t)cta * fm.chunk;
-    const int64_t end = min(pos + fm.chunk, fm.total);
-    const int group = Hq / Hkv;
+    int64_t pos = (int64_t)cta * cm.chunk;
+    const int64_t end = min(pos + cm.chunk, cm.total);
+    const int group = A.Hq / A.Hkv;
     bool cv_ready = false;
     uint32_t lut_phase = 0;
 
-    while (pos < end) {
-        int bh, t0, len;
-        locate(n_q, B, Hq, pos, &bh, &t0, &len);
-        const int n = (int)min((int64_t)(len - t0), end - pos);
-        const int b = bh / Hq, hq = bh - b * Hq, hkv = hq / group;
-
-        const int64_t head_off = ((int64_t)b * Hkv + hkv) * ld_tok * M;
-        const uint8_t *kbase = codes_k + head_off + q4 * 16;
-        const uint8_t *vbase = codes_v + head_off + q4 * 16;
-        const int lo = t0, hi = t0 + n;           // token range of this segment
+    Segment sg;
+    while (next_segment(A.n_q, A.B, A.Hq, &pos, end, &sg)) {
+        const int bh = sg.bh;
+        const int b = bh / A.Hq, hq = bh - b * A.Hq, hkv = hq / group;
+        const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
+        const uint8_t *kbase = A.codes_k + head_off + q4 * 16;
+        const uint8_t *vbase = A.codes_v + head_off + q4 * 16;
+        const int lo = sg.lo, hi = sg.hi;             // token range of this segment
         const int u0 = lo >> 4, u1 = (hi + 15) >> 4;  // 16-token units (absolute)
 
         // code prefetch first: these loads fly while the LUT is built
@@ -292,17 +463,17 @@ __global__ void __launch_bounds__(NT, 1)
         if (kLutFromQ) {
             // lut[c][i] = scale * (q[2i] C[c][i].x + q[2i+1] C[c][i].y); thread owns
             // subspaces i0, i0+1 (i0 = 2*(tid & 31)) of centroids c = tid/32 + 16k
-            const float4 qq = __ldg(reinterpret_cast<const float4 *>(q_g + (int64_t)bh * D) +
+            const float4 qq = __ldg(reinterpret_cast<const float4 *>(A.q + (int64_t)bh * D) +
                                     (tid & 31));
-            const float4 *src = reinterpret_cast<const float4 *>(ck_g);
+            const float4 *src = reinterpret_cast<const float4 *>(A.ck);
             float4 cc[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 float2 o;
-                o.x = scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
-                o.y = scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
+                o.x = A.scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
+                o.y = A.scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
                 reinterpret_cast<float2 *>(lut_s)[tid + k * NT] = o;
             }
         } else if (tid == 0) {
@@ -310,9 +481,19 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int c = 0; c < LUT_BYTES / 16384; ++c)
                 bulk_g2s(sbase + c * 16384,
-                         reinterpret_cast<const char *>(lut_g + (int64_t)bh * KSUB * M) + c * 16384,
+                         reinterpret_cast<const char *>(A.lut + (int64_t)bh * KSUB * M) + c * 16384,
                          16384, bar_lut);
         }
+        // dense partial by the CTA holding the head's last tokens (for most CTAs
+        // their first segment, so it overlaps the prologue)
+#ifndef PQKV_NO_DENSE
+        const bool do_dense = A.counters != nullptr && sg.last;
+#else
+        const bool do_dense = false;
+#endif
+        if (do_dense)
+            dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent, A.k_cur,
+                             A.v_cur, A.Hkv, bh, b, hkv, warp, lane, dn_m, dn_l, dn_acc);
         if (!kLutFromQ) {
             mbar_wait(bar_lut, lut_phase);
             lut_phase ^= 1u;
@@ -322,6 +503,35 @@ __global__ void __launch_bounds__(NT, 1)
             cv_ready = true;
         }
         __syncthreads();
+#ifdef PQKV_TRACE
+        if (nseg_ == 0) PQKV_TR(2, gtime());
+#endif
+        if (do_dense && tid < D) {
+            // merge the 16 warps' dense states into record dense_base + bh
+            float Mx = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w)
+                if (dn_l[w] > 0.f) Mx = fmaxf(Mx, dn_m[w]);
+            float L = 0.f, acc = 0.f;
+            if (Mx != -INFINITY) {
+#pragma unroll
+                for (int w = 0; w < WARPS; ++w) {
+                    if (dn_l[w] > 0.f) {
+                        const float f = expf(dn_m[w] - Mx);
+                        L += dn_l[w] * f;
+                        acc += dn_acc[w][tid] * f;
+                    }
+                }
+            }
+            float *rec = A.parts + ((int64_t)A.num_ctas + (int64_t)A.B * A.Hq + bh) * (D + kPS);
+            rec[kPS + tid] = acc;
+            if (tid == 0) {
+                rec[0] = Mx;
+                rec[1] = L;
+                rec[2] = 0.f;
+                rec[3] = 0.f;
+            }
+        }
 
         SlotState S;
         S.m = -INFINITY;
@@ -333,6 +543,9 @@ __global__ void __launch_bounds__(NT, 1)
         // pending load is only waited for when its unit is processed
         int u = u0 + warp;
         while (true) {
+            // pin the lane-constant address words in registers (no remat)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
 #define PQKV_STEP(UX)                                                                   \
     if (u >= u1) break;                                                                 \
     if ((u << 4) >= lo && (u << 4) + 16 <= hi) {                                        \
@@ -350,6 +563,9 @@ __global__ void __launch_bounds__(NT, 1)
         }
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
+#ifdef PQKV_TRACE
+        if (nseg_++ == 0) PQKV_TR(3, gtime());
+#endif
         float mw = S.m;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
@@ -381,7 +597,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         __syncthreads();
         if (tid < D) {
-            float *rec = parts + ((int64_t)cta + bh) * (D + kPS);
+            float *rec = A.parts + ((int64_t)cta + bh) * (D + kPS);
             rec[kPS + tid] = (colsum[0][tid] + colsum[1][tid]) + (colsum[2][tid] + colsum[3][tid]);
             if (tid == 0) {
                 float L = 0.f;
@@ -393,9 +609,43 @@ __global__ void __launch_bounds__(NT, 1)
                 rec[3] = 0.f;
             }
         }
-        pos += n;
+
+    }
+    // ---- arrivals, after all of this CTA's segments (kept out of the segment
+    // loop, whose code generation it would otherwise disturb): per segment, the
+    // last CTA to finish the head merges its records in CTA order
+    // (deterministic), then the dense record, and finalizes
+    if (A.counters != nullptr) {
+        if (tid < D) __threadfence();  // this CTA's record (and dense record) writers
+        int64_t p2 = (int64_t)cta * cm.chunk;
+        Segment s2;
+        while (next_segment(A.n_q, A.B, A.Hq, &p2, end, &s2)) {
+            __syncthreads();  // flag_s reuse; fences done
+            if (tid == 0) {
+                int c_first, c_last, len;
+                head_ctas(A.n_q, A.Hq, s2.bh, cm.chunk, &c_first, &c_last, &len);
+                const int old = atomicAdd(A.counters + s2.bh, 1);
+                const bool last = (old == c_last - c_first);
+                if (last) {
+                    A.counters[s2.bh] = 0;  // ready for the next launch
+                    __threadfence();
+                }
+                flag_s[0] = last ? 1 : 0;
+                flag_s[1] = c_first;
+                flag_s[2] = c_last;
+            }
+            __syncthreads();
+            if (flag_s[0] && tid < D)
+                finish_head(A.parts, (int64_t)A.num_ctas + (int64_t)A.B * A.Hq, s2.bh, flag_s[1],
+                            flag_s[2], tid, A.out, A.lse, A.merged);
+        }
     }
     if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight
+#ifdef PQKV_TRACE
+    __syncthreads();
+    PQKV_TR(4, gtime());
+    PQKV_TR(5, nseg_);
+#endif
 }
 }  // namespace fast
 
@@ -418,16 +668,15 @@ __global__ void __launch_bounds__(GT)
     __shared__ float red[GT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int dsub = d / M;
-    const FlatMap fm = flat_map(n_q, B, Hq, num_ctas);
+    const CostMap cm = cost_map(n_q, B, Hq, num_ctas);
     const int cta = blockIdx.x;
-    int64_t pos = (int64_t)cta * fm.chunk;
-    const int64_t end = min(pos + fm.chunk, fm.total);
+    int64_t pos = (int64_t)cta * cm.chunk;
+    const int64_t end = min(pos + cm.chunk, cm.total);
     const int group = Hq / Hkv;
 
-    while (pos < end) {
-        int bh, t0, len;
-        locate(n_q, B, Hq, pos, &bh, &t0, &len);
-        const int n = (int)min((int64_t)(len - t0), end - pos);
+    Segment sg;
+    while (next_segment(n_q, B, Hq, &pos, end, &sg)) {
+        const int bh = sg.bh, t0 = sg.lo, n = sg.hi - sg.lo;
         const int b = bh / Hq, hq = bh - b * Hq, hkv = hq / group;
         const float *lut = lut_g + (int64_t)bh * ksub * M;
         const int64_t head_off = ((int64_t)b * Hkv + hkv) * ld_tok * M;
@@ -496,7 +745,6 @@ __global__ void __launch_bounds__(GT)
             rec[2] = 0.f;
             rec[3] = 0.f;
         }
-        pos += n;
         __syncthreads();
     }
 }
@@ -564,18 +812,17 @@ __global__ void __launch_bounds__(FT)
 
     // 1. quantized partials of this head, merged in CTA order (deterministic)
     if (parts != nullptr && n_q != nullptr) {
-        const FlatMap fm = flat_map(n_q, B, Hq, num_ctas);
-        int len;
-        const int64_t s0 = head_start(n_q, Hq, bh, &len);
-        if (len > 0) {
-            const int64_t c_first = s0 / fm.chunk, c_last = (s0 + len - 1) / fm.chunk;
-            for (int64_t c0 = c_first; c0 <= c_last; c0 += 8) {
-                const int cnt = (int)min((int64_t)8, c_last - c0 + 1);
+        const CostMap cm = cost_map(n_q, B, Hq, num_ctas);
+        int c_first, c_last, len;
+        head_ctas(n_q, Hq, bh, cm.chunk, &c_first, &c_last, &len);
+        if (len > 0) {  // an empty head's single record is empty: skip it (may be unwritten)
+            for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+                const int cnt = min(8, c_last - c0 + 1);
                 float rm[8], rl[8], ra[8][FMAXD / FT];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     if (k < cnt) {
-                        const float *rec = parts + (c0 + k + bh) * (int64_t)(d + kPS);
+                        const float *rec = parts + ((int64_t)c0 + k + bh) * (d + kPS);
                         rm[k] = rec[0];
                         rl[k] = rec[1];
 #pragma unroll
@@ -752,8 +999,15 @@ extern "C" int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas) {
     return PQKV_OK;
 }
 
+#ifdef PQKV_TRACE
+extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {
+    return cudaMemcpyFromSymbol(host, fast::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
+               ? 0 : 2;
+}
+#endif
+
 extern "C" int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d) {
-    return ((int64_t)num_ctas + (int64_t)B * Hq) * (int64_t)(d + kPS);
+    return ((int64_t)num_ctas + 2 * (int64_t)B * Hq) * (int64_t)(d + kPS);
 }
 
 static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int M, int nbits,
@@ -768,23 +1022,52 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
 }
 
 template <bool kLutFromQ>
-static int launch_fast(const float *q, float scale, const float *ck, const float *lut, int B,
-                       int Hq, int Hkv, const void *codes_k, const void *codes_v, int64_t ld_tok,
-                       const int32_t *n_q, const float *cb_v, int num_ctas, float *partials,
-                       cudaStream_t st) {
-    static bool attr_set = false;
+static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
+    static int attr_set[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
     auto kern = fast::decode_partials_m64b8<kLutFromQ>;
-    if (!attr_set) {
+    if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              fast::SMEM_BYTES);
-        if (e != cudaSuccess)
-            return fail(PQKV_ECUDA, "pqkv_decode_partials: %s", cudaGetErrorString(e));
-        attr_set = true;
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+        if (dev < 64) attr_set[dev] = 1;
     }
-    kern<<<num_ctas, fast::NT, fast::SMEM_BYTES, st>>>(
-        q, scale, ck, lut, B, Hq, Hkv, (const uint8_t *)codes_k, (const uint8_t *)codes_v, ld_tok,
-        n_q, cb_v, num_ctas, partials);
-    return launch_status("pqkv_decode_partials");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(args.num_ctas);
+    cfg.blockDim = dim3(fast::NT);
+    cfg.dynamicSmemBytes = fast::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+    return launch_status(fn);
+}
+
+static fast::Args fast_args(const float *q, float scale, const float *ck, const float *lut, int B,
+                            int Hq, int Hkv, const void *codes_k, const void *codes_v,
+                            int64_t ld_tok, const int32_t *n_q, const float *cb_v, int num_ctas,
+                            float *partials) {
+    fast::Args a = {};
+    a.q = q;
+    a.scale = scale;
+    a.ck = ck;
+    a.lut = lut;
+    a.B = B;
+    a.Hq = Hq;
+    a.Hkv = Hkv;
+    a.codes_k = (const uint8_t *)codes_k;
+    a.codes_v = (const uint8_t *)codes_v;
+    a.ld_tok = ld_tok;
+    a.n_q = n_q;
+    a.cv = cb_v;
+    a.num_ctas = num_ctas;
+    a.parts = partials;
+    return a;
 }
 
 static int launch_generic(const float *lut, int B, int Hq, int Hkv, const void *codes_k,
@@ -814,8 +1097,9 @@ extern "C" int pqkv_decode_partials(const float *q, float scale, const float *cb
                    "pqkv_decode_partials: null pointer");
     cudaStream_t st = as_stream(stream);
     if (is_fast_geometry(d, M, nbits))
-        return launch_fast<true>(q, scale, cb_k, nullptr, B, Hq, Hkv, codes_k, codes_v, ld_tok,
-                                 n_q, cb_v, num_ctas, partials, st);
+        return launch_fast<true>(fast_args(q, scale, cb_k, nullptr, B, Hq, Hkv, codes_k, codes_v,
+                                           ld_tok, n_q, cb_v, num_ctas, partials),
+                                 false, st, "pqkv_decode_partials");
     PQKV_CHECK_ARG(lut_ws != nullptr, "pqkv_decode_partials: this geometry needs lut_ws");
     rc = pqkv_build_lut(q, (int64_t)B * Hq, d, cb_k, M, nbits, scale, lut_ws, stream);
     if (rc) return rc;
@@ -835,8 +1119,9 @@ extern "C" int pqkv_decode_partials_lut(const float *lut, int B, int Hq, int Hkv
                    "pqkv_decode_partials_lut: null pointer");
     cudaStream_t st = as_stream(stream);
     if (is_fast_geometry(d, M, nbits))
-        return launch_fast<false>(nullptr, 0.f, nullptr, lut, B, Hq, Hkv, codes_k, codes_v, ld_tok,
-                                  n_q, cb_v, num_ctas, partials, st);
+        return launch_fast<false>(fast_args(nullptr, 0.f, nullptr, lut, B, Hq, Hkv, codes_k,
+                                            codes_v, ld_tok, n_q, cb_v, num_ctas, partials),
+                                  false, st, "pqkv_decode_partials_lut");
     return launch_generic(lut, B, Hq, Hkv, codes_k, codes_v, ld_tok, n_q, cb_v, d, M, nbits,
                           num_ctas, partials, st);
 }
@@ -865,6 +1150,53 @@ extern "C" int pqkv_decode_finish(const float *partials, int num_ctas, int B, in
         partials, num_ctas, B, Hq, Hkv, d, n_q, q, scale, recent_k, recent_v, ld_recent, n_recent,
         k_cur, v_cur, out, lse, merged, dch);
     return launch_status("pqkv_decode_finish");
+}
+
+extern "C" int pqkv_decode_attention(
+    const float *q, float scale, const float *cb_k, float *lut_ws, int B, int Hq, int Hkv,
+    const void *codes_k, const void *codes_v, int64_t ld_tok, const int32_t *n_q,
+    const float *cb_v, int d, int M, int nbits, const float *recent_k, const float *recent_v,
+    int64_t ld_recent, const int32_t *n_recent, const float *k_cur, const float *v_cur,
+    int num_ctas, float *partials, int32_t *counters, float *out, float *lse, float *merged,
+    int flags, void *stream) {
+    int rc = check_decode_args("pqkv_decode_attention", B, Hq, Hkv, d, M, nbits, num_ctas, ld_tok);
+    if (rc) return rc;
+    PQKV_CHECK_ARG(ld_recent >= 0 && ld_recent < (1 << 16),
+                   "pqkv_decode_attention: bad ld_recent");
+    PQKV_CHECK_ARG((k_cur == nullptr) == (v_cur == nullptr),
+                   "pqkv_decode_attention: k_cur and v_cur go together");
+    PQKV_CHECK_ARG((recent_k == nullptr) == (recent_v == nullptr),
+                   "pqkv_decode_attention: recent_k and recent_v go together");
+    PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS)) == 0,
+                   "pqkv_decode_attention: unknown flags");
+    if (B == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
+                   "pqkv_decode_attention: null pointer");
+    cudaStream_t st = as_stream(stream);
+    if (!is_fast_geometry(d, M, nbits)) {
+        // generic geometries: tables, split partials, then the finish kernel
+        rc = pqkv_decode_partials(q, scale, cb_k, lut_ws, B, Hq, Hkv, codes_k, codes_v, ld_tok,
+                                  n_q, cb_v, d, M, nbits, num_ctas, partials, stream);
+        if (rc) return rc;
+        return pqkv_decode_finish(partials, num_ctas, B, Hq, Hkv, d, n_q, q, scale, recent_k,
+                                  recent_v, ld_recent, n_recent, k_cur, v_cur, out, lse, merged,
+                                  stream);
+    }
+    PQKV_CHECK_ARG(counters != nullptr, "pqkv_decode_attention: null counters");
+    fast::Args a = fast_args(q, scale, cb_k, nullptr, B, Hq, Hkv, codes_k, codes_v, ld_tok, n_q,
+                             cb_v, num_ctas, partials);
+    a.counters = counters;
+    a.recent_k = recent_k;
+    a.recent_v = recent_v;
+    a.ld_recent = ld_recent;
+    a.n_recent = n_recent;
+    a.k_cur = k_cur;
+    a.v_cur = v_cur;
+    a.out = out;
+    a.lse = lse;
+    a.merged = merged;
+    a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
+    return launch_fast<true>(a, (flags & PQKV_DECODE_PDL) != 0, st, "pqkv_decode_attention");
 }
 
 extern "C" int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_heads, int d,

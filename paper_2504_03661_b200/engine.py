@@ -3,18 +3,18 @@
 The reference decodes one head of one sequence per call (attention.py:214,
 a per-head Python loop in harness.py:195-201).  Here one call covers a whole
 layer: every sequence b < B and query head hq < Hq, with GQA (query head hq
-reads KV head hq // (Hq // Hkv)).  Two launches per layer:
+reads KV head hq // (Hq // Hkv)).  One launch per layer
+(``pqkv_decode_attention``): one persistent CTA per SM builds each head's key
+LUT in shared memory (build_key_lut, attention.py:70-83) and streams the codes
+of all heads (quantized_partial, attention.py:114-166); the CTA holding a
+head's first tokens also computes the dense partial over the recent rows +
+current token (dense_partial :169-190), and the last CTA to finish a head
+merges its records in a fixed order and finalizes (:193-211, 264-274).
+With ``pdl=True`` consecutive layers overlap: a layer's grid starts loading
+its value codebook while the previous layer's last CTAs drain.
 
-1. ``pqkv_decode_partials``  one persistent CTA per SM builds each head's key
-                             LUT in shared memory (build_key_lut,
-                             attention.py:70-83) and streams the codes of all
-                             heads (quantized_partial, attention.py:114-166)
-2. ``pqkv_decode_finish``    per head: fixed-order merge of the split partials,
-                             dense partial over recent rows + current token,
-                             finalize (attention.py:169-211, 264-274)
-
-Both run on one stream with device-resident lengths, so a whole decode
-step (all layers) can be captured in a CUDA graph and replayed.
+Lengths are device-resident, so a whole decode step (all layers) can be
+captured in a CUDA graph and replayed.
 
 Multi-GPU: head/batch sharding needs no collective -- each
 rank runs ``PQDecoder`` on its own heads.  A sequence split (128K context)
@@ -39,13 +39,14 @@ class PQDecoder:
     """Decode attention for one (B, Hq, Hkv, geometry) launch shape."""
 
     def __init__(self, B: int, Hq: int, Hkv: int, config: PQConfig, device=None,
-                 num_ctas: int | None = None):
+                 num_ctas: int | None = None, pdl: bool = False, static_codebooks: bool = False):
         if Hq % Hkv:
             raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
         self.B, self.Hq, self.Hkv, self.config = B, Hq, Hkv, config
         self.ws = K.DecodeWorkspace(B, Hq, config.d, config.M, config.nbits, device=device,
                                     num_ctas=num_ctas)
         self.device = self.ws.device
+        self.pdl, self.static_codebooks = pdl, static_codebooks
 
     @property
     def num_ctas(self) -> int:
@@ -67,11 +68,11 @@ class PQDecoder:
         qf = q if (q.dtype == torch.float32 and q.is_contiguous()) else q.float().contiguous()
         if out is None and finalize:
             out = torch.empty((B, Hq, d), dtype=torch.float32, device=q.device)
-        K.decode_partials(self.ws, self.Hkv, qf.view(B * Hq, d), sc, cb_k_layout, codes_k,
-                          codes_v, n_q, cb_v_layout, stream=stream)
-        K.decode_finish(self.ws, self.Hkv, n_q, qf, sc, recent_k=recent_k, recent_v=recent_v,
-                        n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
-                        merged=merged, stream=stream)
+        K.decode_attention(self.ws, self.Hkv, qf.view(B * Hq, d), sc, cb_k_layout, codes_k,
+                           codes_v, n_q, cb_v_layout, recent_k=recent_k, recent_v=recent_v,
+                           n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
+                           merged=merged, pdl=self.pdl, static_codebooks=self.static_codebooks,
+                           stream=stream)
         return out
 
 

@@ -151,6 +151,8 @@ class DecodeWorkspace:
             self.num_ctas = num_ctas or N.decode_grid(d, M, nbits)
         nf = N.partials_floats(self.num_ctas, B, Hq, d)
         self.partials = torch.empty(nf, dtype=torch.float32, device=self.device)
+        # arrival counters of the fused launch (self-resetting)
+        self.counters = torch.zeros(B * Hq, dtype=torch.int32, device=self.device)
         # the fast path builds its tables in shared memory; other geometries
         # need a global LUT scratch
         self.lut = None if is_fast_geometry(d, M, nbits) else torch.empty(
@@ -211,6 +213,34 @@ def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, re
            ws.num_ctas if ws is not None else 0, B, Hq, Hkv, d, N.ptr(n_q), N.ptr(q),
            float(scale), N.ptr(recent_k), N.ptr(recent_v), ld_recent, N.ptr(n_recent),
            N.ptr(k_cur), N.ptr(v_cur), N.ptr(out), N.ptr(lse), N.ptr(merged),
+           N.stream_ptr(stream))
+
+
+def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout, codes_k,
+                     codes_v, n_q, cb_v_layout, recent_k=None, recent_v=None, n_recent=None,
+                     k_cur=None, v_cur=None, out=None, lse=None, merged=None, pdl: bool = False,
+                     static_codebooks: bool = False, stream=None) -> None:
+    """One fused launch per layer (m64b8): quantized span + dense window +
+    fixed-order merge + finalize for every (b, hq); other geometries fall back
+    to decode_partials + decode_finish inside the library.
+
+    q: (B*Hq, d) float32; codes (B, Hkv, cap, M); recent (B, Hkv, R, d);
+    out (B*Hq, d); lse (B*Hq,); merged (B*Hq, d+4).  pdl lets the launch
+    overlap the previous kernel's tail; static_codebooks additionally loads
+    the value codebook before waiting for it (the codebooks must then have
+    been written before the previous kernel started, e.g. at load time)."""
+    _check_codes(ws, Hkv, codes_k, codes_v)
+    ld_recent = 0
+    if recent_k is not None:
+        if recent_k.shape != recent_v.shape or recent_k.dim() != 4:
+            raise ValueError("recent_k/recent_v must both be (B, Hkv, R, d)")
+        ld_recent = recent_k.shape[2]
+    flags = (N.DECODE_PDL if pdl else 0) | (N.DECODE_STATIC_CODEBOOKS if static_codebooks else 0)
+    N.call("pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
+           ws.B, ws.Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q),
+           N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, N.ptr(recent_k), N.ptr(recent_v), ld_recent,
+           N.ptr(n_recent), N.ptr(k_cur), N.ptr(v_cur), ws.num_ctas, N.ptr(ws.partials),
+           N.ptr(ws.counters), N.ptr(out), N.ptr(lse), N.ptr(merged), flags,
            N.stream_ptr(stream))
 
 

@@ -271,6 +271,102 @@ def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+def _fused_inputs(B, Hq, Hkv, n, R, seed):
+    from paper_2504_03661_b200 import kernels as K
+    rng = np.random.default_rng(seed)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    return dict(
+        q=t(rng.standard_normal((B * Hq, 128)).astype(np.float32)),
+        cbk=K.key_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8),
+        cbv=K.value_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8),
+        ck=t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8)),
+        cv=t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8)),
+        rk=t(rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)),
+        rv=t(rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)),
+        kc=t(rng.standard_normal((B, Hkv, 128)).astype(np.float32)),
+        vc=t(rng.standard_normal((B, Hkv, 128)).astype(np.float32)))
+
+
+@pytest.mark.parametrize("pdl", [False, True])
+def test_fused_launch_matches_two_launch_path(pdl):
+    """pqkv_decode_attention (one launch: dense window by the first CTA of a
+    head, last-arriver merge) == pqkv_decode_partials + pqkv_decode_finish,
+    for out, lse and the merged record; counters return to zero."""
+    from paper_2504_03661_b200 import kernels as K
+    B, Hq, Hkv, n, R = 3, 8, 4, 9000, 32
+    x = _fused_inputs(B, Hq, Hkv, n, R, 5)
+    nq = torch.tensor([9000, 17, 0], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([31, 0, 5], dtype=torch.int32, device="cuda")
+    ws = K.DecodeWorkspace(B, Hq, 128, 64, 8)
+    sc = K.default_scale(128)
+    o1 = torch.empty((B * Hq, 128), device="cuda")
+    l1 = torch.empty(B * Hq, device="cuda")
+    m1 = torch.empty((B * Hq, 132), device="cuda")
+    K.decode_partials(ws, Hkv, x["q"], sc, x["cbk"], x["ck"], x["cv"], nq, x["cbv"])
+    K.decode_finish(ws, Hkv, nq, x["q"], sc, x["rk"], x["rv"], nr, x["kc"], x["vc"], out=o1,
+                    lse=l1, merged=m1)
+    o2, l2, m2 = torch.empty_like(o1), torch.empty_like(l1), torch.empty_like(m1)
+    for _ in range(3):  # repeated launches reuse the self-resetting counters
+        K.decode_attention(ws, Hkv, x["q"], sc, x["cbk"], x["ck"], x["cv"], nq, x["cbv"],
+                           x["rk"], x["rv"], nr, x["kc"], x["vc"], out=o2, lse=l2, merged=m2,
+                           pdl=pdl, static_codebooks=pdl)
+    torch.cuda.synchronize()
+    assert int(ws.counters.abs().sum()) == 0
+    np.testing.assert_allclose(o2.cpu().numpy(), o1.cpu().numpy(), rtol=2e-6, atol=1e-6)
+    np.testing.assert_allclose(l2.cpu().numpy(), l1.cpu().numpy(), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(m2.cpu().numpy(), m1.cpu().numpy(), rtol=2e-6, atol=1e-6)
+
+
+def test_fused_graph_replay_deterministic():
+    """A CUDA-graph-captured multi-layer step with PDL launches replays to the
+    same bits every time (fixed merge order, static work split)."""
+    from paper_2504_03661_b200 import kernels as K
+    B, Hq, Hkv, n, R, L = 1, 32, 32, 6000, 31, 3
+    xs = [_fused_inputs(B, Hq, Hkv, n, R, 40 + l) for l in range(L)]
+    nq = torch.tensor([n], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([R], dtype=torch.int32, device="cuda")
+    ws = K.DecodeWorkspace(B, Hq, 128, 64, 8)
+    outs = torch.zeros((L, B * Hq, 128), device="cuda")
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+
+    def step():
+        for l, x in enumerate(xs):
+            K.decode_attention(ws, Hkv, x["q"], K.default_scale(128), x["cbk"], x["ck"], x["cv"],
+                               nq, x["cbv"], x["rk"], x["rv"], nr, x["kc"], x["vc"],
+                               out=outs[l], pdl=True, static_codebooks=True, stream=st)
+
+    with torch.cuda.stream(st):
+        step()
+    st.synchronize()
+    ref = outs.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        step()
+    for _ in range(4):
+        outs.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(outs, ref)
+    # and against the oracle for one head of each layer
+    for l, x in enumerate(xs):
+        h = 7
+        ckr = K.relayout(x["ck"], False).cpu().numpy()
+        cvr = K.relayout(x["cv"], False).cpu().numpy()
+        want = O.decode_from_snapshot(
+            x["q"][h].cpu().numpy(), x["kc"][0, h].cpu().numpy(), x["vc"][0, h].cpu().numpy(),
+            ckr[0, h], cvr[0, h], x["rk"][0, h].cpu().numpy(), x["rv"][0, h].cpu().numpy(),
+            *_plain_codebooks(x), block_size=1 << 30)
+        np.testing.assert_allclose(ref[l, h].cpu().numpy(), want, rtol=RTOL, atol=ATOL)
+
+
+def _plain_codebooks(x):
+    """Invert the fast-path codebook layouts back to (M, ksub, dsub)."""
+    ck = x["cbk"].view(256, 64, 2).permute(1, 0, 2).contiguous().cpu().numpy()
+    cv = x["cbv"].view(2, 256, 32, 2).permute(0, 2, 1, 3).reshape(64, 256, 2).cpu().numpy()
+    return ck, cv
+
+
 def test_batched_decoder_more_ctas_than_tokens():
     got, want = _batched_case(2, 2, 2, 64, [40, 9], [1, 2], num_ctas=300)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
