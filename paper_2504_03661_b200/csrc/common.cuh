@@ -82,7 +82,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // finish kernels both evaluate this map from the device-resident n_q, so the
 // host never needs the lengths.
 constexpr int kChunkAlign = 16;
-constexpr int kSwitchCost = 1024;  // tokens-equivalent of a head switch (measured)
+#ifndef PQKV_SWITCH_COST
+#define PQKV_SWITCH_COST 1536
+#endif
+constexpr int kSwitchCost = PQKV_SWITCH_COST;  // tokens-equivalent of a head switch (measured)
 
 struct CostMap {
     int64_t total;

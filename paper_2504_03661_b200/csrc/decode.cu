@@ -63,7 +63,7 @@ constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                   // red_m[16], re
 constexpr int OFF_COL = OFF_RED + 2 * WARPS * 4;                // colsum[4][128]
 constexpr int OFF_DNS = OFF_COL + 4 * D * 4;                    // dense m[16], l[16], acc[16][128]
 constexpr int OFF_BAR = OFF_DNS + (2 * WARPS + WARPS * D) * 4;  // 2 mbarriers
-constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flag, c_first, c_last
+constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [4]
 constexpr int SMEM_BYTES = OFF_FLAG + 16;
 
 #ifdef PQKV_TRACE
@@ -300,6 +300,10 @@ __device__ __noinline__ void dense_warp_state(const float *q, float scale, const
     reinterpret_cast<float4 *>(dn_acc[warp])[lane] = da;
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // merge_partials (attention.py:193-204) of record (mb, lb, ab) into (m, l, acc);
 // identity on lb == 0
 __device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb, float lb,
@@ -361,6 +365,21 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
     }
 }
 
+// build_key_lut (attention.py:70-83) into shared memory, centroid-major:
+// lut[c][i] = scale * (q[2i] C[c][i].x + q[2i+1] C[c][i].y); thread tid owns
+// subspaces 2(tid & 31), +1 of centroids tid / 32 + 16k (cc = its codebook slice)
+__device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[16], const float *qh,
+                                          float scale, int tid) {
+    const float4 qq = __ldg(reinterpret_cast<const float4 *>(qh) + (tid & 31));
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        float2 o;
+        o.x = scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
+        o.y = scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
+        reinterpret_cast<float2 *>(lut_s)[tid + k * NT] = o;
+    }
+}
+
 // kLutFromQ: build each head's LUT in shared memory from q and the
 // centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
 // otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
@@ -406,10 +425,16 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
                          reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
         }
     }
-#ifndef PQKV_NO_PDL
+    // the first segment's slice of the key codebook (static, like the value
+    // codebook): with early_cv these loads also fly before the dependency wait
+    float4 cc0[16];
+    if (kLutFromQ && A.early_cv) {
+        const float4 *src = reinterpret_cast<const float4 *>(A.ck);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cc0[k] = __ldg(src + tid + k * NT);
+    }
     pdl_launch_dependents();
     pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
-#endif
     if (tid == 0 && !A.early_cv) {
         mbar_expect_tx(bar_cv, CV_BYTES);
 #pragma unroll
@@ -442,6 +467,19 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     bool cv_ready = false;
     uint32_t lut_phase = 0;
 
+    // first segment's table from the preloaded slice, before the segment loop
+    // (no earlier epilogue uses lut_s) -- the slice's registers are dead by the
+    // time the load ring fills
+    bool lut_prebuilt = false;
+    if (kLutFromQ && A.early_cv) {
+        int64_t p0 = pos;
+        Segment s0;
+        if (next_segment(A.n_q, A.B, A.Hq, &p0, end, &s0)) {
+            lut_build(lut_s, cc0, A.q + (int64_t)s0.bh * D, A.scale, tid);
+            lut_prebuilt = true;
+        }
+    }
+
     Segment sg;
     while (next_segment(A.n_q, A.B, A.Hq, &pos, end, &sg)) {
         const int bh = sg.bh;
@@ -452,7 +490,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         const int lo = sg.lo, hi = sg.hi;             // token range of this segment
         const int u0 = lo >> 4, u1 = (hi + 15) >> 4;  // 16-token units (absolute)
 
-        // code prefetch first: these loads fly while the LUT is built
+        const bool pre = lut_prebuilt;  // first segment's table built before the loop
+        lut_prebuilt = false;
+
+        // code prefetch: these loads fly while the LUT is built
         Unit U0, U1;
         U0.ka = U0.va = U0.kb = U0.vb = make_uint4(0, 0, 0, 0);
         U1 = U0;
@@ -461,20 +502,12 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 
         __syncthreads();  // previous segment's epilogue is done with lut_s
         if (kLutFromQ) {
-            // lut[c][i] = scale * (q[2i] C[c][i].x + q[2i+1] C[c][i].y); thread owns
-            // subspaces i0, i0+1 (i0 = 2*(tid & 31)) of centroids c = tid/32 + 16k
-            const float4 qq = __ldg(reinterpret_cast<const float4 *>(A.q + (int64_t)bh * D) +
-                                    (tid & 31));
-            const float4 *src = reinterpret_cast<const float4 *>(A.ck);
-            float4 cc[16];
+            if (!pre) {
+                float4 cc[16];
+                const float4 *src = reinterpret_cast<const float4 *>(A.ck);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                float2 o;
-                o.x = A.scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
-                o.y = A.scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
-                reinterpret_cast<float2 *>(lut_s)[tid + k * NT] = o;
+                for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
+                lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
             }
         } else if (tid == 0) {
             mbar_expect_tx(bar_lut, LUT_BYTES);
@@ -611,33 +644,43 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         }
 
     }
+#ifdef PQKV_TRACE
+    PQKV_TR(6, gtime());
+#endif
     // ---- arrivals, after all of this CTA's segments (kept out of the segment
-    // loop, whose code generation it would otherwise disturb): per segment, the
-    // last CTA to finish the head merges its records in CTA order
-    // (deterministic), then the dense record, and finalizes
+    // loop, whose code generation it would otherwise disturb).  Thread group
+    // g = tid / 128 handles segments g, g + 4, ... in parallel: its leader
+    // bumps the head's arrival counter, and the last CTA to arrive merges the
+    // head's records in CTA order (deterministic), then the dense record, and
+    // finalizes.
     if (A.counters != nullptr) {
-        if (tid < D) __threadfence();  // this CTA's record (and dense record) writers
+        __syncthreads();  // every record (and dense record) write of this CTA is done
+        const int grp = tid >> 7, gt = tid & (D - 1);
         int64_t p2 = (int64_t)cta * cm.chunk;
         Segment s2;
-        while (next_segment(A.n_q, A.B, A.Hq, &p2, end, &s2)) {
-            __syncthreads();  // flag_s reuse; fences done
-            if (tid == 0) {
-                int c_first, c_last, len;
-                head_ctas(A.n_q, A.Hq, s2.bh, cm.chunk, &c_first, &c_last, &len);
-                const int old = atomicAdd(A.counters + s2.bh, 1);
+        for (int k = 0; next_segment(A.n_q, A.B, A.Hq, &p2, end, &s2); ++k) {
+            if ((k & 3) != grp) continue;
+            int c_first, c_last, len;
+            head_ctas(A.n_q, A.Hq, s2.bh, cm.chunk, &c_first, &c_last, &len);
+            if (gt == 0) {
+                // acq_rel at gpu scope: releases this CTA's records (ordered
+                // before by the barrier, fences are cumulative) and, for the
+                // last arriver, acquires every other CTA's
+                int old;
+                asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "l"(A.counters + s2.bh)
+                             : "memory");
                 const bool last = (old == c_last - c_first);
-                if (last) {
-                    A.counters[s2.bh] = 0;  // ready for the next launch
-                    __threadfence();
-                }
-                flag_s[0] = last ? 1 : 0;
-                flag_s[1] = c_first;
-                flag_s[2] = c_last;
+                if (last) A.counters[s2.bh] = 0;  // ready for the next launch
+                flag_s[grp] = last ? 1 : 0;
             }
-            __syncthreads();
-            if (flag_s[0] && tid < D)
-                finish_head(A.parts, (int64_t)A.num_ctas + (int64_t)A.B * A.Hq, s2.bh, flag_s[1],
-                            flag_s[2], tid, A.out, A.lse, A.merged);
+            named_bar_sync(1 + grp, D);  // this group's 128 threads
+            const bool last = flag_s[grp] != 0;
+            named_bar_sync(1 + grp, D);  // flag_s[grp] is read before its reuse
+            if (last)
+                finish_head(A.parts, (int64_t)A.num_ctas + (int64_t)A.B * A.Hq, s2.bh, c_first,
+                            c_last, gt, A.out, A.lse, A.merged);
         }
     }
     if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight

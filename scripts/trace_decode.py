@@ -34,7 +34,8 @@ out = torch.empty((B_ * Hq, 128), device=dev)
 mode = os.environ.get("TRACE_MODE", "fused")
 for _ in range(5):
     if mode == "fused":
-        K.decode_attention(ws, Hkv, q, 0.088, cbk, ck, cv, nq, cbv, rk, rv, nr, out=out)
+        K.decode_attention(ws, Hkv, q, 0.088, cbk, ck, cv, nq, cbv, rk, rv, nr, out=out,
+                           static_codebooks=os.environ.get("TRACE_STATIC") == "1")
     else:
         K.decode_partials(ws, Hkv, q, 0.088, cbk, ck, cv, nq, cbv)
 torch.cuda.synchronize()
@@ -45,15 +46,22 @@ T = T.reshape(1024, 8)[: ws.num_ctas].astype(np.int64)
 ntok = np.zeros(ws.num_ctas)
 t0 = T[:, 1].min()
 rel = (T[:, 1:5] - t0) / 1e3
+seg_end = (T[:, 6] - t0) / 1e3
 print(f"mode={mode} ctas={ws.num_ctas} span_us={(T[:,4].max()-t0)/1e3:.2f}")
 for name, col in (("entry", 0), ("ready", 1), ("loop0_end", 2), ("exit", 3)):
     c = rel[:, col]
     print(f"{name:10s} min {c.min():7.2f} med {np.median(c):7.2f} max {c.max():7.2f} us")
 print("nseg hist", np.bincount(T[:, 5]))
+print(f"segs_done  min {seg_end.min():7.2f} med {np.median(seg_end):7.2f} max {seg_end.max():7.2f} us")
+for k in (1, 2):
+    sel = T[:, 5] == k
+    if sel.any():
+        print(f"  nseg={k}: segs_done med {np.median(seg_end[sel]):7.2f} max {seg_end[sel].max():7.2f}"
+              f"  exit med {np.median(rel[sel, 3]):7.2f} max {rel[sel, 3].max():7.2f}")
 order = np.argsort(rel[:, 3])
-print("slowest exits (cta, sm, nseg, entry, ready, loop0, exit):")
+print("slowest exits (cta, sm, nseg, entry, ready, loop0, segs_done, exit):")
 for i in order[-8:]:
-    print(i, T[i, 0], T[i, 5], *np.round(rel[i], 2))
+    print(i, T[i, 0], T[i, 5], *np.round(rel[i, :3], 2), round(seg_end[i], 2), round(rel[i, 3], 2))
 print("fastest exits:")
 for i in order[:8]:
     print(i, T[i, 0], T[i, 5], *np.round(rel[i], 2))
