@@ -68,14 +68,14 @@ constexpr int SMEM_BYTES = OFF_FLAG + 16;
 
 #ifdef PQKV_TRACE
 // debug-only timeline: per CTA [smid, t_entry, t_ready, t_loop0_end, t_exit, nseg]
-__device__ unsigned long long g_trace[1024 * 8];
+__device__ unsigned long long g_trace[1024 * 16];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
 #define PQKV_TR(slot, val) \
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_trace[blockIdx.x * 8 + (slot)] = (val)
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_trace[blockIdx.x * 16 + (slot)] = (val)
 #else
 #define PQKV_TR(slot, val)
 #endif
@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     }
     pdl_launch_dependents();
     pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
+#ifdef PQKV_TRACE
+    PQKV_TR(7, gtime());
+#endif
     if (tid == 0 && !A.early_cv) {
         mbar_expect_tx(bar_cv, CV_BYTES);
 #pragma unroll
@@ -477,6 +480,9 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (next_segment(A.n_q, A.B, A.Hq, &p0, end, &s0)) {
             lut_build(lut_s, cc0, A.q + (int64_t)s0.bh * D, A.scale, tid);
             lut_prebuilt = true;
+#ifdef PQKV_TRACE
+            PQKV_TR(8, gtime());  // first table built
+#endif
         }
     }
 
@@ -534,6 +540,9 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (!cv_ready) {
             mbar_wait(bar_cv, 0);
             cv_ready = true;
+#ifdef PQKV_TRACE
+            PQKV_TR(9, gtime());  // value codebook arrived
+#endif
         }
         __syncthreads();
 #ifdef PQKV_TRACE
@@ -644,6 +653,9 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         }
 
     }
+#ifdef PQKV_TRACE
+    PQKV_TR(6, gtime());
+#endif
 #ifdef PQKV_TRACE
     PQKV_TR(6, gtime());
 #endif

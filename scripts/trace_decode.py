@@ -39,10 +39,10 @@ for _ in range(5):
     else:
         K.decode_partials(ws, Hkv, q, 0.088, cbk, ck, cv, nq, cbv)
 torch.cuda.synchronize()
-T = np.zeros(1024 * 8, dtype=np.uint64)
+T = np.zeros(1024 * 16, dtype=np.uint64)
 N.load().pqkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert N.load().pqkv_debug_trace(T.ctypes.data, T.size) == 0
-T = T.reshape(1024, 8)[: ws.num_ctas].astype(np.int64)
+T = T.reshape(1024, 16)[: ws.num_ctas].astype(np.int64)
 ntok = np.zeros(ws.num_ctas)
 t0 = T[:, 1].min()
 rel = (T[:, 1:5] - t0) / 1e3
@@ -52,6 +52,11 @@ for name, col in (("entry", 0), ("ready", 1), ("loop0_end", 2), ("exit", 3)):
     c = rel[:, col]
     print(f"{name:10s} min {c.min():7.2f} med {np.median(c):7.2f} max {c.max():7.2f} us")
 print("nseg hist", np.bincount(T[:, 5]))
+for name, col in (("post_wait", 7), ("lut_pre", 8), ("dense", 10), ("cv_ready", 9)):
+    c = (T[:, col] - t0) / 1e3
+    c = c[T[:, col] > 0]
+    if len(c):
+        print(f"{name:10s} min {c.min():7.2f} med {np.median(c):7.2f} max {c.max():7.2f} us")
 print(f"segs_done  min {seg_end.min():7.2f} med {np.median(seg_end):7.2f} max {seg_end.max():7.2f} us")
 for k in (1, 2):
     sel = T[:, 5] == k
