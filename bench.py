@@ -296,10 +296,15 @@ def run_ours(args):
     g.manual_seed(1234 + rank)
     codes_k = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
     codes_v = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
-    cbk = [K.key_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS)
-           for _ in range(L)]
-    cbv = [K.value_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS)
-           for _ in range(L)]
+    # every layer's codebook layouts in one allocation (kept L2-resident below)
+    cb_words = M * 256 * 2
+    cb_all = torch.empty((L, 2, cb_words), device=dev)
+    cbk = [K.key_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS,
+                                 out=cb_all[l, 0]) for l in range(L)]
+    cbv = [K.value_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS,
+                                   half=args.f16_value_codebook,
+                                   out=None if args.f16_value_codebook else cb_all[l, 1])
+           for l in range(L)]
     rk = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
     rv = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
     n_q = torch.full((B,), n, dtype=torch.int32, device=dev)
@@ -308,12 +313,18 @@ def run_ours(args):
     kc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
     vc = torch.randn((L, B, Hkv, D), generator=g, device=dev)
     out = torch.empty((L, B, Hq, D), device=dev)
+    cb_copies = int(os.environ.get("PQKV_CB_COPIES", "1"))  # experiment: replicated codebooks
+    if cb_copies > 1:
+        cbk = [c.repeat(cb_copies) for c in cbk]
+        cbv = [c.repeat(cb_copies) for c in cbv]
     torch.cuda.synchronize()  # codebook layouts are written before any decode launch
     # one fused launch per layer; PDL lets layer l+1 load its value codebook
     # while layer l's last CTAs drain (codebooks are static: prepared above)
     dec = PQDecoder(B, Hq, Hkv, cfg, device=dev, pdl=not args.no_pdl,
                     static_codebooks=not args.no_pdl)
     stream = torch.cuda.Stream(device=dev)
+    if not args.no_l2_persist:
+        N.call("pqkv_l2_persist", N.ptr(cb_all), cb_all.numel() * 4, 1.0, N.stream_ptr(stream))
 
     def step():
         for l in range(L):
@@ -451,6 +462,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-encode", action="store_true")
+    ap.add_argument("--no-l2-persist", action="store_true",
+                    help="do not pin the codebooks in L2 (persisting access-policy window)")
+    ap.add_argument("--f16-value-codebook", action="store_true",
+                    help="fp16 value-codebook mode (stated tolerance, DESIGN.md)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

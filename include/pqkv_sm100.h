@@ -94,6 +94,19 @@ int pqkv_prepare_key_codebook(const float *cb_k, int d, int M, int nbits,
                               float *out, void *stream);
 int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits,
                                 float *out, void *stream);
+/* The same re-layout with fp16 entries ([2][256][32] half2, 64 KiB; round to
+ * nearest) for decode launches with PQKV_DECODE_F16_VALUE_CODEBOOK: 4-byte
+ * shared-memory gathers instead of 8 (no reference counterpart -- a stated
+ * tolerance mode; products and sums stay fp32). */
+int pqkv_prepare_value_codebook_f16(const float *cb_v, int d, int M, int nbits,
+                                    void *out, void *stream);
+
+/* Keep [base, base + bytes) -- e.g. every layer's codebook layouts in one
+ * allocation -- resident in L2 for kernels launched on `stream` (and graphs
+ * captured from it): sets the persisting-L2 carve-out and the stream's access
+ * policy window (hitProp persisting, missProp streaming).  base == NULL
+ * clears it.  No reference counterpart (a B200 memory-placement knob). */
+int pqkv_l2_persist(const void *base, size_t bytes, float hit_ratio, void *stream);
 
 /* Number of persistent CTAs pqkv_decode_partials uses on the current device
  * (one per SM for the fast path); needed to size the partials buffer. */
@@ -169,6 +182,8 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              previous kernel on the stream started (e.g. at
                              load time), so they may be read before that
                              kernel finishes (with PQKV_DECODE_PDL) */
+#define PQKV_DECODE_F16_VALUE_CODEBOOK 4 /* cb_v is the fp16 layout of
+                             pqkv_prepare_value_codebook_f16 */
 
 /* One fused launch per layer: decode_step (attention.py:214-287) for every
  * (b, hq) -- pqkv_decode_partials' quantized span, the dense partial of the

@@ -18,7 +18,7 @@ from .build import LIB
 PQKV_OK, PQKV_EINVAL, PQKV_ECUDA = 0, 1, 2
 DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 PARTIAL_HEADER = 4
-DECODE_PDL, DECODE_STATIC_CODEBOOKS = 1, 2  # pqkv_decode_attention flags
+DECODE_PDL, DECODE_STATIC_CODEBOOKS, DECODE_F16_VALUE_CODEBOOK = 1, 2, 4  # decode flags
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -34,7 +34,9 @@ SIGNATURES = {
     "pqkv_reconstruct": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
     "pqkv_build_lut": (_I, [_P, _I64, _I, _P, _I, _I, _F, _P, _P]),
     "pqkv_prepare_value_codebook": (_I, [_P, _I, _I, _I, _P, _P]),
+    "pqkv_prepare_value_codebook_f16": (_I, [_P, _I, _I, _I, _P, _P]),
     "pqkv_decode_grid": (_I, [_I, _I, _I, ctypes.POINTER(_I)]),
+    "pqkv_l2_persist": (_I, [_P, ctypes.c_size_t, _F, _P]),
     "pqkv_partials_floats": (_I64, [_I, _I, _I, _I]),
     "pqkv_prepare_key_codebook": (_I, [_P, _I, _I, _I, _P, _P]),
     "pqkv_decode_partials": (_I, [_P, _F, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _I, _I, _I,

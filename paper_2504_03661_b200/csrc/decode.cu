@@ -67,15 +67,18 @@ constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flag
 constexpr int SMEM_BYTES = OFF_FLAG + 16;
 
 #ifdef PQKV_TRACE
-// debug-only timeline: per CTA [smid, t_entry, t_ready, t_loop0_end, t_exit, nseg]
-__device__ unsigned long long g_trace[1024 * 16];
+// debug-only timeline: per (launch mod 64, CTA) [smid, t_entry, t_ready,
+// t_loop0_end, t_exit, nseg, t_segs_done, t_post_wait, t_lut_pre, t_cv_ready]
+constexpr int kTraceLaunches = 64, kTraceCtas = 256;
+__device__ unsigned long long g_trace[kTraceLaunches * kTraceCtas * 16];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define PQKV_TR(slot, val) \
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_trace[blockIdx.x * 16 + (slot)] = (val)
+#define PQKV_TR(slot, val)                                                          \
+    if (threadIdx.x == 0 && blockIdx.x < kTraceCtas)                                \
+    g_trace[((A.trace_id % kTraceLaunches) * kTraceCtas + blockIdx.x) * 16 + (slot)] = (val)
 #else
 #define PQKV_TR(slot, val)
 #endif
@@ -100,6 +103,7 @@ struct Args {
     const float *k_cur, *v_cur;
     float *out, *lse, *merged;
     int early_cv;  // value codebook may be read before the grid-dependency wait
+    int trace_id;  // PQKV_TRACE builds: launch sequence number
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
@@ -127,6 +131,25 @@ __device__ __forceinline__ unsigned long long lds_cv(uint32_t a) {
     unsigned long long v;
     asm volatile("ld.shared.b64 %0, [%1+0x10400];" : "=l"(v) : "r"(a));
     return v;
+}
+
+// fp16 value codebook ([2][256][32] half2, 128-byte rows) at the same offset
+__device__ __forceinline__ uint32_t lds_cv32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1+0x10400];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// acc.xy += p * (half2) c.xy, the products and sums in fp32
+__device__ __forceinline__ void ffma2_h(unsigned long long &acc, float p, uint32_t h) {
+    float a, b;
+    asm("{\n.reg .f16 lo, hi;\nmov.b32 {lo, hi}, %2;\ncvt.f32.f16 %0, lo;\ncvt.f32.f16 %1, hi;\n}"
+        : "=f"(a), "=f"(b)
+        : "r"(h));
+    unsigned long long c, pp;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(c) : "f"(a), "f"(b));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(pp) : "f"(p));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pp), "l"(c));
 }
 
 // acc.xy += p * c.xy  (one FFMA2 with a broadcast scalar)
@@ -221,7 +244,7 @@ __device__ __forceinline__ float lut_score(const uint4 k, const uint32_t (&packK
     return (sp[0] + sp[1]) + (sp[2] + sp[3]);
 }
 
-template <bool kMask>
+template <bool kMask, bool kHalfCV>
 __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
                                              const uint32_t (&packK)[8],
                                              const uint32_t (&packV)[8], bool okA, bool okB) {
@@ -231,12 +254,10 @@ __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
     sb += __shfl_xor_sync(0xffffffffu, sb, 1);
     sa += __shfl_xor_sync(0xffffffffu, sa, 2);
     sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-    if (kMask) {
-        if (!okA && !okB) return;
-        if (!okA) sa = -INFINITY;
-        if (!okB) sb = -INFINITY;
-    }
-    const float mx = fmaxf(sa, sb);
+    // masked tokens take p = 0 without a branch (a branch in the unit body
+    // makes the compiler drain the ring's pending loads); only the rare
+    // running-max increase branches
+    const float mx = fmaxf(kMask && !okA ? -INFINITY : sa, kMask && !okB ? -INFINITY : sb);
     if (mx > S.m) {
         const float f = fast_exp2((S.m - mx) * kLog2e);
         S.l *= f;
@@ -244,17 +265,24 @@ __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
         for (int k = 0; k < 16; ++k) fmul2(S.acc[k], f);
         S.m = mx;
     }
-    const float pa = fast_exp2((sa - S.m) * kLog2e);
-    const float pb = fast_exp2((sb - S.m) * kLog2e);
+    const float pa = (kMask && !okA) ? 0.f : fast_exp2((sa - S.m) * kLog2e);
+    const float pb = (kMask && !okB) ? 0.f : fast_exp2((sb - S.m) * kLog2e);
     S.l += pa + pb;
     const uint32_t wa[4] = {U.va.x, U.va.y, U.va.z, U.va.w};
     const uint32_t wb[4] = {U.vb.x, U.vb.y, U.vb.z, U.vb.w};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const unsigned long long ca = lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
-        const unsigned long long cb = lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
-        ffma2(S.acc[j], pa, ca);
-        ffma2(S.acc[j], pb, cb);
+        if (kHalfCV) {  // 4-byte gathers: address = PRMT(...) >> 1 (128-byte rows)
+            const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)) >> 1);
+            const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)) >> 1);
+            ffma2_h(S.acc[j], pa, ca);
+            ffma2_h(S.acc[j], pb, cb);
+        } else {
+            const unsigned long long ca = lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+            const unsigned long long cb = lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+            ffma2(S.acc[j], pa, ca);
+            ffma2(S.acc[j], pb, cb);
+        }
     }
 }
 
@@ -383,8 +411,13 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[16], 
 // kLutFromQ: build each head's LUT in shared memory from q and the
 // centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
 // otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
-template <bool kLutFromQ>
+template <bool kLutFromQ, bool kHalfCV>
 __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
+    constexpr int kCvBytes = kHalfCV ? CV_BYTES / 2 : CV_BYTES;
+#ifndef PQKV_CB_COPIES
+#define PQKV_CB_COPIES 1
+#endif
+    const int cb_copy = blockIdx.x % PQKV_CB_COPIES;  // replicated codebooks (L2 hot spot)
     extern __shared__ __align__(128) unsigned char smem[];
 #ifdef PQKV_TRACE
     unsigned smid_;
@@ -402,7 +435,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + WARPS);
     int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_lut)
+    if ((sbase & 0xFFFFFFu) != kDynBase || (kHalfCV && (sbase >> 31))) __trap();  // see lds_lut
     const uint32_t cta_byte = sbase & 0xFF000000u;
     const uint32_t bar_cv = sbase + OFF_BAR;
     const uint32_t bar_lut = sbase + OFF_BAR + 8;
@@ -418,18 +451,19 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         mbar_init(bar_cv, 1);
         mbar_init(bar_lut, 1);
         if (A.early_cv) {
-            mbar_expect_tx(bar_cv, CV_BYTES);
+            mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
-            for (int c = 0; c < CV_BYTES / 16384; ++c)
+            for (int c = 0; c < kCvBytes / 16384; ++c)
                 bulk_g2s(sbase + LUT_BYTES + c * 16384,
-                         reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
+                         reinterpret_cast<const char *>(A.cv) + cb_copy * kCvBytes + c * 16384,
+                         16384, bar_cv);
         }
     }
     // the first segment's slice of the key codebook (static, like the value
     // codebook): with early_cv these loads also fly before the dependency wait
     float4 cc0[16];
     if (kLutFromQ && A.early_cv) {
-        const float4 *src = reinterpret_cast<const float4 *>(A.ck);
+        const float4 *src = reinterpret_cast<const float4 *>(A.ck) + cb_copy * (LUT_BYTES / 8);
 #pragma unroll
         for (int k = 0; k < 16; ++k) cc0[k] = __ldg(src + tid + k * NT);
     }
@@ -439,11 +473,12 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     PQKV_TR(7, gtime());
 #endif
     if (tid == 0 && !A.early_cv) {
-        mbar_expect_tx(bar_cv, CV_BYTES);
+        mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
-        for (int c = 0; c < CV_BYTES / 16384; ++c)
+        for (int c = 0; c < kCvBytes / 16384; ++c)
             bulk_g2s(sbase + LUT_BYTES + c * 16384,
-                     reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
+                     reinterpret_cast<const char *>(A.cv) + cb_copy * kCvBytes + c * 16384,
+                     16384, bar_cv);
     }
 
     // lane-constant address bytes (see header comment)
@@ -459,7 +494,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             pv |= (uint32_t)((i & 31) * 8) << (8 * e);
         }
         packK[jp] = pk | cta_byte;
-        packV[jp] = pv | ((uint32_t)(q4 >> 1) << 16) | cta_byte;
+        // fp16 codebook: the address is this PRMT result >> 1, so the CTA byte
+        // rides pre-shifted
+        packV[jp] = pv | ((uint32_t)(q4 >> 1) << 16) |
+                    (kHalfCV ? ((cta_byte >> 24) << 25) : cta_byte);
     }
 
     const CostMap cm = cost_map(A.n_q, A.B, A.Hq, A.num_ctas);
@@ -510,7 +548,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (kLutFromQ) {
             if (!pre) {
                 float4 cc[16];
-                const float4 *src = reinterpret_cast<const float4 *>(A.ck);
+                const float4 *src = reinterpret_cast<const float4 *>(A.ck) + cb_copy * (LUT_BYTES / 8);
 #pragma unroll
                 for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
                 lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
@@ -584,6 +622,27 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         // static 2-unit (32-token) register ring per warp: no register moves, a
         // pending load is only waited for when its unit is processed
         int u = u0 + warp;
+#ifndef PQKV_BRANCHY_LOOP
+        // straight-line steady state: the warp's unit count rounded up to the
+        // ring depth, every unit processed masked (units past the segment
+        // load nothing and contribute p = 0)
+        const int nunits = max(0, (u1 - u0 - warp + WARPS - 1) / WARPS);
+        for (int trip = 0; trip < (nunits + 1) / 2; ++trip) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
+#define PQKV_STEP(UX)                                                                   \
+    {                                                                                   \
+        const int ta = (u << 4) + slot;                                                 \
+        process_unit<true, kHalfCV>(UX, S, packK, packV, ta >= lo && ta < hi,          \
+                                    ta + 8 >= lo && ta + 8 < hi);                       \
+        load_unit(UX, kbase, vbase, u + 2 * WARPS, slot, lo, hi);                       \
+        u += WARPS;                                                                     \
+    }
+            PQKV_STEP(U0)
+            PQKV_STEP(U1)
+#undef PQKV_STEP
+        }
+#else
         while (true) {
             // pin the lane-constant address words in registers (no remat)
 #pragma unroll
@@ -591,10 +650,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #define PQKV_STEP(UX)                                                                   \
     if (u >= u1) break;                                                                 \
     if ((u << 4) >= lo && (u << 4) + 16 <= hi) {                                        \
-        process_unit<false>(UX, S, packK, packV, true, true);                           \
+        process_unit<false, kHalfCV>(UX, S, packK, packV, true, true);                  \
     } else {                                                                            \
         const int ta = (u << 4) + slot;                                                 \
-        process_unit<true>(UX, S, packK, packV, ta >= lo && ta < hi,                    \
+        process_unit<true, kHalfCV>(UX, S, packK, packV, ta >= lo && ta < hi,          \
                            ta + 8 >= lo && ta + 8 < hi);                                \
     }                                                                                   \
     load_unit(UX, kbase, vbase, u + 2 * WARPS, slot, lo, hi);                           \
@@ -603,6 +662,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             PQKV_STEP(U1)
 #undef PQKV_STEP
         }
+#endif
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
 #ifdef PQKV_TRACE
@@ -1055,7 +1115,7 @@ extern "C" int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas) {
 }
 
 #ifdef PQKV_TRACE
-extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {
+extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {  // n <= 64 * 256 * 16
     return cudaMemcpyFromSymbol(host, fast::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
                ? 0 : 2;
 }
@@ -1076,18 +1136,22 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
     return PQKV_OK;
 }
 
-template <bool kLutFromQ>
+template <bool kLutFromQ, bool kHalfCV = false>
 static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
     static int attr_set[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = fast::decode_partials_m64b8<kLutFromQ>;
+    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV>;
     if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              fast::SMEM_BYTES);
         if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
         if (dev < 64) attr_set[dev] = 1;
     }
+#ifdef PQKV_TRACE
+    static int trace_seq = 0;
+    const_cast<fast::Args &>(args).trace_id = trace_seq++;
+#endif
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(args.num_ctas);
     cfg.blockDim = dim3(fast::NT);
@@ -1222,7 +1286,8 @@ extern "C" int pqkv_decode_attention(
                    "pqkv_decode_attention: k_cur and v_cur go together");
     PQKV_CHECK_ARG((recent_k == nullptr) == (recent_v == nullptr),
                    "pqkv_decode_attention: recent_k and recent_v go together");
-    PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS)) == 0,
+    PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
+                              PQKV_DECODE_F16_VALUE_CODEBOOK)) == 0,
                    "pqkv_decode_attention: unknown flags");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
@@ -1251,7 +1316,10 @@ extern "C" int pqkv_decode_attention(
     a.lse = lse;
     a.merged = merged;
     a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
-    return launch_fast<true>(a, (flags & PQKV_DECODE_PDL) != 0, st, "pqkv_decode_attention");
+    const bool pdl = (flags & PQKV_DECODE_PDL) != 0;
+    if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK)
+        return launch_fast<true, true>(a, pdl, st, "pqkv_decode_attention");
+    return launch_fast<true, false>(a, pdl, st, "pqkv_decode_attention");
 }
 
 extern "C" int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_heads, int d,

@@ -1,6 +1,8 @@
 // Small per-step / per-load kernels: key lookup tables, the value-codebook
 // re-layout for the fast path, reconstruct (test helper), the reference's
 // lower-seam kernels (_kernels.py), and the library's error/version plumbing.
+#include <cuda_fp16.h>
+
 #include <cstdarg>
 
 #include "common.cuh"
@@ -54,6 +56,14 @@ __global__ void prepare_cv_kernel(const float2 *__restrict__ cb_v, float2 *__res
     if (idx >= 64 * 256) return;
     const int i = idx >> 8, c = idx & 255;
     out[((i >> 5) * 256 + c) * 32 + (i & 31)] = cb_v[idx];
+}
+
+// Value codebook -> [half][c][32] half2 (round to nearest) for the fp16 mode.
+__global__ void prepare_cv_f16_kernel(const float2 *__restrict__ cb_v, __half2 *__restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over (i, c)
+    if (idx >= 64 * 256) return;
+    const int i = idx >> 8, c = idx & 255;
+    out[((i >> 5) * 256 + c) * 32 + (i & 31)] = __float22half2_rn(cb_v[idx]);
 }
 
 // Key codebook -> centroid-major [c][i] float2 for the in-kernel LUT build.
@@ -141,6 +151,38 @@ extern "C" int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int 
     PQKV_CHECK_ARG(cb_v && out, "pqkv_prepare_value_codebook: null pointer");
     prepare_cv_kernel<<<64, 256, 0, as_stream(stream)>>>((const float2 *)cb_v, (float2 *)out);
     return launch_status("pqkv_prepare_value_codebook");
+}
+
+extern "C" int pqkv_prepare_value_codebook_f16(const float *cb_v, int d, int M, int nbits,
+                                               void *out, void *stream) {
+    PQKV_CHECK_ARG(is_fast_geometry(d, M, nbits),
+                   "pqkv_prepare_value_codebook_f16: only the m64b8 (d=128) geometry");
+    PQKV_CHECK_ARG(cb_v && out, "pqkv_prepare_value_codebook_f16: null pointer");
+    prepare_cv_f16_kernel<<<64, 256, 0, as_stream(stream)>>>((const float2 *)cb_v,
+                                                              (__half2 *)out);
+    return launch_status("pqkv_prepare_value_codebook_f16");
+}
+
+extern "C" int pqkv_l2_persist(const void *base, size_t bytes, float hit_ratio, void *stream) {
+    PQKV_CHECK_ARG(hit_ratio >= 0.f && hit_ratio <= 1.f, "pqkv_l2_persist: hit_ratio out of [0, 1]");
+    int dev = 0, max_persist = 0, max_window = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess)
+        return fail(PQKV_ECUDA, "pqkv_l2_persist: device query failed");
+    const size_t window = bytes < (size_t)max_window ? bytes : (size_t)max_window;
+    const size_t carve = window < (size_t)max_persist ? window : (size_t)max_persist;
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, base ? carve : 0);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "pqkv_l2_persist: %s", cudaGetErrorString(e));
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    v.accessPolicyWindow.num_bytes = base ? window : 0;
+    v.accessPolicyWindow.hitRatio = hit_ratio;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    e = cudaStreamSetAttribute(as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &v);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "pqkv_l2_persist: %s", cudaGetErrorString(e));
+    return PQKV_OK;
 }
 
 extern "C" int pqkv_prepare_key_codebook(const float *cb_k, int d, int M, int nbits, float *out,

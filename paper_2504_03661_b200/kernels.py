@@ -115,25 +115,45 @@ def is_fast_geometry(d: int, M: int, nbits: int) -> bool:
     return d == 128 and M == 64 and nbits == 8
 
 
-def key_codebook_layout(cb_k: torch.Tensor, nbits: int, stream=None) -> torch.Tensor:
-    """The key codebook as the decode kernel reads it (centroid-major for m64b8)."""
+def _layout_out(out, n: int, dtype, device):
+    if out is None:
+        return torch.empty(n, dtype=dtype, device=device)
+    if out.numel() != n or out.dtype != dtype or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous {dtype} buffer of {n} elements")
+    return out
+
+
+def key_codebook_layout(cb_k: torch.Tensor, nbits: int, stream=None, out=None) -> torch.Tensor:
+    """The key codebook as the decode kernel reads it (centroid-major for m64b8).
+    `out` may place it in a caller buffer (e.g. one allocation for all layers,
+    kept L2-resident with pqkv_l2_persist)."""
     M, ksub, dsub = cb_k.shape
     cb_k = _contig(cb_k.float())
     if not is_fast_geometry(M * dsub, M, nbits):
         return cb_k
-    out = torch.empty(M * ksub * dsub, dtype=torch.float32, device=cb_k.device)
+    out = _layout_out(out, M * ksub * dsub, torch.float32, cb_k.device)
     N.call("pqkv_prepare_key_codebook", N.ptr(cb_k), M * dsub, M, nbits, N.ptr(out),
            N.stream_ptr(stream))
     return out
 
 
-def value_codebook_layout(cb_v: torch.Tensor, nbits: int, stream=None) -> torch.Tensor:
-    """The value codebook as the decode kernel reads it (re-laid out for m64b8)."""
+def value_codebook_layout(cb_v: torch.Tensor, nbits: int, stream=None,
+                          half: bool = False, out=None) -> torch.Tensor:
+    """The value codebook as the decode kernel reads it (re-laid out for m64b8).
+    half=True: the fp16 layout for decode_attention(..., f16_value_codebook=True)
+    (4-byte gathers; a stated-tolerance mode)."""
     M, ksub, dsub = cb_v.shape
     cb_v = _contig(cb_v.float())
+    if half:
+        if not is_fast_geometry(M * dsub, M, nbits):
+            raise ValueError("the fp16 value-codebook mode exists only for m64b8")
+        out = _layout_out(out, M * ksub * dsub, torch.float16, cb_v.device)
+        N.call("pqkv_prepare_value_codebook_f16", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
+               N.stream_ptr(stream))
+        return out
     if not is_fast_geometry(M * dsub, M, nbits):
         return cb_v
-    out = torch.empty(M * ksub * dsub, dtype=torch.float32, device=cb_v.device)
+    out = _layout_out(out, M * ksub * dsub, torch.float32, cb_v.device)
     N.call("pqkv_prepare_value_codebook", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
            N.stream_ptr(stream))
     return out
@@ -236,6 +256,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
             raise ValueError("recent_k/recent_v must both be (B, Hkv, R, d)")
         ld_recent = recent_k.shape[2]
     flags = (N.DECODE_PDL if pdl else 0) | (N.DECODE_STATIC_CODEBOOKS if static_codebooks else 0)
+    if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
+        flags |= N.DECODE_F16_VALUE_CODEBOOK
     N.call("pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
            ws.B, ws.Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q),
            N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, N.ptr(recent_k), N.ptr(recent_v), ld_recent,

@@ -1,0 +1,59 @@
+"""Diagnostic: per-layer / per-CTA timeline of the decode kernel inside the
+bench's graph-replayed 32-layer step (library built with -DPQKV_TRACE).
+usage (GPU box): python scripts/trace_graph.py [bench flags...]"""
+import ctypes, os, subprocess, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2504_03661_b200 import build as B
+lib = os.path.join(B.OUT_DIR, "libpqkv_sm100_trace.so")
+if not os.path.exists(lib):
+    B.build(force=True, lib=lib, defines=("PQKV_TRACE",))
+os.environ["PQKV_SM100_LIB"] = lib
+import torch
+from paper_2504_03661_b200 import kernels as K, _native as N
+from paper_2504_03661_b200.engine import PQDecoder, random_codes
+from paper_2504_03661_b200.pq_core import PQConfig
+dev = torch.device("cuda", 0)
+L, Bb, Hq, Hkv, n, R = 32, 1, 32, 32, 32768, 31
+g = torch.Generator(device=dev); g.manual_seed(0)
+ck = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
+cv = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
+cbk = [K.key_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8) for _ in range(L)]
+cbv = [K.value_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8) for _ in range(L)]
+q = torch.randn((L, Bb, Hq, 128), generator=g, device=dev)
+rk = torch.randn((L, Bb, Hkv, R, 128), generator=g, device=dev); rv = torch.randn_like(rk)
+kc = torch.randn((L, Bb, Hkv, 128), generator=g, device=dev); vc = torch.randn_like(kc)
+nq = torch.full((Bb,), n, dtype=torch.int32, device=dev); nr = torch.full((Bb,), R, dtype=torch.int32, device=dev)
+out = torch.empty((L, Bb, Hq, 128), device=dev)
+torch.cuda.synchronize()
+dec = PQDecoder(Bb, Hq, Hkv, PQConfig(128, 64, 8), device=dev, pdl=True, static_codebooks=True)
+st = torch.cuda.Stream()
+def step():
+    for l in range(L):
+        dec(q[l], ck[l], cv[l], nq, cbk[l], cbv[l], rk[l], rv[l], nr, kc[l], vc[l], out=out[l])
+with torch.cuda.stream(st):
+    step(); step()  # launches 0..63: the second step fills trace slots 32..63
+torch.cuda.synchronize()
+T = np.zeros(64 * 256 * 16, dtype=np.uint64)
+N.load().pqkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+assert N.load().pqkv_debug_trace(T.ctypes.data, T.size) == 0
+T = T.reshape(64, 256, 16)[32:64, :dec.ws.num_ctas].astype(np.int64)
+t0 = T[0, :, 1].min()
+rel = lambda c: (c - t0) / 1e3
+print(f"{'layer':>5} {'first_in':>8} {'last_in':>8} {'post_wait':>9} {'ready_med':>9} {'ready_max':>9} "
+      f"{'segs_med':>8} {'segs_max':>8} {'exit_min':>8} {'exit_max':>8}")
+prev_exit = None
+for l in range(32):
+    x = T[l]
+    print(f"{l:5d} {rel(x[:,1].min()):8.2f} {rel(x[:,1].max()):8.2f} {rel(np.median(x[:,7])):9.2f} "
+          f"{rel(np.median(x[:,2])):9.2f} {rel(x[:,2].max()):9.2f} {rel(np.median(x[:,6])):8.2f} "
+          f"{rel(x[:,6].max()):8.2f} {rel(x[:,4].min()):8.2f} {rel(x[:,4].max()):8.2f}")
+span = (T[31, :, 4].max() - T[0, :, 1].min()) / 1e3
+print(f"32 layers: {span:.1f} us -> {span/32:.2f} us/layer")
+# average phase durations per CTA
+ready = (T[:, :, 2] - T[:, :, 1]) / 1e3
+loop = (T[:, :, 6] - T[:, :, 2]) / 1e3
+fin = (T[:, :, 4] - T[:, :, 6]) / 1e3
+print(f"per CTA (median over layers/CTAs): entry->ready {np.median(ready):.2f} us, ready->segs_done {np.median(loop):.2f} us, segs_done->exit {np.median(fin):.2f} us")
+np.save(os.path.join(ROOT, "gpurun_out", "trace_graph.npy"), T)

@@ -232,7 +232,7 @@ def _oracle_heads(q, ck_codes, cv_codes, n_q, rk, rv, n_r, kcur, vcur, cents_k, 
     return out
 
 
-def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None):
+def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_cv=False):
     from paper_2504_03661_b200 import kernels as K
     from paper_2504_03661_b200.engine import PQDecoder
     import paper_2504_03661_b200 as P
@@ -251,12 +251,16 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None):
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     dec = PQDecoder(B, Hq, Hkv, cfg, num_ctas=num_ctas)
     cbk = K.key_codebook_layout(t(cents_k), 8)
-    cbv = K.value_codebook_layout(t(cents_v), 8)
+    cbv = K.value_codebook_layout(t(cents_v), 8, half=half_cv)
     dk, dv = K.relayout(t(codes_k), True), K.relayout(t(codes_v), True)  # decode layout
     out = dec(t(q), dk, dv, t(np.array(n_q, np.int32)), cbk, cbv, t(rk), t(rv),
               t(np.array(n_r, np.int32)), t(kc), t(vc))
     want = _oracle_heads(q, codes_k, codes_v, n_q, rk, rv, n_r, kc, vc, cents_k, cents_v,
                          Hq // Hkv)
+    if half_cv:  # the oracle on the fp16-rounded value codebook too
+        want16 = _oracle_heads(q, codes_k, codes_v, n_q, rk, rv, n_r, kc, vc, cents_k,
+                               cents_v.astype(np.float16).astype(np.float32), Hq // Hkv)
+        return out.cpu().numpy(), want, want16
     return out.cpu().numpy(), want
 
 
@@ -269,6 +273,22 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None):
 def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
     got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
+    (1, 4, 4, 3000, [3000], [31]),
+    (2, 8, 2, 5000, [4999, 1234], [5, 32]),
+    (3, 2, 1, 700, [0, 1, 7], [0, 3, 0]),
+])
+def test_f16_value_codebook_mode(B, Hq, Hkv, cap, n_q, n_r):
+    """PQKV_DECODE_F16_VALUE_CODEBOOK: the value codebook is stored as fp16
+    (round to nearest), products and sums stay fp32.  Stated tolerance: equal
+    to the fp64 oracle run on the fp16-rounded codebook within the exact
+    path's 1e-5, and to the fp64 oracle on the original codebook within
+    rtol 2e-3 / atol 2e-4 (the codebook rounding, 2^-12 relative per entry)."""
+    got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True)
+    np.testing.assert_allclose(got, want16, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(got, want, rtol=2e-3, atol=2e-4)
 
 
 def _fused_inputs(B, Hq, Hkv, n, R, seed):
