@@ -320,8 +320,10 @@ def run_ours(args):
     torch.cuda.synchronize()  # codebook layouts are written before any decode launch
     # one fused launch per layer; PDL lets layer l+1 load its value codebook
     # while layer l's last CTAs drain (codebooks are static: prepared above)
+    # codebooks (load time) and codes below n_q (appended by earlier steps) are
+    # not written by the kernel a launch overlaps: PDL may read them early
     dec = PQDecoder(B, Hq, Hkv, cfg, device=dev, pdl=not args.no_pdl,
-                    static_codebooks=not args.no_pdl)
+                    static_codebooks=not args.no_pdl, early_codes=not args.no_pdl)
     stream = torch.cuda.Stream(device=dev)
     if not args.no_l2_persist:
         N.call("pqkv_l2_persist", N.ptr(cb_all), cb_all.numel() * 4, 1.0, N.stream_ptr(stream))

@@ -94,10 +94,11 @@ int pqkv_prepare_key_codebook(const float *cb_k, int d, int M, int nbits,
                               float *out, void *stream);
 int pqkv_prepare_value_codebook(const float *cb_v, int d, int M, int nbits,
                                 float *out, void *stream);
-/* The same re-layout with fp16 entries ([2][256][32] half2, 64 KiB; round to
+/* The value codebook with fp16 entries ([256][2][32] half2, 64 KiB; round to
  * nearest) for decode launches with PQKV_DECODE_F16_VALUE_CODEBOOK: 4-byte
- * shared-memory gathers instead of 8 (no reference counterpart -- a stated
- * tolerance mode; products and sums stay fp32). */
+ * shared-memory gathers instead of 8 and fp16 softmax weights in mixed
+ * f16 x f16 + f32 FMAs (no reference counterpart -- a stated-tolerance mode;
+ * the sums stay fp32). */
 int pqkv_prepare_value_codebook_f16(const float *cb_v, int d, int M, int nbits,
                                     void *out, void *stream);
 
@@ -184,6 +185,12 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              kernel finishes (with PQKV_DECODE_PDL) */
 #define PQKV_DECODE_F16_VALUE_CODEBOOK 4 /* cb_v is the fp16 layout of
                              pqkv_prepare_value_codebook_f16 */
+#define PQKV_DECODE_EARLY_CODES 8 /* n_q and the codes below it were written
+                             before the previous kernel on the stream started
+                             (the codes of a decode step are appended by an
+                             earlier step), so the work split and the first
+                             code loads may precede that kernel's end (with
+                             PQKV_DECODE_PDL) */
 
 /* One fused launch per layer: decode_step (attention.py:214-287) for every
  * (b, hq) -- pqkv_decode_partials' quantized span, the dense partial of the

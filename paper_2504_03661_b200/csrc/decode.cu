@@ -55,7 +55,16 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 namespace fast {
 constexpr int M = 64, KSUB = 256, D = 128;
-constexpr int WARPS = 16, NT = WARPS * 32;  // one persistent CTA per SM
+#ifndef PQKV_WARPS
+#define PQKV_WARPS 16
+#endif
+constexpr int WARPS = PQKV_WARPS, NT = WARPS * 32;  // one persistent CTA per SM
+constexpr int NG = NT / 128;  // 128-thread groups (epilogue column parts, finishers)
+static_assert(NT % 128 == 0, "WARPS must be a multiple of 4");
+#ifndef PQKV_RING
+#define PQKV_RING 2
+#endif
+constexpr int RING = PQKV_RING;  // register ring depth (units of 16 tokens per warp)
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
 // shared-memory map (bytes from the dynamic base)
@@ -102,7 +111,8 @@ struct Args {
     const int32_t *n_recent;
     const float *k_cur, *v_cur;
     float *out, *lse, *merged;
-    int early_cv;  // value codebook may be read before the grid-dependency wait
+    int early_cv;     // codebooks may be read before the grid-dependency wait
+    int early_codes;  // n_q and the codes below it may be read before it, too
     int trace_id;  // PQKV_TRACE builds: launch sequence number
 };
 
@@ -133,23 +143,34 @@ __device__ __forceinline__ unsigned long long lds_cv(uint32_t a) {
     return v;
 }
 
-// fp16 value codebook ([2][256][32] half2, 128-byte rows) at the same offset
+// fp16 value codebook ([256][2][32] half2: 256-byte rows, subspace half in
+// byte 7 of the address) at the same offset
 __device__ __forceinline__ uint32_t lds_cv32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.b32 %0, [%1+0x10400];" : "=r"(v) : "r"(a));
     return v;
 }
 
-// acc.xy += p * (half2) c.xy, the products and sums in fp32
-__device__ __forceinline__ void ffma2_h(unsigned long long &acc, float p, uint32_t h) {
+// acc.xy += p16 * (half2) c: two mixed-precision FMAs (f16 x f16 products
+// are exact in fp32; the sums are fp32)
+__device__ __forceinline__ void fhfma2(unsigned long long &acc, uint16_t p16, uint32_t h) {
     float a, b;
-    asm("{\n.reg .f16 lo, hi;\nmov.b32 {lo, hi}, %2;\ncvt.f32.f16 %0, lo;\ncvt.f32.f16 %1, hi;\n}"
-        : "=f"(a), "=f"(b)
-        : "r"(h));
-    unsigned long long c, pp;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(c) : "f"(a), "f"(b));
-    asm("mov.b64 %0, {%1,%1};" : "=l"(pp) : "f"(p));
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pp), "l"(c));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(acc));
+    asm("{\n.reg .f16 lo, hi, pp;\nmov.b32 {lo, hi}, %2;\nmov.b16 pp, %3;\n"
+        "fma.rn.f32.f16 %0, lo, pp, %0;\nfma.rn.f32.f16 %1, hi, pp, %1;\n}"
+        : "+f"(a), "+f"(b)
+        : "r"(h), "h"(p16));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(acc) : "f"(a), "f"(b));
+}
+__device__ __forceinline__ uint16_t f2h(float x) {
+    uint16_t h;
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(x));
+    return h;
+}
+__device__ __forceinline__ float h2f(uint16_t h) {
+    float x;
+    asm("cvt.f32.f16 %0, %1;" : "=f"(x) : "h"(h));
+    return x;
 }
 
 // acc.xy += p * c.xy  (one FFMA2 with a broadcast scalar)
@@ -265,18 +286,25 @@ __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
         for (int k = 0; k < 16; ++k) fmul2(S.acc[k], f);
         S.m = mx;
     }
-    const float pa = (kMask && !okA) ? 0.f : fast_exp2((sa - S.m) * kLog2e);
-    const float pb = (kMask && !okB) ? 0.f : fast_exp2((sb - S.m) * kLog2e);
+    float pa = (kMask && !okA) ? 0.f : fast_exp2((sa - S.m) * kLog2e);
+    float pb = (kMask && !okB) ? 0.f : fast_exp2((sb - S.m) * kLog2e);
+    uint16_t pa16 = 0, pb16 = 0;
+    if (kHalfCV) {  // fp16 weights for the mixed-precision FMAs; l sums the same weights
+        pa16 = f2h(pa);
+        pb16 = f2h(pb);
+        pa = h2f(pa16);
+        pb = h2f(pb16);
+    }
     S.l += pa + pb;
     const uint32_t wa[4] = {U.va.x, U.va.y, U.va.z, U.va.w};
     const uint32_t wb[4] = {U.vb.x, U.vb.y, U.vb.z, U.vb.w};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (kHalfCV) {  // 4-byte gathers: address = PRMT(...) >> 1 (128-byte rows)
-            const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)) >> 1);
-            const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)) >> 1);
-            ffma2_h(S.acc[j], pa, ca);
-            ffma2_h(S.acc[j], pb, cb);
+        if (kHalfCV) {  // 4-byte gathers
+            const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+            const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+            fhfma2(S.acc[j], pa16, ca);
+            fhfma2(S.acc[j], pb16, cb);
         } else {
             const unsigned long long ca = lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
             const unsigned long long cb = lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
@@ -435,7 +463,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + WARPS);
     int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    if ((sbase & 0xFFFFFFu) != kDynBase || (kHalfCV && (sbase >> 31))) __trap();  // see lds_lut
+    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_lut)
     const uint32_t cta_byte = sbase & 0xFF000000u;
     const uint32_t bar_cv = sbase + OFF_BAR;
     const uint32_t bar_lut = sbase + OFF_BAR + 8;
@@ -450,7 +478,11 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     if (tid == 0) {
         mbar_init(bar_cv, 1);
         mbar_init(bar_lut, 1);
+#ifdef PQKV_DIAG_NOCV
+        if (false) {
+#else
         if (A.early_cv) {
+#endif
             mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
             for (int c = 0; c < kCvBytes / 16384; ++c)
@@ -462,15 +494,53 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     // the first segment's slice of the key codebook (static, like the value
     // codebook): with early_cv these loads also fly before the dependency wait
     float4 cc0[16];
-    if (kLutFromQ && A.early_cv) {
+#ifndef PQKV_CK_PRELOAD
+#define PQKV_CK_PRELOAD 0
+#endif
+    if (kLutFromQ && A.early_cv && PQKV_CK_PRELOAD) {
         const float4 *src = reinterpret_cast<const float4 *>(A.ck) + cb_copy * (LUT_BYTES / 8);
 #pragma unroll
         for (int k = 0; k < 16; ++k) cc0[k] = __ldg(src + tid + k * NT);
     }
+    const int cta = blockIdx.x;
+    const int group = A.Hq / A.Hkv;
+    // The first segment's code ring.  With early_codes (n_q and the codes
+    // below it were written before the previous kernel on the stream started)
+    // the cost map and these loads are issued before the grid-dependency wait;
+    // otherwise right after it, ahead of the table build, so the ring's DRAM
+    // latency overlaps the build.
+    Unit Ur[RING];
+#pragma unroll
+    for (int rr = 0; rr < RING; ++rr) Ur[rr].ka = Ur[rr].va = Ur[rr].kb = Ur[rr].vb = make_uint4(0, 0, 0, 0);
+    CostMap cm;
+    Segment s0;
+    bool have_s0 = false;
+    int64_t pos = 0, end = 0;
+    auto first_ring = [&]() {
+        cm = cost_map(A.n_q, A.B, A.Hq, A.num_ctas);
+        pos = (int64_t)cta * cm.chunk;
+        end = min(pos + cm.chunk, cm.total);
+        int64_t p0 = pos;
+        have_s0 = next_segment(A.n_q, A.B, A.Hq, &p0, end, &s0);
+        if (have_s0) {
+            const int b = s0.bh / A.Hq, hkv = (s0.bh - b * A.Hq) / group;
+            const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
+            const int u0 = s0.lo >> 4;
+#pragma unroll
+            for (int rr = 0; rr < RING; ++rr)
+                load_unit(Ur[rr], A.codes_k + head_off + q4 * 16, A.codes_v + head_off + q4 * 16,
+                          u0 + warp + rr * WARPS, slot, s0.lo, s0.hi);
+        }
+    };
+    if (A.early_codes) first_ring();
     pdl_launch_dependents();
     pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
 #ifdef PQKV_TRACE
     PQKV_TR(7, gtime());
+#endif
+    if (!A.early_codes) first_ring();
+#ifdef PQKV_TRACE
+    PQKV_TR(10, gtime());  // cost map read, first ring issued
 #endif
     if (tid == 0 && !A.early_cv) {
         mbar_expect_tx(bar_cv, kCvBytes);
@@ -491,39 +561,31 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             const int j = 2 * jp + e;
             const int i = 16 * q4 + ((j + r) & 15);
             pk |= (uint32_t)(i * 4) << (8 * e);
-            pv |= (uint32_t)((i & 31) * 8) << (8 * e);
+            // fp32: [half][c][32] float2 -> half << 16 | code << 8 | slot * 8;
+            // fp16: [c][half][32] half2 -> code << 8 | half << 7 | slot * 4
+            pv |= (uint32_t)(kHalfCV ? (q4 >> 1) * 128 + (i & 31) * 4 : (i & 31) * 8) << (8 * e);
         }
         packK[jp] = pk | cta_byte;
-        // fp16 codebook: the address is this PRMT result >> 1, so the CTA byte
-        // rides pre-shifted
-        packV[jp] = pv | ((uint32_t)(q4 >> 1) << 16) |
-                    (kHalfCV ? ((cta_byte >> 24) << 25) : cta_byte);
+        packV[jp] = pv | (kHalfCV ? 0u : (uint32_t)(q4 >> 1) << 16) | cta_byte;
     }
 
-    const CostMap cm = cost_map(A.n_q, A.B, A.Hq, A.num_ctas);
-    const int cta = blockIdx.x;
-    int64_t pos = (int64_t)cta * cm.chunk;
-    const int64_t end = min(pos + cm.chunk, cm.total);
-    const int group = A.Hq / A.Hkv;
     bool cv_ready = false;
     uint32_t lut_phase = 0;
 
     // first segment's table from the preloaded slice, before the segment loop
-    // (no earlier epilogue uses lut_s) -- the slice's registers are dead by the
-    // time the load ring fills
+    // (no earlier epilogue uses lut_s)
     bool lut_prebuilt = false;
-    if (kLutFromQ && A.early_cv) {
-        int64_t p0 = pos;
-        Segment s0;
-        if (next_segment(A.n_q, A.B, A.Hq, &p0, end, &s0)) {
-            lut_build(lut_s, cc0, A.q + (int64_t)s0.bh * D, A.scale, tid);
-            lut_prebuilt = true;
-#ifdef PQKV_TRACE
-            PQKV_TR(8, gtime());  // first table built
+    if (kLutFromQ && A.early_cv && PQKV_CK_PRELOAD && have_s0) {
+#ifndef PQKV_DIAG_NOLUT
+        lut_build(lut_s, cc0, A.q + (int64_t)s0.bh * D, A.scale, tid);
 #endif
-        }
+        lut_prebuilt = true;
+#ifdef PQKV_TRACE
+        PQKV_TR(8, gtime());  // first table built
+#endif
     }
 
+    bool ring_loaded = have_s0;  // the first segment's ring is in flight
     Segment sg;
     while (next_segment(A.n_q, A.B, A.Hq, &pos, end, &sg)) {
         const int bh = sg.bh;
@@ -538,13 +600,20 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         lut_prebuilt = false;
 
         // code prefetch: these loads fly while the LUT is built
-        Unit U0, U1;
-        U0.ka = U0.va = U0.kb = U0.vb = make_uint4(0, 0, 0, 0);
-        U1 = U0;
-        load_unit(U0, kbase, vbase, u0 + warp, slot, lo, hi);
-        load_unit(U1, kbase, vbase, u0 + warp + WARPS, slot, lo, hi);
+        if (!ring_loaded) {
+#pragma unroll
+            for (int rr = 0; rr < RING; ++rr)
+                load_unit(Ur[rr], kbase, vbase, u0 + warp + rr * WARPS, slot, lo, hi);
+        }
+        ring_loaded = false;
+#ifdef PQKV_TRACE
+        if (nseg_ == 0) PQKV_TR(11, gtime());  // ring loads issued
+#endif
 
         __syncthreads();  // previous segment's epilogue is done with lut_s
+#ifdef PQKV_TRACE
+        if (nseg_ == 0) PQKV_TR(12, gtime());
+#endif
         if (kLutFromQ) {
             if (!pre) {
                 float4 cc[16];
@@ -571,10 +640,16 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (do_dense)
             dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent, A.k_cur,
                              A.v_cur, A.Hkv, bh, b, hkv, warp, lane, dn_m, dn_l, dn_acc);
+#ifdef PQKV_TRACE
+        if (nseg_ == 0) PQKV_TR(13, gtime());
+#endif
         if (!kLutFromQ) {
             mbar_wait(bar_lut, lut_phase);
             lut_phase ^= 1u;
         }
+#ifdef PQKV_DIAG_NOCV
+        cv_ready = true;
+#endif
         if (!cv_ready) {
             mbar_wait(bar_cv, 0);
             cv_ready = true;
@@ -619,50 +694,27 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) S.acc[k] = 0ull;
 
-        // static 2-unit (32-token) register ring per warp: no register moves, a
-        // pending load is only waited for when its unit is processed
+        // static RING-unit register ring per warp: no register moves, a pending
+        // load is only waited for when its unit is processed.  Straight-line
+        // steady state: the warp's unit count rounded up to the ring depth,
+        // every unit processed masked (units past the segment load nothing and
+        // contribute p = 0) -- a branch in the body would make the compiler
+        // drain the ring's pending loads.
         int u = u0 + warp;
-#ifndef PQKV_BRANCHY_LOOP
-        // straight-line steady state: the warp's unit count rounded up to the
-        // ring depth, every unit processed masked (units past the segment
-        // load nothing and contribute p = 0)
         const int nunits = max(0, (u1 - u0 - warp + WARPS - 1) / WARPS);
-        for (int trip = 0; trip < (nunits + 1) / 2; ++trip) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
-#define PQKV_STEP(UX)                                                                   \
-    {                                                                                   \
-        const int ta = (u << 4) + slot;                                                 \
-        process_unit<true, kHalfCV>(UX, S, packK, packV, ta >= lo && ta < hi,          \
-                                    ta + 8 >= lo && ta + 8 < hi);                       \
-        load_unit(UX, kbase, vbase, u + 2 * WARPS, slot, lo, hi);                       \
-        u += WARPS;                                                                     \
-    }
-            PQKV_STEP(U0)
-            PQKV_STEP(U1)
-#undef PQKV_STEP
-        }
-#else
-        while (true) {
+        for (int trip = 0; trip < (nunits + RING - 1) / RING; ++trip) {
             // pin the lane-constant address words in registers (no remat)
 #pragma unroll
             for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
-#define PQKV_STEP(UX)                                                                   \
-    if (u >= u1) break;                                                                 \
-    if ((u << 4) >= lo && (u << 4) + 16 <= hi) {                                        \
-        process_unit<false, kHalfCV>(UX, S, packK, packV, true, true);                  \
-    } else {                                                                            \
-        const int ta = (u << 4) + slot;                                                 \
-        process_unit<true, kHalfCV>(UX, S, packK, packV, ta >= lo && ta < hi,          \
-                           ta + 8 >= lo && ta + 8 < hi);                                \
-    }                                                                                   \
-    load_unit(UX, kbase, vbase, u + 2 * WARPS, slot, lo, hi);                           \
-    u += WARPS;
-            PQKV_STEP(U0)
-            PQKV_STEP(U1)
-#undef PQKV_STEP
+#pragma unroll
+            for (int rr = 0; rr < RING; ++rr) {
+                const int ta = (u << 4) + slot;
+                process_unit<true, kHalfCV>(Ur[rr], S, packK, packV, ta >= lo && ta < hi,
+                                            ta + 8 >= lo && ta + 8 < hi);
+                load_unit(Ur[rr], kbase, vbase, u + RING * WARPS, slot, lo, hi);
+                u += WARPS;
+            }
         }
-#endif
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
 #ifdef PQKV_TRACE
@@ -691,7 +743,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         }
         __syncthreads();
         {
-            const int col = tid & (D - 1), part = tid >> 7;
+            const int col = tid & (D - 1), part = tid >> 7;  // NG parts of 32 rows
             float cs = 0.f;
 #pragma unroll 8
             for (int rr = part * 32; rr < part * 32 + 32; ++rr) cs += lut_s[rr * D + col];
@@ -700,7 +752,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         __syncthreads();
         if (tid < D) {
             float *rec = A.parts + ((int64_t)cta + bh) * (D + kPS);
-            rec[kPS + tid] = (colsum[0][tid] + colsum[1][tid]) + (colsum[2][tid] + colsum[3][tid]);
+            float a = colsum[0][tid];
+#pragma unroll
+            for (int pp = 1; pp < NG; ++pp) a += colsum[pp][tid];
+            rec[kPS + tid] = a;
             if (tid == 0) {
                 float L = 0.f;
 #pragma unroll
@@ -731,7 +786,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         int64_t p2 = (int64_t)cta * cm.chunk;
         Segment s2;
         for (int k = 0; next_segment(A.n_q, A.B, A.Hq, &p2, end, &s2); ++k) {
-            if ((k & 3) != grp) continue;
+            if (k % NG != grp) continue;
             int c_first, c_last, len;
             head_ctas(A.n_q, A.Hq, s2.bh, cm.chunk, &c_first, &c_last, &len);
             if (gt == 0) {
@@ -1287,7 +1342,7 @@ extern "C" int pqkv_decode_attention(
     PQKV_CHECK_ARG((recent_k == nullptr) == (recent_v == nullptr),
                    "pqkv_decode_attention: recent_k and recent_v go together");
     PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
-                              PQKV_DECODE_F16_VALUE_CODEBOOK)) == 0,
+                              PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES)) == 0,
                    "pqkv_decode_attention: unknown flags");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
@@ -1316,6 +1371,7 @@ extern "C" int pqkv_decode_attention(
     a.lse = lse;
     a.merged = merged;
     a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
+    a.early_codes = (flags & PQKV_DECODE_EARLY_CODES) ? 1 : 0;
     const bool pdl = (flags & PQKV_DECODE_PDL) != 0;
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK)
         return launch_fast<true, true>(a, pdl, st, "pqkv_decode_attention");

@@ -58,12 +58,13 @@ __global__ void prepare_cv_kernel(const float2 *__restrict__ cb_v, float2 *__res
     out[((i >> 5) * 256 + c) * 32 + (i & 31)] = cb_v[idx];
 }
 
-// Value codebook -> [half][c][32] half2 (round to nearest) for the fp16 mode.
+// Value codebook -> [c][half][32] half2 (round to nearest) for the fp16 mode:
+// 256-byte rows, so the decode kernel forms the address with one PRMT.
 __global__ void prepare_cv_f16_kernel(const float2 *__restrict__ cb_v, __half2 *__restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over (i, c)
     if (idx >= 64 * 256) return;
     const int i = idx >> 8, c = idx & 255;
-    out[((i >> 5) * 256 + c) * 32 + (i & 31)] = __float22half2_rn(cb_v[idx]);
+    out[(c * 2 + (i >> 5)) * 32 + (i & 31)] = __float22half2_rn(cb_v[idx]);
 }
 
 // Key codebook -> centroid-major [c][i] float2 for the in-kernel LUT build.

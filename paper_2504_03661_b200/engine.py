@@ -39,14 +39,15 @@ class PQDecoder:
     """Decode attention for one (B, Hq, Hkv, geometry) launch shape."""
 
     def __init__(self, B: int, Hq: int, Hkv: int, config: PQConfig, device=None,
-                 num_ctas: int | None = None, pdl: bool = False, static_codebooks: bool = False):
+                 num_ctas: int | None = None, pdl: bool = False, static_codebooks: bool = False,
+                 early_codes: bool = False):
         if Hq % Hkv:
             raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
         self.B, self.Hq, self.Hkv, self.config = B, Hq, Hkv, config
         self.ws = K.DecodeWorkspace(B, Hq, config.d, config.M, config.nbits, device=device,
                                     num_ctas=num_ctas)
         self.device = self.ws.device
-        self.pdl, self.static_codebooks = pdl, static_codebooks
+        self.pdl, self.static_codebooks, self.early_codes = pdl, static_codebooks, early_codes
 
     @property
     def num_ctas(self) -> int:
@@ -72,6 +73,7 @@ class PQDecoder:
                            codes_v, n_q, cb_v_layout, recent_k=recent_k, recent_v=recent_v,
                            n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
                            merged=merged, pdl=self.pdl, static_codebooks=self.static_codebooks,
+                           early_codes=self.early_codes,
                            stream=stream)
         return out
 

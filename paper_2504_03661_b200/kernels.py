@@ -239,7 +239,8 @@ def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, re
 def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout, codes_k,
                      codes_v, n_q, cb_v_layout, recent_k=None, recent_v=None, n_recent=None,
                      k_cur=None, v_cur=None, out=None, lse=None, merged=None, pdl: bool = False,
-                     static_codebooks: bool = False, stream=None) -> None:
+                     static_codebooks: bool = False, early_codes: bool = False,
+                     stream=None) -> None:
     """One fused launch per layer (m64b8): quantized span + dense window +
     fixed-order merge + finalize for every (b, hq); other geometries fall back
     to decode_partials + decode_finish inside the library.
@@ -248,7 +249,9 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
     out (B*Hq, d); lse (B*Hq,); merged (B*Hq, d+4).  pdl lets the launch
     overlap the previous kernel's tail; static_codebooks additionally loads
     the value codebook before waiting for it (the codebooks must then have
-    been written before the previous kernel started, e.g. at load time)."""
+    been written before the previous kernel started, e.g. at load time);
+    early_codes likewise for n_q and the codes below it (appended by earlier
+    steps): the work split and the first code loads then precede the wait."""
     _check_codes(ws, Hkv, codes_k, codes_v)
     ld_recent = 0
     if recent_k is not None:
@@ -256,6 +259,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
             raise ValueError("recent_k/recent_v must both be (B, Hkv, R, d)")
         ld_recent = recent_k.shape[2]
     flags = (N.DECODE_PDL if pdl else 0) | (N.DECODE_STATIC_CODEBOOKS if static_codebooks else 0)
+    if early_codes:
+        flags |= N.DECODE_EARLY_CODES
     if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
         flags |= N.DECODE_F16_VALUE_CODEBOOK
     N.call("pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),

@@ -54,6 +54,44 @@ __global__ void __launch_bounds__(512, 1) reg_ring(const uint8_t *buf, int64_t b
     if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// the decode kernel's pattern: two streams per CTA (K codes and V codes of a
+// head, in different halves of the buffer); a unit = 2 x 512 B of each
+template <int D>
+__global__ void __launch_bounds__(512, 1) reg_ring_kv(const uint8_t *buf, int64_t bytes, uint32_t *sink) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t half = bytes / 2;
+    const int64_t per_cta = half / gridDim.x;
+    const uint8_t *kb = buf + per_cta * blockIdx.x + lane * 16;
+    const uint8_t *vb = kb + half;
+    const int64_t units = per_cta / 1024;
+    uint4 r[D][4];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const int64_t u = warp + d * 16;
+        if (u < units) {
+            r[d][0] = ldg_stream(kb + u * 1024); r[d][1] = ldg_stream(vb + u * 1024);
+            r[d][2] = ldg_stream(kb + u * 1024 + 512); r[d][3] = ldg_stream(vb + u * 1024 + 512);
+        }
+    }
+    for (int64_t u = warp; u < units; u += 16 * D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int64_t uu = u + d * 16;
+            if (uu < units) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc ^= r[d][k].x ^ r[d][k].y ^ r[d][k].z ^ r[d][k].w;
+                const int64_t un = uu + 16 * D;
+                if (un < units) {
+                    r[d][0] = ldg_stream(kb + un * 1024); r[d][1] = ldg_stream(vb + un * 1024);
+                    r[d][2] = ldg_stream(kb + un * 1024 + 512); r[d][3] = ldg_stream(vb + un * 1024 + 512);
+                }
+            }
+        }
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
 // CTA pair (2c, 2c+1) shares a chunk; rank r reads 32-byte half r of every
 // 64-byte row (lane l: row l >> 1 of a 16-row group, 16 bytes at 32r + 16(l & 1))
 template <int D>
@@ -163,6 +201,8 @@ int main() {
     rep("reg_ring<2>", time_it(reg_ring<2>, 512, 0, buf, bytes, sink, sms));
     rep("reg_ring<3>", time_it(reg_ring<3>, 512, 0, buf, bytes, sink, sms));
     rep("reg_ring<4>", time_it(reg_ring<4>, 512, 0, buf, bytes, sink, sms));
+    rep("reg_ring_kv<1>", time_it(reg_ring_kv<1>, 512, 0, buf, bytes, sink, sms));
+    rep("reg_ring_kv<2>", time_it(reg_ring_kv<2>, 512, 0, buf, bytes, sink, sms));
     rep("reg_ring_half<2>", time_it(reg_ring_half<2>, 512, 0, buf, bytes, sink, sms));
     rep("reg_ring_half<4>", time_it(reg_ring_half<4>, 512, 0, buf, bytes, sink, sms));
     rep("tma<4,8K>", time_it(tma_ring<4, 8192>, 544, 4 * 8192 + 256, buf, bytes, sink, sms));

@@ -6,7 +6,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2504_03661_b200 import build as B
-lib = os.path.join(B.OUT_DIR, "libpqkv_sm100_trace.so")
+lib = os.environ.get("TRACE_LIB") or os.path.join(B.OUT_DIR, "libpqkv_sm100_trace.so")
 if not os.path.exists(lib):
     B.build(force=True, lib=lib, defines=("PQKV_TRACE",))
 os.environ["PQKV_SM100_LIB"] = lib
@@ -19,26 +19,36 @@ L, Bb, Hq, Hkv, n, R = 32, 1, 32, 32, 32768, 31
 g = torch.Generator(device=dev); g.manual_seed(0)
 ck = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
 cv = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
-cbk = [K.key_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8) for _ in range(L)]
-cbv = [K.value_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8) for _ in range(L)]
+cb_all = torch.empty((L, 2, 64 * 256 * 2), device=dev)
+cbk = [K.key_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8, out=cb_all[l, 0]) for l in range(L)]
+cbv = [K.value_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8, out=cb_all[l, 1]) for l in range(L)]
 q = torch.randn((L, Bb, Hq, 128), generator=g, device=dev)
 rk = torch.randn((L, Bb, Hkv, R, 128), generator=g, device=dev); rv = torch.randn_like(rk)
 kc = torch.randn((L, Bb, Hkv, 128), generator=g, device=dev); vc = torch.randn_like(kc)
 nq = torch.full((Bb,), n, dtype=torch.int32, device=dev); nr = torch.full((Bb,), R, dtype=torch.int32, device=dev)
 out = torch.empty((L, Bb, Hq, 128), device=dev)
 torch.cuda.synchronize()
-dec = PQDecoder(Bb, Hq, Hkv, PQConfig(128, 64, 8), device=dev, pdl=True, static_codebooks=True)
+dec = PQDecoder(Bb, Hq, Hkv, PQConfig(128, 64, 8), device=dev, pdl=True, static_codebooks=True, early_codes=os.environ.get("EARLY", "1") == "1")
 st = torch.cuda.Stream()
+if os.environ.get("L2_PERSIST") == "1":
+    N.call("pqkv_l2_persist", N.ptr(cb_all), cb_all.numel() * 4, 1.0, N.stream_ptr(st))
+    print("codebooks pinned in L2")
 def step():
     for l in range(L):
         dec(q[l], ck[l], cv[l], nq, cbk[l], cbv[l], rk[l], rv[l], nr, kc[l], vc[l], out=out[l])
 with torch.cuda.stream(st):
     step(); step()  # launches 0..63: the second step fills trace slots 32..63
+if os.environ.get("GRAPH") == "1":  # replay a captured step (trace ids are baked in: 64..95 -> slots 0..31)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        step()
+    gr.replay(); gr.replay()
 torch.cuda.synchronize()
 T = np.zeros(64 * 256 * 16, dtype=np.uint64)
 N.load().pqkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert N.load().pqkv_debug_trace(T.ctypes.data, T.size) == 0
-T = T.reshape(64, 256, 16)[32:64, :dec.ws.num_ctas].astype(np.int64)
+sl = slice(0, 32) if os.environ.get("GRAPH") == "1" else slice(32, 64)
+T = T.reshape(64, 256, 16)[sl, :dec.ws.num_ctas].astype(np.int64)
 t0 = T[0, :, 1].min()
 rel = lambda c: (c - t0) / 1e3
 print(f"{'layer':>5} {'first_in':>8} {'last_in':>8} {'post_wait':>9} {'ready_med':>9} {'ready_max':>9} "
@@ -55,5 +65,8 @@ print(f"32 layers: {span:.1f} us -> {span/32:.2f} us/layer")
 ready = (T[:, :, 2] - T[:, :, 1]) / 1e3
 loop = (T[:, :, 6] - T[:, :, 2]) / 1e3
 fin = (T[:, :, 4] - T[:, :, 6]) / 1e3
+for name, c in (("post_wait", 7), ("cost_map", 10), ("lut_pre", 8), ("ring_issued", 11), ("sync1", 12), ("dense", 13), ("cv_ready", 9), ("ready", 2)):
+    v = np.median((T[4:, :, c] - T[4:, :, 7].min(axis=1, keepdims=True)) / 1e3)
+    print(f"  {name:10s} median {v:6.2f} us after the layer's first post-wait")
 print(f"per CTA (median over layers/CTAs): entry->ready {np.median(ready):.2f} us, ready->segs_done {np.median(loop):.2f} us, segs_done->exit {np.median(fin):.2f} us")
 np.save(os.path.join(ROOT, "gpurun_out", "trace_graph.npy"), T)

@@ -282,12 +282,13 @@ def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
 ])
 def test_f16_value_codebook_mode(B, Hq, Hkv, cap, n_q, n_r):
     """PQKV_DECODE_F16_VALUE_CODEBOOK: the value codebook is stored as fp16
-    (round to nearest), products and sums stay fp32.  Stated tolerance: equal
-    to the fp64 oracle run on the fp16-rounded codebook within the exact
-    path's 1e-5, and to the fp64 oracle on the original codebook within
-    rtol 2e-3 / atol 2e-4 (the codebook rounding, 2^-12 relative per entry)."""
+    and the softmax weights enter the value sums as fp16 (round to nearest,
+    2^-12 relative each); the sums and the normaliser stay fp32.  Stated
+    tolerance: vs the fp64 oracle run on the fp16-rounded codebook, rtol 1e-3
+    / atol 1e-4 (the weight rounding alone); vs the fp64 oracle on the
+    original codebook, rtol 2e-3 / atol 2e-4."""
     got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True)
-    np.testing.assert_allclose(got, want16, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(got, want16, rtol=1e-3, atol=1e-4)
     np.testing.assert_allclose(got, want, rtol=2e-3, atol=2e-4)
 
 
