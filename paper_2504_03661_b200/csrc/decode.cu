@@ -442,10 +442,7 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[16], 
 template <bool kLutFromQ, bool kHalfCV>
 __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     constexpr int kCvBytes = kHalfCV ? CV_BYTES / 2 : CV_BYTES;
-#ifndef PQKV_CB_COPIES
-#define PQKV_CB_COPIES 1
-#endif
-    const int cb_copy = blockIdx.x % PQKV_CB_COPIES;  // replicated codebooks (L2 hot spot)
+
     extern __shared__ __align__(128) unsigned char smem[];
 #ifdef PQKV_TRACE
     unsigned smid_;
@@ -478,30 +475,17 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     if (tid == 0) {
         mbar_init(bar_cv, 1);
         mbar_init(bar_lut, 1);
-#ifdef PQKV_DIAG_NOCV
-        if (false) {
-#else
         if (A.early_cv) {
-#endif
             mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
             for (int c = 0; c < kCvBytes / 16384; ++c)
                 bulk_g2s(sbase + LUT_BYTES + c * 16384,
-                         reinterpret_cast<const char *>(A.cv) + cb_copy * kCvBytes + c * 16384,
+                         reinterpret_cast<const char *>(A.cv) + c * 16384,
                          16384, bar_cv);
         }
     }
-    // the first segment's slice of the key codebook (static, like the value
-    // codebook): with early_cv these loads also fly before the dependency wait
-    float4 cc0[16];
-#ifndef PQKV_CK_PRELOAD
-#define PQKV_CK_PRELOAD 0
-#endif
-    if (kLutFromQ && A.early_cv && PQKV_CK_PRELOAD) {
-        const float4 *src = reinterpret_cast<const float4 *>(A.ck) + cb_copy * (LUT_BYTES / 8);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) cc0[k] = __ldg(src + tid + k * NT);
-    }
+    // (the key codebook slice is NOT preloaded into registers before the wait:
+    // 64 live registers across it spill the main loop -- measured)
     const int cta = blockIdx.x;
     const int group = A.Hq / A.Hkv;
     // The first segment's code ring.  With early_codes (n_q and the codes
@@ -547,7 +531,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #pragma unroll
         for (int c = 0; c < kCvBytes / 16384; ++c)
             bulk_g2s(sbase + LUT_BYTES + c * 16384,
-                     reinterpret_cast<const char *>(A.cv) + cb_copy * kCvBytes + c * 16384,
+                     reinterpret_cast<const char *>(A.cv) + c * 16384,
                      16384, bar_cv);
     }
 
@@ -572,19 +556,6 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     bool cv_ready = false;
     uint32_t lut_phase = 0;
 
-    // first segment's table from the preloaded slice, before the segment loop
-    // (no earlier epilogue uses lut_s)
-    bool lut_prebuilt = false;
-    if (kLutFromQ && A.early_cv && PQKV_CK_PRELOAD && have_s0) {
-#ifndef PQKV_DIAG_NOLUT
-        lut_build(lut_s, cc0, A.q + (int64_t)s0.bh * D, A.scale, tid);
-#endif
-        lut_prebuilt = true;
-#ifdef PQKV_TRACE
-        PQKV_TR(8, gtime());  // first table built
-#endif
-    }
-
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
     Segment sg;
     while (next_segment(A.n_q, A.B, A.Hq, &pos, end, &sg)) {
@@ -595,9 +566,6 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         const uint8_t *vbase = A.codes_v + head_off + q4 * 16;
         const int lo = sg.lo, hi = sg.hi;             // token range of this segment
         const int u0 = lo >> 4, u1 = (hi + 15) >> 4;  // 16-token units (absolute)
-
-        const bool pre = lut_prebuilt;  // first segment's table built before the loop
-        lut_prebuilt = false;
 
         // code prefetch: these loads fly while the LUT is built
         if (!ring_loaded) {
@@ -615,13 +583,14 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (nseg_ == 0) PQKV_TR(12, gtime());
 #endif
         if (kLutFromQ) {
-            if (!pre) {
-                float4 cc[16];
-                const float4 *src = reinterpret_cast<const float4 *>(A.ck) + cb_copy * (LUT_BYTES / 8);
+            float4 cc[16];
+            const float4 *src = reinterpret_cast<const float4 *>(A.ck);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
-                lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
-            }
+            for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
+            lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
+#ifdef PQKV_TRACE
+            if (nseg_ == 0) PQKV_TR(8, gtime());  // first table built
+#endif
         } else if (tid == 0) {
             mbar_expect_tx(bar_lut, LUT_BYTES);
 #pragma unroll
@@ -647,9 +616,6 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             mbar_wait(bar_lut, lut_phase);
             lut_phase ^= 1u;
         }
-#ifdef PQKV_DIAG_NOCV
-        cv_ready = true;
-#endif
         if (!cv_ready) {
             mbar_wait(bar_cv, 0);
             cv_ready = true;
