@@ -65,6 +65,11 @@ static_assert(NT % 128 == 0, "WARPS must be a multiple of 4");
 #define PQKV_RING 2
 #endif
 constexpr int RING = PQKV_RING;  // register ring depth (units of 16 tokens per warp)
+#ifndef PQKV_GROUP
+#define PQKV_GROUP 1
+#endif
+constexpr int GROUP = PQKV_GROUP;  // units processed together (key phase, one max update, value phase)
+static_assert(RING % GROUP == 0, "the ring holds whole groups");
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
 // shared-memory map (bytes from the dynamic base)
@@ -265,20 +270,36 @@ __device__ __forceinline__ float lut_score(const uint4 k, const uint32_t (&packK
     return (sp[0] + sp[1]) + (sp[2] + sp[3]);
 }
 
-template <bool kMask, bool kHalfCV>
-__device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
-                                             const uint32_t (&packK)[8],
-                                             const uint32_t (&packV)[8], bool okA, bool okB) {
-    float sa = lut_score(U.ka, packK);
-    float sb = lut_score(U.kb, packK);
-    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-    sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-    sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-    // masked tokens take p = 0 without a branch (a branch in the unit body
-    // makes the compiler drain the ring's pending loads); only the rare
-    // running-max increase branches
-    const float mx = fmaxf(kMask && !okA ? -INFINITY : sa, kMask && !okB ? -INFINITY : sb);
+// NU units (2 NU tokens per lane) in one pass: all key gathers first, one
+// running-max update, then all value gathers -- more independent work per
+// phase for the latency-bound warp.  Masked tokens (outside the segment) take
+// p = 0 without a branch (a branch in the loop body makes the compiler drain
+// the ring's pending loads); only the rare running-max increase branches.
+template <bool kHalfCV, int NU>
+__device__ __forceinline__ void process_units(const Unit *U, SlotState &S,
+                                              const uint32_t (&packK)[8],
+                                              const uint32_t (&packV)[8], const bool *okA,
+                                              const bool *okB) {
+    float sa[NU], sb[NU];
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        sa[n] = lut_score(U[n].ka, packK);
+        sb[n] = lut_score(U[n].kb, packK);
+    }
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        sa[n] += __shfl_xor_sync(0xffffffffu, sa[n], 1);
+        sb[n] += __shfl_xor_sync(0xffffffffu, sb[n], 1);
+    }
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        sa[n] += __shfl_xor_sync(0xffffffffu, sa[n], 2);
+        sb[n] += __shfl_xor_sync(0xffffffffu, sb[n], 2);
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NU; ++n)
+        mx = fmaxf(mx, fmaxf(okA[n] ? sa[n] : -INFINITY, okB[n] ? sb[n] : -INFINITY));
     if (mx > S.m) {
         const float f = fast_exp2((S.m - mx) * kLog2e);
         S.l *= f;
@@ -286,30 +307,39 @@ __device__ __forceinline__ void process_unit(const Unit &U, SlotState &S,
         for (int k = 0; k < 16; ++k) fmul2(S.acc[k], f);
         S.m = mx;
     }
-    float pa = (kMask && !okA) ? 0.f : fast_exp2((sa - S.m) * kLog2e);
-    float pb = (kMask && !okB) ? 0.f : fast_exp2((sb - S.m) * kLog2e);
-    uint16_t pa16 = 0, pb16 = 0;
-    if (kHalfCV) {  // fp16 weights for the mixed-precision FMAs; l sums the same weights
-        pa16 = f2h(pa);
-        pb16 = f2h(pb);
-        pa = h2f(pa16);
-        pb = h2f(pb16);
-    }
-    S.l += pa + pb;
-    const uint32_t wa[4] = {U.va.x, U.va.y, U.va.z, U.va.w};
-    const uint32_t wb[4] = {U.vb.x, U.vb.y, U.vb.z, U.vb.w};
+    float pa[NU], pb[NU];
+    uint16_t pa16[NU], pb16[NU];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (kHalfCV) {  // 4-byte gathers
-            const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
-            const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
-            fhfma2(S.acc[j], pa16, ca);
-            fhfma2(S.acc[j], pb16, cb);
-        } else {
-            const unsigned long long ca = lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
-            const unsigned long long cb = lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
-            ffma2(S.acc[j], pa, ca);
-            ffma2(S.acc[j], pb, cb);
+    for (int n = 0; n < NU; ++n) {
+        pa[n] = okA[n] ? fast_exp2((sa[n] - S.m) * kLog2e) : 0.f;
+        pb[n] = okB[n] ? fast_exp2((sb[n] - S.m) * kLog2e) : 0.f;
+        if (kHalfCV) {  // fp16 weights for the mixed-precision FMAs; l sums the same weights
+            pa16[n] = f2h(pa[n]);
+            pb16[n] = f2h(pb[n]);
+            pa[n] = h2f(pa16[n]);
+            pb[n] = h2f(pb16[n]);
+        }
+        S.l += pa[n] + pb[n];
+    }
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        const uint32_t wa[4] = {U[n].va.x, U[n].va.y, U[n].va.z, U[n].va.w};
+        const uint32_t wb[4] = {U[n].vb.x, U[n].vb.y, U[n].vb.z, U[n].vb.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (kHalfCV) {  // 4-byte gathers
+                const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+                const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+                fhfma2(S.acc[j], pa16[n], ca);
+                fhfma2(S.acc[j], pb16[n], cb);
+            } else {
+                const unsigned long long ca =
+                    lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+                const unsigned long long cb =
+                    lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+                ffma2(S.acc[j], pa[n], ca);
+                ffma2(S.acc[j], pb[n], cb);
+            }
         }
     }
 }
@@ -424,11 +454,23 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
 // build_key_lut (attention.py:70-83) into shared memory, centroid-major:
 // lut[c][i] = scale * (q[2i] C[c][i].x + q[2i+1] C[c][i].y); thread tid owns
 // subspaces 2(tid & 31), +1 of centroids tid / 32 + 16k (cc = its codebook slice)
-__device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[16], const float *qh,
-                                          float scale, int tid) {
+// The key codebook layout is [256][32] float4 (two subspaces per float4);
+// thread tid owns float4 slots f = tid + k * NT, i.e. subspaces 2(tid & 31),
+// +1 (NT is a multiple of 32) of centroid f / 32.
+constexpr int kLutSlots = KSUB * M / 2;  // 8192 float4 of the [256][64] float2 codebook
+constexpr int kLutIters = (kLutSlots + NT - 1) / NT;          // per thread
+__device__ __forceinline__ void lut_load(float4 (&cc)[kLutIters], const float *ck, int tid) {
+    const float4 *src = reinterpret_cast<const float4 *>(ck);
+#pragma unroll
+    for (int k = 0; k < kLutIters; ++k)
+        if (kLutSlots % NT == 0 || tid + k * NT < kLutSlots) cc[k] = __ldg(src + tid + k * NT);
+}
+__device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[kLutIters],
+                                          const float *qh, float scale, int tid) {
     const float4 qq = __ldg(reinterpret_cast<const float4 *>(qh) + (tid & 31));
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < kLutIters; ++k) {
+        if (kLutSlots % NT != 0 && tid + k * NT >= kLutSlots) break;
         float2 o;
         o.x = scale * fmaf(qq.y, cc[k].y, qq.x * cc[k].x);
         o.y = scale * fmaf(qq.w, cc[k].w, qq.z * cc[k].z);
@@ -583,10 +625,8 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (nseg_ == 0) PQKV_TR(12, gtime());
 #endif
         if (kLutFromQ) {
-            float4 cc[16];
-            const float4 *src = reinterpret_cast<const float4 *>(A.ck);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) cc[k] = __ldg(src + tid + k * NT);
+            float4 cc[kLutIters];
+            lut_load(cc, A.ck, tid);
             lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
 #ifdef PQKV_TRACE
             if (nseg_ == 0) PQKV_TR(8, gtime());  // first table built
@@ -673,12 +713,20 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
 #pragma unroll
-            for (int rr = 0; rr < RING; ++rr) {
-                const int ta = (u << 4) + slot;
-                process_unit<true, kHalfCV>(Ur[rr], S, packK, packV, ta >= lo && ta < hi,
-                                            ta + 8 >= lo && ta + 8 < hi);
-                load_unit(Ur[rr], kbase, vbase, u + RING * WARPS, slot, lo, hi);
-                u += WARPS;
+            for (int g = 0; g < RING / GROUP; ++g) {
+                bool okA[GROUP], okB[GROUP];
+#pragma unroll
+                for (int n = 0; n < GROUP; ++n) {
+                    const int ta = ((u + n * WARPS) << 4) + slot;
+                    okA[n] = ta >= lo && ta < hi;
+                    okB[n] = ta + 8 >= lo && ta + 8 < hi;
+                }
+                process_units<kHalfCV, GROUP>(Ur + g * GROUP, S, packK, packV, okA, okB);
+#pragma unroll
+                for (int n = 0; n < GROUP; ++n)
+                    load_unit(Ur[g * GROUP + n], kbase, vbase, u + (n + RING) * WARPS, slot, lo,
+                              hi);
+                u += GROUP * WARPS;
             }
         }
 
