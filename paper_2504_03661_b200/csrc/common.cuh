@@ -86,13 +86,21 @@ constexpr int kChunkAlign = 16;
 #define PQKV_SWITCH_COST 1536
 #endif
 constexpr int kSwitchCost = PQKV_SWITCH_COST;  // tokens-equivalent of a head switch (measured)
+// kDenseCost trailing units: the dense partial (recent rows + current token)
+// paid by the CTA holding the head's end, so that CTA gets fewer tokens
+#ifndef PQKV_DENSE_COST
+#define PQKV_DENSE_COST 0
+#endif
+constexpr int kDenseCost = PQKV_DENSE_COST;
 
 struct CostMap {
     int64_t total;
     int64_t chunk;
 };
 
-__device__ __forceinline__ int64_t head_span(int n) { return kSwitchCost + (int64_t)max(n, 1); }
+__device__ __forceinline__ int64_t head_span(int n) {
+    return kSwitchCost + (int64_t)max(n, 1) + kDenseCost;
+}
 
 __device__ __forceinline__ CostMap cost_map(const int32_t *__restrict__ n_q, int B, int Hq,
                                             int num_ctas) {
@@ -120,7 +128,7 @@ __device__ __forceinline__ void head_ctas(const int32_t *__restrict__ n_q, int H
                                           int64_t chunk, int *c_first, int *c_last, int *len) {
     const int64_t t0 = head_token0(n_q, Hq, bh, len);
     *c_first = (int)(t0 / chunk);
-    *c_last = (int)((t0 + max(*len, 1) - 1) / chunk);
+    *c_last = (int)((t0 + max(*len, 1) + kDenseCost - 1) / chunk);
 }
 
 struct Segment {
@@ -156,7 +164,7 @@ __device__ __forceinline__ bool next_segment(const int32_t *__restrict__ n_q, in
         *pos = seg_end;
         if (a < seg_end) {
             s->bh = b * Hq + hq;
-            s->lo = (int)(a - t0);
+            s->lo = (int)min(a - t0, (int64_t)n);  // == n inside the dense units
             s->hi = (int)min(seg_end - t0, (int64_t)n);
             s->len = n;
             s->first = (a == t0);

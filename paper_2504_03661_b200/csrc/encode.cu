@@ -113,6 +113,195 @@ __global__ void __launch_bounds__(256) encode_staged(const TX *__restrict__ x, i
     codes[code_cell(v, i, ld_codes, rot_base)] = (CT)arg;
 }
 
+// dsub == 2 (the m64b8 geometry): VPT vectors per thread share every
+// centroid read (one 16-byte + one 8-byte broadcast LDS per centroid per VPT
+// vectors), leaving four FP64 ops per (vector, centroid) for the distance:
+//   xc = x0 c0 (exact) ; xc = fma(x1, c1, xc) = round(x0 c0 + x1 c1)
+//   t  = fma(-2, xc, xx) = round(xx - 2 xc)   (2 xc is exact)
+//   d2 = t + cc
+// -- the reference's roundings in the reference's order -- then the clamp at
+// 0 and the strict first-minimum scan.
+#ifndef PQKV_ENC_VPT
+#define PQKV_ENC_VPT 4
+#endif
+#ifndef PQKV_ENC_FILTER
+#define PQKV_ENC_FILTER 1
+#endif
+template <typename TX, typename CT, int VPT>
+__global__ void __launch_bounds__(256) encode_dsub2(const TX *__restrict__ x, int64_t n,
+                                                    int64_t ld_x, const float *__restrict__ cents,
+                                                    int ksub, CT *__restrict__ codes,
+                                                    int64_t ld_codes, int64_t rot_base) {
+    extern __shared__ double sm[];
+    double2 *c_s = reinterpret_cast<double2 *>(sm);  // [ksub] (c0, c1)
+    double *cc_s = sm + 2 * (size_t)ksub;             // [ksub] c0^2 + c1^2 (numpy order)
+    const int i = blockIdx.y;
+    const float2 *ci = reinterpret_cast<const float2 *>(cents + (size_t)i * ksub * 2);
+    for (int c = threadIdx.x; c < ksub; c += blockDim.x) {
+        const float2 f = __ldg(ci + c);
+        const double a = f.x, b = f.y;
+        c_s[c] = make_double2(a, b);
+        cc_s[c] = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));  // squares exact
+    }
+    __syncthreads();
+
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x * VPT + threadIdx.x;
+    double x0[VPT], x1[VPT], xx[VPT], best[VPT];
+    int arg[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int64_t v = v0 + (int64_t)k * blockDim.x;
+        const int64_t vv = v < n ? v : n - 1;
+        x0[k] = load_x<TX>(x + vv * ld_x + (int64_t)i * 2);
+        x1[k] = load_x<TX>(x + vv * ld_x + (int64_t)i * 2 + 1);
+        xx[k] = __dadd_rn(__dmul_rn(x0[k], x0[k]), __dmul_rn(x1[k], x1[k]));
+        best[k] = INFINITY;
+        arg[k] = 0;
+    }
+#pragma unroll 2
+    for (int c = 0; c < ksub; ++c) {
+        const double2 cv = c_s[c];
+        const double cc = cc_s[c];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const double xc = __fma_rn(x1[k], cv.y, __dmul_rn(x0[k], cv.x));
+            const double d2 = fmax(__dadd_rn(__fma_rn(-2.0, xc, xx[k]), cc), 0.0);
+            if (d2 < best[k]) {
+                best[k] = d2;
+                arg[k] = c;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int64_t v = v0 + (int64_t)k * blockDim.x;
+        if (v < n) codes[code_cell(v, i, ld_codes, rot_base)] = (CT)arg[k];
+    }
+}
+
+// dsub == 2 with an fp32 filter: the FP64 pipe of this part is narrow, so the
+// scan over the centroids runs in fp32 on the direct form (x - c)^2 (no
+// cancellation) while tracking the best and second-best distance.  When the
+// two are further apart than the combined error bound of the fp32 distances
+// and of the reference's fp64 expanded form, the fp32 argmin IS the
+// reference's argmin (no other centroid can reach it, and no exact fp64 tie
+// is possible); otherwise -- near ties, exact ties, x on a centroid -- the
+// (vector, subspace) is re-scanned with the exact FP64 formula above.
+template <typename TX, typename CT, int VPT>
+__global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict__ x, int64_t n,
+                                                           int64_t ld_x,
+                                                           const float *__restrict__ cents,
+                                                           int ksub, CT *__restrict__ codes,
+                                                           int64_t ld_codes, int64_t rot_base) {
+    extern __shared__ double sm[];
+    double2 *c_s = reinterpret_cast<double2 *>(sm);                   // [ksub]
+    double *cc_s = sm + 2 * (size_t)ksub;                              // [ksub]
+    float2 *cf_s = reinterpret_cast<float2 *>(sm + 3 * (size_t)ksub);  // [ksub]
+    __shared__ float ccmax_s;
+    const int i = blockIdx.y;
+    const float2 *ci = reinterpret_cast<const float2 *>(cents + (size_t)i * ksub * 2);
+    if (threadIdx.x == 0) ccmax_s = 0.f;
+    __syncthreads();
+    float ccmax = 0.f;
+    for (int c = threadIdx.x; c < ksub; c += blockDim.x) {
+        const float2 f = __ldg(ci + c);
+        const double a = f.x, b = f.y;
+        c_s[c] = make_double2(a, b);
+        cc_s[c] = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+        cf_s[c] = f;
+        ccmax = fmaxf(ccmax, (float)cc_s[c]);
+    }
+    atomicMax(reinterpret_cast<int *>(&ccmax_s), __float_as_int(ccmax));  // non-negative floats
+    __syncthreads();
+    ccmax = ccmax_s;
+
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x * VPT + threadIdx.x;
+    float xf0[VPT], xf1[VPT], b1[VPT], b2[VPT];
+    int arg[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int64_t v = v0 + (int64_t)k * blockDim.x;
+        const int64_t vv = v < n ? v : n - 1;
+        xf0[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2);
+        xf1[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2 + 1);
+        b1[k] = INFINITY;
+        b2[k] = INFINITY;
+        arg[k] = 0;
+    }
+#pragma unroll 2
+    for (int c = 0; c < ksub; ++c) {
+        const float2 cv = cf_s[c];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const float dx = xf0[k] - cv.x, dy = xf1[k] - cv.y;
+            const float d = fmaf(dy, dy, dx * dx);
+            arg[k] = d < b1[k] ? c : arg[k];
+            b2[k] = fminf(b2[k], fmaxf(b1[k], d));
+            b1[k] = fminf(b1[k], d);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int64_t v = v0 + (int64_t)k * blockDim.x;
+        if (v >= n) continue;
+        // |d32 - d_true| <= ~4 u d_true (u = 2^-24); the reference's fp64
+        // expanded form is within ~4 * 2^-53 (|x|^2 + 2|x.c| + |c|^2) of d_true
+        const float xx = fmaf(xf1[k], xf1[k], xf0[k] * xf0[k]);
+        const float tol = 2e-6f * b1[k] + 1e-13f * (xx + ccmax) + 1e-30f;
+        int a = arg[k];
+        if (!(b2[k] > b1[k] + tol)) {  // near tie: the exact scan
+            const double x0 = (double)xf0[k], x1 = (double)xf1[k];
+            const double xxd = __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1));
+            double best = INFINITY;
+            for (int c = 0; c < ksub; ++c) {
+                const double2 cv = c_s[c];
+                const double xc = __fma_rn(x1, cv.y, __dmul_rn(x0, cv.x));
+                const double d2 = fmax(__dadd_rn(__fma_rn(-2.0, xc, xxd), cc_s[c]), 0.0);
+                if (d2 < best) {
+                    best = d2;
+                    a = c;
+                }
+            }
+        }
+        codes[code_cell(v, i, ld_codes, rot_base)] = (CT)a;
+    }
+}
+
+template <typename TX, typename CT>
+int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
+                        int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
+                        cudaStream_t st) {
+    constexpr int VPT = PQKV_ENC_VPT;
+    const size_t smem = (size_t)ksub * (3 * sizeof(double) + sizeof(float2));
+    auto k = encode_dsub2_filter<TX, CT, VPT>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
+    }
+    dim3 grid((unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)M);
+    k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes,
+                               rot_base);
+    return launch_status("pqkv_encode");
+}
+
+template <typename TX, typename CT>
+int launch_dsub2(const void *x, int64_t n, int64_t ld_x, const float *cents, int M, int ksub,
+                 void *codes, int64_t ld_codes, int64_t rot_base, cudaStream_t st) {
+    constexpr int VPT = PQKV_ENC_VPT;
+    const size_t smem = (size_t)ksub * 3 * sizeof(double);
+    auto k = encode_dsub2<TX, CT, VPT>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
+    }
+    dim3 grid((unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)M);
+    k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes,
+                               rot_base);
+    return launch_status("pqkv_encode");
+}
+
 // Any dsub: operands read from global memory (L1-resident per subspace).
 template <typename TX, typename CT>
 __global__ void __launch_bounds__(256) encode_generic(const TX *__restrict__ x, int64_t n,
@@ -175,7 +364,18 @@ int dispatch_encode(const void *x, int64_t n, int d, int64_t ld_x, const float *
     if (staged_smem <= 160 * 1024) {
         switch (dsub) {
             case 1: return launch_staged<TX, CT, 1>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
-            case 2: return launch_staged<TX, CT, 2>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
+            case 2:
+#if PQKV_ENC_VPT > 0
+#if PQKV_ENC_FILTER
+                if (ksub * 32 <= 160 * 1024)
+                    return launch_dsub2_filter<TX, CT>(x, n, ld_x, cents, M, ksub, codes,
+                                                       ld_codes, rot_base, st);
+#endif
+                if (ksub * 3 * sizeof(double) <= 160 * 1024)
+                    return launch_dsub2<TX, CT>(x, n, ld_x, cents, M, ksub, codes, ld_codes,
+                                                rot_base, st);
+#endif
+                return launch_staged<TX, CT, 2>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
             case 4: return launch_staged<TX, CT, 4>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
             case 8: return launch_staged<TX, CT, 8>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);
             case 16: return launch_staged<TX, CT, 16>(x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st);

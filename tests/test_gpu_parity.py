@@ -74,6 +74,37 @@ def test_encode_large_m64b8_vs_c_oracle():
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("scale", [1.0, 1e-3, 1e3])
+def test_encode_near_ties_vs_oracle(scale):
+    """The fp32 filter of the dsub=2 encoder hands near ties to the exact fp64
+    scan: vectors on centroids, on midpoints between centroid pairs (exact and
+    rounded ties), and nudged by a few ulps off midpoints -- bit-exact against
+    the fp64 restatement of assign_codes at three magnitudes."""
+    from paper_2504_03661_b200 import kernels as K
+    rng = np.random.default_rng(11)
+    M, ksub = 64, 256
+    cents = (rng.standard_normal((M, ksub, 2)) * scale).astype(np.float32)
+    # exact duplicate centroids: ties in fp64 -> lowest index
+    cents[:, 200] = cents[:, 17]
+    n = 3072
+    X = np.empty((n, 2 * M), dtype=np.float32)
+    for i in range(M):
+        a = rng.integers(0, ksub, n)
+        b = rng.integers(0, ksub, n)
+        ca, cb = cents[i, a].astype(np.float64), cents[i, b].astype(np.float64)
+        mid = ((ca + cb) / 2).astype(np.float32)
+        kind = np.arange(n) % 4
+        x = np.where(kind[:, None] == 0, cents[i, a], mid)
+        nudge = np.nextafter(mid, np.float32(np.inf) * np.sign(rng.standard_normal((n, 2))))
+        x = np.where(kind[:, None] == 2, nudge, x)
+        x = np.where(kind[:, None] == 3, cents[i, 17], x)
+        X[:, 2 * i: 2 * i + 2] = x
+    got = K.encode(torch.from_numpy(X).cuda(), torch.from_numpy(cents).cuda(), 8).cpu().numpy()
+    want = O.assign_codes(X, cents, 8)
+    np.testing.assert_array_equal(got, want)
+    assert (got[3::4] == 17).all()  # duplicates of centroid 17 resolve to the lower index
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_encode_half_inputs(dtype):
     """bf16/f16 rows are upcast exactly; codes equal the oracle on the upcast values."""
