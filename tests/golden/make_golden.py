@@ -215,8 +215,25 @@ def make_cache(pq_core, kv_cache):
     np.savez_compressed(os.path.join(OUT, "cache.npz"), **out)
 
 
+def make_synth(harness):
+    """The reference's synthetic KV streams (harness.py:37-93) for three specs."""
+    out = {}
+    specs = [dict(n_tokens=64, d=128, seed=0),
+             dict(n_tokens=50, d=128, seed=3, outlier_channels=[7, 63]),
+             dict(n_tokens=40, d=64, seed=9, sigma=0.5, outlier_channels=[1],
+                  outlier_rate=0.01, outlier_magnitude=30.0)]
+    for si, sp in enumerate(specs):
+        K, V = harness.synth_kv(harness.SynthSpec(**sp))
+        out[f"s{si}_K"], out[f"s{si}_V"] = K, V
+    np.savez_compressed(os.path.join(OUT, "synth.npz"), **out)
+
+
 def main():
     pq_core, attention, kv_cache, fileio, harness = _ref()
+    if "--synth-only" in sys.argv:
+        make_synth(harness)
+        return
+    make_synth(harness)
     make_encode(pq_core, harness)
     make_attention(pq_core, attention, kv_cache)
     make_fileio(pq_core, fileio)
