@@ -30,6 +30,7 @@ and ignored (the GPU split is chosen per SM count).
 
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass
 
@@ -131,6 +132,21 @@ def _decode_codes(codes: torch.Tensor, cfg) -> torch.Tensor:
     if K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits):
         return K.relayout(codes, to_decode=True)
     return codes.contiguous()
+
+
+_tls = threading.local()
+
+
+def _step_workspace(cfg, dev) -> "K.DecodeWorkspace":
+    """decode_step's single-head workspace, one per (thread, device, geometry)
+    (its arrival counters make a workspace single-stream)."""
+    cache = getattr(_tls, "ws", None)
+    if cache is None:
+        cache = _tls.ws = {}
+    key = (str(dev), cfg.d, cfg.M, cfg.nbits)
+    if key not in cache:
+        cache[key] = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
+    return cache[key]
 
 
 def _n_tensor(n: int, device) -> torch.Tensor:
@@ -278,6 +294,32 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
                    torch.float32, dev).reshape(-1)
     if kc.shape[0] != cfg.d or vc.shape[0] != cfg.d:
         raise ValueError(f"k_n/v_n width must be d={cfg.d}")
+
+    if (timings is None and hasattr(cache, "raw_snapshot")
+            and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits)):
+        # one fused launch (quantized span + recent rows + current token, merge,
+        # finalize) with a per-thread cached workspace
+        ws = _step_workspace(cfg, dev)
+        r = int(rk.shape[0])
+        out = torch.empty((1, cfg.d), dtype=torch.float32, device=dev)
+        if n_q:
+            ck = ck_raw.view(1, 1, n_q, cfg.M)
+            cv = cv_raw.view(1, 1, n_q, cfg.M)
+        else:  # nothing quantized yet: any valid buffer (no code is read)
+            ck = cv = torch.zeros((1, 1, 1, cfg.M), dtype=torch.uint8, device=dev)
+        K.decode_attention(ws, 1, q.view(1, -1), sc, cb_K.device_key_layout(dev), ck, cv,
+                           _n_tensor(n_q, dev), cb_V.device_value_layout(dev),
+                           recent_k=rk.view(1, 1, r, cfg.d) if r else None,
+                           recent_v=rv.view(1, 1, r, cfg.d) if r else None,
+                           n_recent=_n_tensor(r, dev) if r else None,
+                           k_cur=kc.view(1, 1, -1), v_cur=vc.view(1, 1, -1), out=out)
+        if counters is not None:
+            counters.lut_lookups += n_q * cfg.M
+            counters.adds += n_q * cfg.M
+            counters.code_bytes_read += 2 * n_q * cfg.M * cfg.cell_width
+            counters.dense_bytes_read += 2 * (r + 1) * cfg.d * 4
+        cache.append_decode(k_n, v_n)
+        return out[0].double().cpu().numpy() if host else out[0]
 
     t0 = time.perf_counter()
     ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
