@@ -113,7 +113,7 @@ int pqkv_l2_persist(const void *base, size_t bytes, float hit_ratio, void *strea
  * (one per SM for the fast path); needed to size the partials buffer. */
 int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas);
 
-/* Floats needed for the partials workspace: (num_ctas + 2*B*Hq) * (d + 4)
+/* Floats needed for the partials workspace: (2*num_ctas + 2*B*Hq) * (d + 4)
  * (split records, then one dense-window record per head). */
 int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d);
 
@@ -185,6 +185,10 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              kernel finishes (with PQKV_DECODE_PDL) */
 #define PQKV_DECODE_F16_VALUE_CODEBOOK 4 /* cb_v is the fp16 layout of
                              pqkv_prepare_value_codebook_f16 */
+#define PQKV_DECODE_ONE_HEAD_PER_CTA 16 /* fp16 mode with an even GQA group:
+                             keep one query head per CTA (by default a CTA
+                             serves two query heads of a KV head and shares
+                             the value gathers) */
 #define PQKV_DECODE_EARLY_CODES 8 /* n_q and the codes below it were written
                              before the previous kernel on the stream started
                              (the codes of a decode step are appended by an

@@ -59,7 +59,6 @@ constexpr int M = 64, KSUB = 256, D = 128;
 #define PQKV_WARPS 16
 #endif
 constexpr int WARPS = PQKV_WARPS, NT = WARPS * 32;  // one persistent CTA per SM
-constexpr int NG = NT / 128;  // 128-thread groups (epilogue column parts, finishers)
 static_assert(NT % 128 == 0, "WARPS must be a multiple of 4");
 #ifndef PQKV_RING
 #define PQKV_RING 2
@@ -73,10 +72,13 @@ static_assert(RING % GROUP == 0, "the ring holds whole groups");
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
 // shared-memory map (bytes from the dynamic base)
-constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                   // red_m[16], red_l[16]
-constexpr int OFF_COL = OFF_RED + 2 * WARPS * 4;                // colsum[4][128]
-constexpr int OFF_DNS = OFF_COL + 4 * D * 4;                    // dense m[16], l[16], acc[16][128]
-constexpr int OFF_BAR = OFF_DNS + (2 * WARPS + WARPS * D) * 4;  // 2 mbarriers
+// sized for up to PQKV_WARPS_MAX warps and two heads per CTA
+#define PQKV_WARPS_MAX 16
+constexpr int WMAX = PQKV_WARPS_MAX;
+constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                 // red_m[2][W], red_l[2][W]
+constexpr int OFF_COL = OFF_RED + 4 * WMAX * 4;               // colsum[2 * NG][128]
+constexpr int OFF_DNS = OFF_COL + 8 * D * 4;                  // dense m[W], l[W], acc[W][128]
+constexpr int OFF_BAR = OFF_DNS + (2 * WMAX + WMAX * D) * 4;  // 2 mbarriers
 constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [4]
 constexpr int SMEM_BYTES = OFF_FLAG + 16;
 
@@ -136,23 +138,26 @@ __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
 // in the LDS immediate, so each lookup is exactly PRMT + LDS.
 constexpr uint32_t kDynBase = 0x400;
 
-__device__ __forceinline__ float lds_lut(uint32_t a) {
+// key table of head k (of HG) at dynamic offset k * 64 KiB
+template <int IMM>
+__device__ __forceinline__ float lds_f32(uint32_t a) {
     float v;
-    asm volatile("ld.shared.f32 %0, [%1+0x400];" : "=f"(v) : "r"(a));
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(IMM));
     return v;
 }
 
+// value codebook after the HG key tables: fp32 [2][256][32] float2, or fp16
+// [256][2][32] half2 (256-byte rows, subspace half in byte 7 of the address)
+template <int HG>
 __device__ __forceinline__ unsigned long long lds_cv(uint32_t a) {
     unsigned long long v;
-    asm volatile("ld.shared.b64 %0, [%1+0x10400];" : "=l"(v) : "r"(a));
+    asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(0x400 + HG * 0x10000));
     return v;
 }
-
-// fp16 value codebook ([256][2][32] half2: 256-byte rows, subspace half in
-// byte 7 of the address) at the same offset
+template <int HG>
 __device__ __forceinline__ uint32_t lds_cv32(uint32_t a) {
     uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1+0x10400];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(0x400 + HG * 0x10000));
     return v;
 }
 
@@ -251,75 +256,88 @@ __device__ __forceinline__ void load_unit(Unit &U, const uint8_t *kbase, const u
     }
 }
 
+// Online-softmax state of one token slot for the HG query heads a CTA serves
+// (HG = 2: two query heads of one KV head share every value gather).
+template <int HG>
 struct SlotState {
-    float m, l;
-    unsigned long long acc[16];  // float2 per (rotated) subspace of this lane's quarter
+    float m[HG], l[HG];
+    unsigned long long acc[HG][16];  // float2 per (rotated) subspace of this lane's quarter
 };
 
-__device__ __forceinline__ float lut_score(const uint4 k, const uint32_t (&packK)[8]) {
+template <int HG>
+__device__ __forceinline__ void lut_score(const uint4 k, const uint32_t (&packK)[8],
+                                          float (&out)[HG]) {
     const uint32_t w[4] = {k.x, k.y, k.z, k.w};
-    float sp[4];
+    float sp[HG][4];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const float x = lds_lut(__byte_perm(w[j >> 2], packK[j >> 1], sel_for(j)));
-        if (j < 4)
-            sp[j] = x;
-        else
-            sp[j & 3] += x;
+        const uint32_t a = __byte_perm(w[j >> 2], packK[j >> 1], sel_for(j));
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            const float x = h == 0 ? lds_f32<0x400>(a) : lds_f32<0x10400>(a);
+            if (j < 4)
+                sp[h][j] = x;
+            else
+                sp[h][j & 3] += x;
+        }
     }
-    return (sp[0] + sp[1]) + (sp[2] + sp[3]);
+#pragma unroll
+    for (int h = 0; h < HG; ++h) out[h] = (sp[h][0] + sp[h][1]) + (sp[h][2] + sp[h][3]);
 }
 
 // NU units (2 NU tokens per lane) in one pass: all key gathers first, one
-// running-max update, then all value gathers -- more independent work per
-// phase for the latency-bound warp.  Masked tokens (outside the segment) take
-// p = 0 without a branch (a branch in the loop body makes the compiler drain
-// the ring's pending loads); only the rare running-max increase branches.
-template <bool kHalfCV, int NU>
-__device__ __forceinline__ void process_units(const Unit *U, SlotState &S,
+// running-max update per head, then all value gathers -- more independent
+// work per phase for the latency-bound warp.  Masked tokens (outside the
+// segment) take p = 0 without a branch (a branch in the loop body makes the
+// compiler drain the ring's pending loads); only the rare running-max
+// increase branches.
+template <bool kHalfCV, int NU, int HG>
+__device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
                                               const uint32_t (&packK)[8],
                                               const uint32_t (&packV)[8], const bool *okA,
                                               const bool *okB) {
-    float sa[NU], sb[NU];
+    float sa[NU][HG], sb[NU][HG];
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
-        sa[n] = lut_score(U[n].ka, packK);
-        sb[n] = lut_score(U[n].kb, packK);
+        lut_score<HG>(U[n].ka, packK, sa[n]);
+        lut_score<HG>(U[n].kb, packK, sb[n]);
     }
 #pragma unroll
-    for (int n = 0; n < NU; ++n) {
-        sa[n] += __shfl_xor_sync(0xffffffffu, sa[n], 1);
-        sb[n] += __shfl_xor_sync(0xffffffffu, sb[n], 1);
-    }
+    for (int off = 1; off <= 2; off <<= 1)
 #pragma unroll
-    for (int n = 0; n < NU; ++n) {
-        sa[n] += __shfl_xor_sync(0xffffffffu, sa[n], 2);
-        sb[n] += __shfl_xor_sync(0xffffffffu, sb[n], 2);
-    }
-    float mx = -INFINITY;
+        for (int n = 0; n < NU; ++n)
 #pragma unroll
-    for (int n = 0; n < NU; ++n)
-        mx = fmaxf(mx, fmaxf(okA[n] ? sa[n] : -INFINITY, okB[n] ? sb[n] : -INFINITY));
-    if (mx > S.m) {
-        const float f = fast_exp2((S.m - mx) * kLog2e);
-        S.l *= f;
+            for (int h = 0; h < HG; ++h) {
+                sa[n][h] += __shfl_xor_sync(0xffffffffu, sa[n][h], off);
+                sb[n][h] += __shfl_xor_sync(0xffffffffu, sb[n][h], off);
+            }
+    float pa[NU][HG], pb[NU][HG];
+    uint16_t pa16[NU][HG], pb16[NU][HG];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) fmul2(S.acc[k], f);
-        S.m = mx;
-    }
-    float pa[NU], pb[NU];
-    uint16_t pa16[NU], pb16[NU];
+    for (int h = 0; h < HG; ++h) {
+        float mx = -INFINITY;
 #pragma unroll
-    for (int n = 0; n < NU; ++n) {
-        pa[n] = okA[n] ? fast_exp2((sa[n] - S.m) * kLog2e) : 0.f;
-        pb[n] = okB[n] ? fast_exp2((sb[n] - S.m) * kLog2e) : 0.f;
-        if (kHalfCV) {  // fp16 weights for the mixed-precision FMAs; l sums the same weights
-            pa16[n] = f2h(pa[n]);
-            pb16[n] = f2h(pb[n]);
-            pa[n] = h2f(pa16[n]);
-            pb[n] = h2f(pb16[n]);
+        for (int n = 0; n < NU; ++n)
+            mx = fmaxf(mx, fmaxf(okA[n] ? sa[n][h] : -INFINITY, okB[n] ? sb[n][h] : -INFINITY));
+        if (mx > S.m[h]) {
+            const float f = fast_exp2((S.m[h] - mx) * kLog2e);
+            S.l[h] *= f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) fmul2(S.acc[h][k], f);
+            S.m[h] = mx;
         }
-        S.l += pa[n] + pb[n];
+#pragma unroll
+        for (int n = 0; n < NU; ++n) {
+            pa[n][h] = okA[n] ? fast_exp2((sa[n][h] - S.m[h]) * kLog2e) : 0.f;
+            pb[n][h] = okB[n] ? fast_exp2((sb[n][h] - S.m[h]) * kLog2e) : 0.f;
+            if (kHalfCV) {  // fp16 weights for the mixed-precision FMAs; l sums the same
+                pa16[n][h] = f2h(pa[n][h]);
+                pb16[n][h] = f2h(pb[n][h]);
+                pa[n][h] = h2f(pa16[n][h]);
+                pb[n][h] = h2f(pb16[n][h]);
+            }
+            S.l[h] += pa[n][h] + pb[n][h];
+        }
     }
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
@@ -327,18 +345,24 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState &S,
         const uint32_t wb[4] = {U[n].vb.x, U[n].vb.y, U[n].vb.z, U[n].vb.w};
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            if (kHalfCV) {  // 4-byte gathers
-                const uint32_t ca = lds_cv32(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
-                const uint32_t cb = lds_cv32(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
-                fhfma2(S.acc[j], pa16[n], ca);
-                fhfma2(S.acc[j], pb16[n], cb);
+            if (kHalfCV) {  // 4-byte gathers, shared by the HG heads
+                const uint32_t ca = lds_cv32<HG>(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+                const uint32_t cb = lds_cv32<HG>(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+#pragma unroll
+                for (int h = 0; h < HG; ++h) {
+                    fhfma2(S.acc[h][j], pa16[n][h], ca);
+                    fhfma2(S.acc[h][j], pb16[n][h], cb);
+                }
             } else {
                 const unsigned long long ca =
-                    lds_cv(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+                    lds_cv<HG>(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
                 const unsigned long long cb =
-                    lds_cv(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
-                ffma2(S.acc[j], pa[n], ca);
-                ffma2(S.acc[j], pb[n], cb);
+                    lds_cv<HG>(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+#pragma unroll
+                for (int h = 0; h < HG; ++h) {
+                    ffma2(S.acc[h][j], pa[n][h], ca);
+                    ffma2(S.acc[h][j], pb[n][h], cb);
+                }
             }
         }
     }
@@ -352,8 +376,8 @@ __device__ __noinline__ void dense_warp_state(const float *q, float scale, const
                                               const float *recent_v, int64_t ld_recent,
                                               const int32_t *n_recent, const float *k_cur,
                                               const float *v_cur, int Hkv, int bh, int b, int hkv,
-                                              int warp, int lane, float *dn_m, float *dn_l,
-                                              float (*dn_acc)[D]) {
+                                              int warp, int nwarps, int lane, float *dn_m,
+                                              float *dn_l, float (*dn_acc)[D]) {
     const int nr = (n_recent != nullptr && recent_k != nullptr) ? max(n_recent[b], 0) : 0;
     const int rows = nr + (k_cur != nullptr ? 1 : 0);
     const float4 qv = __ldg(reinterpret_cast<const float4 *>(q + (int64_t)bh * D) + lane);
@@ -361,7 +385,7 @@ __device__ __noinline__ void dense_warp_state(const float *q, float scale, const
     const int64_t cbase = ((int64_t)b * Hkv + hkv) * D;
     float dm = -INFINITY, dl = 0.f;
     float4 da = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int rr = warp; rr < rows; rr += WARPS) {
+    for (int rr = warp; rr < rows; rr += nwarps) {
         const float *kr = rr < nr ? recent_k + rbase + (int64_t)rr * D : k_cur + cbase;
         const float *vr = rr < nr ? recent_v + rbase + (int64_t)rr * D : v_cur + cbase;
         const float4 kk = __ldg(reinterpret_cast<const float4 *>(kr) + lane);
@@ -412,9 +436,11 @@ __device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb,
 // records in CTA order (deterministic), then its dense record, and finalizes
 // (merge_partials :193-204, finalize :207-211).  Threads tid < D, one output
 // dimension each.  Out of line: runs once per head.
-__device__ __noinline__ void finish_head(const float *parts, int64_t dense_base, int bh,
-                                         int c_first, int c_last, int tid, float *out, float *lse,
-                                         float *merged) {
+// Records of (split c, virtual head vh, head h of HG) live at HG (c + vh) + h;
+// bh is the query head (dense record dense_base + bh, outputs row bh).
+__device__ __noinline__ void finish_head(const float *parts, int64_t dense_base, int hg, int vh,
+                                         int h, int bh, int c_first, int c_last, int tid,
+                                         float *out, float *lse, float *merged) {
     const float *drec = parts + (dense_base + bh) * (D + kPS);
     // the dense record and the first batch are in flight before any is consumed
     const float dm = __ldcg(drec), dl = __ldcg(drec + 1), da = __ldcg(drec + kPS + tid);
@@ -425,7 +451,7 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (k < cnt) {
-                const float *rec = parts + ((int64_t)c0 + k + bh) * (D + kPS);
+                const float *rec = parts + ((int64_t)hg * (c0 + k + vh) + h) * (D + kPS);
                 rm[k] = __ldcg(rec);
                 rl[k] = __ldcg(rec + 1);
                 ra[k] = __ldcg(rec + kPS + tid);
@@ -458,15 +484,20 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
 // thread tid owns float4 slots f = tid + k * NT, i.e. subspaces 2(tid & 31),
 // +1 (NT is a multiple of 32) of centroid f / 32.
 constexpr int kLutSlots = KSUB * M / 2;  // 8192 float4 of the [256][64] float2 codebook
-constexpr int kLutIters = (kLutSlots + NT - 1) / NT;          // per thread
-__device__ __forceinline__ void lut_load(float4 (&cc)[kLutIters], const float *ck, int tid) {
+template <int NT>
+constexpr int lut_iters() { return (kLutSlots + NT - 1) / NT; }
+template <int NT>
+__device__ __forceinline__ void lut_load(float4 (&cc)[lut_iters<NT>()], const float *ck, int tid) {
+    constexpr int kLutIters = lut_iters<NT>();
     const float4 *src = reinterpret_cast<const float4 *>(ck);
 #pragma unroll
     for (int k = 0; k < kLutIters; ++k)
         if (kLutSlots % NT == 0 || tid + k * NT < kLutSlots) cc[k] = __ldg(src + tid + k * NT);
 }
-__device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[kLutIters],
+template <int NT>
+__device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[lut_iters<NT>()],
                                           const float *qh, float scale, int tid) {
+    constexpr int kLutIters = lut_iters<NT>();
     const float4 qq = __ldg(reinterpret_cast<const float4 *>(qh) + (tid & 31));
 #pragma unroll
     for (int k = 0; k < kLutIters; ++k) {
@@ -481,9 +512,18 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[kLutI
 // kLutFromQ: build each head's LUT in shared memory from q and the
 // centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
 // otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
-template <bool kLutFromQ, bool kHalfCV>
-__global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
+// HG = 2 (fp16 value codebook, even GQA group): a CTA serves two query heads
+// of one KV head -- a "virtual head" -- with two key tables (one PRMT per
+// code byte feeds both) and one value gather per code shared by both heads.
+// W warps per CTA.
+template <bool kLutFromQ, bool kHalfCV, int HG, int W>
+__global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A) {
+    static_assert(HG == 1 || (HG == 2 && kHalfCV && kLutFromQ), "two heads need the fp16 codebook");
+    static_assert(W <= PQKV_WARPS_MAX, "the shared-memory map is sized for PQKV_WARPS_MAX warps");
+    constexpr int WARPS = W, NT = W * 32, NG = NT / 128;
     constexpr int kCvBytes = kHalfCV ? CV_BYTES / 2 : CV_BYTES;
+    constexpr int kCvOff = HG * LUT_BYTES;  // value codebook after the key tables
+    const int Hqv = A.Hq / HG;              // virtual heads per sequence
 
     extern __shared__ __align__(128) unsigned char smem[];
 #ifdef PQKV_TRACE
@@ -495,14 +535,14 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #endif
     float *lut_s = reinterpret_cast<float *>(smem);
     float *red_m = reinterpret_cast<float *>(smem + OFF_RED);
-    float *red_l = red_m + WARPS;
+    float *red_l = red_m + 2 * WARPS;  // [HG][WARPS] each
     float(*colsum)[D] = reinterpret_cast<float(*)[D]>(smem + OFF_COL);
     float *dn_m = reinterpret_cast<float *>(smem + OFF_DNS);
     float *dn_l = dn_m + WARPS;
     float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + WARPS);
     int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_lut)
+    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_f32)
     const uint32_t cta_byte = sbase & 0xFF000000u;
     const uint32_t bar_cv = sbase + OFF_BAR;
     const uint32_t bar_lut = sbase + OFF_BAR + 8;
@@ -521,7 +561,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
             for (int c = 0; c < kCvBytes / 16384; ++c)
-                bulk_g2s(sbase + LUT_BYTES + c * 16384,
+                bulk_g2s(sbase + kCvOff + c * 16384,
                          reinterpret_cast<const char *>(A.cv) + c * 16384,
                          16384, bar_cv);
         }
@@ -543,13 +583,13 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
     bool have_s0 = false;
     int64_t pos = 0, end = 0;
     auto first_ring = [&]() {
-        cm = cost_map(A.n_q, A.B, A.Hq, A.num_ctas);
+        cm = cost_map(A.n_q, A.B, Hqv, A.num_ctas);
         pos = (int64_t)cta * cm.chunk;
         end = min(pos + cm.chunk, cm.total);
         int64_t p0 = pos;
-        have_s0 = next_segment(A.n_q, A.B, A.Hq, &p0, end, &s0);
+        have_s0 = next_segment(A.n_q, A.B, Hqv, &p0, end, &s0);
         if (have_s0) {
-            const int b = s0.bh / A.Hq, hkv = (s0.bh - b * A.Hq) / group;
+            const int b = s0.bh / Hqv, hkv = (s0.bh - b * Hqv) * HG / group;
             const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
             const int u0 = s0.lo >> 4;
 #pragma unroll
@@ -572,7 +612,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         mbar_expect_tx(bar_cv, kCvBytes);
 #pragma unroll
         for (int c = 0; c < kCvBytes / 16384; ++c)
-            bulk_g2s(sbase + LUT_BYTES + c * 16384,
+            bulk_g2s(sbase + kCvOff + c * 16384,
                      reinterpret_cast<const char *>(A.cv) + c * 16384,
                      16384, bar_cv);
     }
@@ -600,9 +640,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
     Segment sg;
-    while (next_segment(A.n_q, A.B, A.Hq, &pos, end, &sg)) {
-        const int bh = sg.bh;
-        const int b = bh / A.Hq, hq = bh - b * A.Hq, hkv = hq / group;
+    while (next_segment(A.n_q, A.B, Hqv, &pos, end, &sg)) {
+        const int vh = sg.bh;  // virtual head: query heads hq0 .. hq0 + HG - 1
+        const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
+        const int bh0 = b * A.Hq + hq0;
         const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
         const uint8_t *kbase = A.codes_k + head_off + q4 * 16;
         const uint8_t *vbase = A.codes_v + head_off + q4 * 16;
@@ -625,9 +666,12 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         if (nseg_ == 0) PQKV_TR(12, gtime());
 #endif
         if (kLutFromQ) {
-            float4 cc[kLutIters];
-            lut_load(cc, A.ck, tid);
-            lut_build(lut_s, cc, A.q + (int64_t)bh * D, A.scale, tid);
+            float4 cc[lut_iters<NT>()];
+            lut_load<NT>(cc, A.ck, tid);
+#pragma unroll
+            for (int h = 0; h < HG; ++h)
+                lut_build<NT>(lut_s + h * (LUT_BYTES / 4), cc, A.q + (int64_t)(bh0 + h) * D,
+                              A.scale, tid);
 #ifdef PQKV_TRACE
             if (nseg_ == 0) PQKV_TR(8, gtime());  // first table built
 #endif
@@ -636,7 +680,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #pragma unroll
             for (int c = 0; c < LUT_BYTES / 16384; ++c)
                 bulk_g2s(sbase + c * 16384,
-                         reinterpret_cast<const char *>(A.lut + (int64_t)bh * KSUB * M) + c * 16384,
+                         reinterpret_cast<const char *>(A.lut + (int64_t)bh0 * KSUB * M) + c * 16384,
                          16384, bar_lut);
         }
         // dense partial by the CTA holding the head's last tokens (for most CTAs
@@ -646,59 +690,70 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #else
         const bool do_dense = false;
 #endif
-        if (do_dense)
-            dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent, A.k_cur,
-                             A.v_cur, A.Hkv, bh, b, hkv, warp, lane, dn_m, dn_l, dn_acc);
-#ifdef PQKV_TRACE
-        if (nseg_ == 0) PQKV_TR(13, gtime());
-#endif
-        if (!kLutFromQ) {
-            mbar_wait(bar_lut, lut_phase);
-            lut_phase ^= 1u;
-        }
-        if (!cv_ready) {
-            mbar_wait(bar_cv, 0);
-            cv_ready = true;
-#ifdef PQKV_TRACE
-            PQKV_TR(9, gtime());  // value codebook arrived
-#endif
-        }
-        __syncthreads();
-#ifdef PQKV_TRACE
-        if (nseg_ == 0) PQKV_TR(2, gtime());
-#endif
-        if (do_dense && tid < D) {
-            // merge the 16 warps' dense states into record dense_base + bh
-            float Mx = -INFINITY;
+        const int64_t dense_base = (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq;
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w)
-                if (dn_l[w] > 0.f) Mx = fmaxf(Mx, dn_m[w]);
-            float L = 0.f, acc = 0.f;
-            if (Mx != -INFINITY) {
-#pragma unroll
-                for (int w = 0; w < WARPS; ++w) {
-                    if (dn_l[w] > 0.f) {
-                        const float f = expf(dn_m[w] - Mx);
-                        L += dn_l[w] * f;
-                        acc += dn_acc[w][tid] * f;
-                    }
+        for (int h = 0; h < HG; ++h) {
+            if (h > 0) __syncthreads();  // the previous head's merge has read dn_*
+            if (do_dense)
+                dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent,
+                                 A.k_cur, A.v_cur, A.Hkv, bh0 + h, b, hkv, warp, WARPS, lane, dn_m,
+                                 dn_l, dn_acc);
+#ifdef PQKV_TRACE
+            if (nseg_ == 0) PQKV_TR(13, gtime());
+#endif
+            if (h == 0) {
+                if (!kLutFromQ) {
+                    mbar_wait(bar_lut, lut_phase);
+                    lut_phase ^= 1u;
+                }
+                if (!cv_ready) {
+                    mbar_wait(bar_cv, 0);
+                    cv_ready = true;
+#ifdef PQKV_TRACE
+                    PQKV_TR(9, gtime());  // value codebook arrived
+#endif
                 }
             }
-            float *rec = A.parts + ((int64_t)A.num_ctas + (int64_t)A.B * A.Hq + bh) * (D + kPS);
-            rec[kPS + tid] = acc;
-            if (tid == 0) {
-                rec[0] = Mx;
-                rec[1] = L;
-                rec[2] = 0.f;
-                rec[3] = 0.f;
+            __syncthreads();
+#ifdef PQKV_TRACE
+            if (nseg_ == 0) PQKV_TR(2, gtime());
+#endif
+            if (do_dense && tid < D) {
+                // merge the warps' dense states into record dense_base + bh0 + h
+                float Mx = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < WARPS; ++w)
+                    if (dn_l[w] > 0.f) Mx = fmaxf(Mx, dn_m[w]);
+                float L = 0.f, acc = 0.f;
+                if (Mx != -INFINITY) {
+#pragma unroll
+                    for (int w = 0; w < WARPS; ++w) {
+                        if (dn_l[w] > 0.f) {
+                            const float f = expf(dn_m[w] - Mx);
+                            L += dn_l[w] * f;
+                            acc += dn_acc[w][tid] * f;
+                        }
+                    }
+                }
+                float *rec = A.parts + (dense_base + bh0 + h) * (D + kPS);
+                rec[kPS + tid] = acc;
+                if (tid == 0) {
+                    rec[0] = Mx;
+                    rec[1] = L;
+                    rec[2] = 0.f;
+                    rec[3] = 0.f;
+                }
             }
         }
 
-        SlotState S;
-        S.m = -INFINITY;
-        S.l = 0.f;
+        SlotState<HG> S;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) S.acc[k] = 0ull;
+        for (int h = 0; h < HG; ++h) {
+            S.m[h] = -INFINITY;
+            S.l[h] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) S.acc[h][k] = 0ull;
+        }
 
         // static RING-unit register ring per warp: no register moves, a pending
         // load is only waited for when its unit is processed.  Straight-line
@@ -721,7 +776,7 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
                     okA[n] = ta >= lo && ta < hi;
                     okB[n] = ta + 8 >= lo && ta + 8 < hi;
                 }
-                process_units<kHalfCV, GROUP>(Ur + g * GROUP, S, packK, packV, okA, okB);
+                process_units<kHalfCV, GROUP, HG>(Ur + g * GROUP, S, packK, packV, okA, okB);
 #pragma unroll
                 for (int n = 0; n < GROUP; ++n)
                     load_unit(Ur[g * GROUP + n], kbase, vbase, u + (n + RING) * WARPS, slot, lo,
@@ -734,53 +789,68 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
 #ifdef PQKV_TRACE
         if (nseg_++ == 0) PQKV_TR(3, gtime());
 #endif
-        float mw = S.m;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
-        if (lane == 0) red_m[warp] = mw;
+        for (int h = 0; h < HG; ++h) {
+            float mw = S.m[h];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+            if (lane == 0) red_m[h * WARPS + warp] = mw;
+        }
         __syncthreads();  // all warps are past the main loop: lut_s is free
-        float Mx = red_m[0];
+        float Mx[HG];
 #pragma unroll
-        for (int w = 1; w < WARPS; ++w) Mx = fmaxf(Mx, red_m[w]);
-        const float f = (S.m == -INFINITY) ? 0.f : fast_exp2((S.m - Mx) * kLog2e);
-        float lw = (q4 == 0) ? S.l * f : 0.f;
+        for (int h = 0; h < HG; ++h) {
+            Mx[h] = red_m[h * WARPS];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
-        if (lane == 0) red_l[warp] = lw;
-        float *rows = lut_s + (warp * 8 + slot) * D;
+            for (int w = 1; w < WARPS; ++w) Mx[h] = fmaxf(Mx[h], red_m[h * WARPS + w]);
+            const float f = (S.m[h] == -INFINITY) ? 0.f : fast_exp2((S.m[h] - Mx[h]) * kLog2e);
+            float lw = (q4 == 0) ? S.l[h] * f : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int i = 16 * q4 + ((j + r) & 15);  // decode layout: byte j <-> this subspace
-            const float2 a = unpack2(S.acc[j]);
-            rows[2 * i] = a.x * f;
-            rows[2 * i + 1] = a.y * f;
+            for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
+            if (lane == 0) red_l[h * WARPS + warp] = lw;
+            // head h's slot rows: [WARPS * 8][128] fp32 in the (now free) key tables
+            float *rows = lut_s + (h * WARPS * 8 + warp * 8 + slot) * D;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int i = 16 * q4 + ((j + r) & 15);  // decode layout: byte j <-> this subspace
+                const float2 a = unpack2(S.acc[h][j]);
+                rows[2 * i] = a.x * f;
+                rows[2 * i + 1] = a.y * f;
+            }
         }
         __syncthreads();
         {
-            const int col = tid & (D - 1), part = tid >> 7;  // NG parts of 32 rows
-            float cs = 0.f;
+            const int col = tid & (D - 1), part = tid >> 7;  // NG parts of 32 rows per head
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                float cs = 0.f;
+                const float *rows = lut_s + h * WARPS * 8 * D;
 #pragma unroll 8
-            for (int rr = part * 32; rr < part * 32 + 32; ++rr) cs += lut_s[rr * D + col];
-            colsum[part][col] = cs;
+                for (int rr = part * 32; rr < part * 32 + 32; ++rr) cs += rows[rr * D + col];
+                colsum[h * NG + part][col] = cs;
+            }
         }
         __syncthreads();
         if (tid < D) {
-            float *rec = A.parts + ((int64_t)cta + bh) * (D + kPS);
-            float a = colsum[0][tid];
 #pragma unroll
-            for (int pp = 1; pp < NG; ++pp) a += colsum[pp][tid];
-            rec[kPS + tid] = a;
-            if (tid == 0) {
-                float L = 0.f;
+            for (int h = 0; h < HG; ++h) {
+                float *rec = A.parts + ((int64_t)HG * (cta + vh) + h) * (D + kPS);
+                float a = colsum[h * NG][tid];
 #pragma unroll
-                for (int w = 0; w < WARPS; ++w) L += red_l[w];
-                rec[0] = Mx;
-                rec[1] = L;
-                rec[2] = 0.f;
-                rec[3] = 0.f;
+                for (int pp = 1; pp < NG; ++pp) a += colsum[h * NG + pp][tid];
+                rec[kPS + tid] = a;
+                if (tid == 0) {
+                    float L = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WARPS; ++w) L += red_l[h * WARPS + w];
+                    rec[0] = Mx[h];
+                    rec[1] = L;
+                    rec[2] = 0.f;
+                    rec[3] = 0.f;
+                }
             }
         }
-
     }
 #ifdef PQKV_TRACE
     PQKV_TR(6, gtime());
@@ -799,10 +869,10 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
         const int grp = tid >> 7, gt = tid & (D - 1);
         int64_t p2 = (int64_t)cta * cm.chunk;
         Segment s2;
-        for (int k = 0; next_segment(A.n_q, A.B, A.Hq, &p2, end, &s2); ++k) {
+        for (int k = 0; next_segment(A.n_q, A.B, Hqv, &p2, end, &s2); ++k) {
             if (k % NG != grp) continue;
             int c_first, c_last, len;
-            head_ctas(A.n_q, A.Hq, s2.bh, cm.chunk, &c_first, &c_last, &len);
+            head_ctas(A.n_q, Hqv, s2.bh, cm.chunk, &c_first, &c_last, &len);
             if (gt == 0) {
                 // acq_rel at gpu scope: releases this CTA's records (ordered
                 // before by the barrier, fences are cumulative) and, for the
@@ -819,9 +889,13 @@ __global__ void __launch_bounds__(NT, 1) decode_partials_m64b8(const Args A) {
             named_bar_sync(1 + grp, D);  // this group's 128 threads
             const bool last = flag_s[grp] != 0;
             named_bar_sync(1 + grp, D);  // flag_s[grp] is read before its reuse
-            if (last)
-                finish_head(A.parts, (int64_t)A.num_ctas + (int64_t)A.B * A.Hq, s2.bh, c_first,
-                            c_last, gt, A.out, A.lse, A.merged);
+            if (last) {
+                const int b2 = s2.bh / Hqv, bq0 = b2 * A.Hq + (s2.bh - b2 * Hqv) * HG;
+#pragma unroll
+                for (int h = 0; h < HG; ++h)
+                    finish_head(A.parts, (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq, HG,
+                                s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged);
+            }
         }
     }
     if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight
@@ -1191,7 +1265,9 @@ extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {  // n <= 64 *
 #endif
 
 extern "C" int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d) {
-    return ((int64_t)num_ctas + 2 * (int64_t)B * Hq) * (int64_t)(d + kPS);
+    // split records (two per split and virtual head when a CTA serves two
+    // query heads) + one dense record per query head
+    return (2 * (int64_t)num_ctas + 2 * (int64_t)B * Hq) * (int64_t)(d + kPS);
 }
 
 static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int M, int nbits,
@@ -1205,12 +1281,15 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
     return PQKV_OK;
 }
 
-template <bool kLutFromQ, bool kHalfCV = false>
+#ifndef PQKV_GQA2_WARPS
+#define PQKV_GQA2_WARPS 12
+#endif
+template <bool kLutFromQ, bool kHalfCV = false, int HG = 1, int W = fast::WARPS>
 static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
     static int attr_set[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV>;
+    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV, HG, W>;
     if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              fast::SMEM_BYTES);
@@ -1223,7 +1302,7 @@ static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const 
 #endif
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(args.num_ctas);
-    cfg.blockDim = dim3(fast::NT);
+    cfg.blockDim = dim3(W * 32);
     cfg.dynamicSmemBytes = fast::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -1356,7 +1435,8 @@ extern "C" int pqkv_decode_attention(
     PQKV_CHECK_ARG((recent_k == nullptr) == (recent_v == nullptr),
                    "pqkv_decode_attention: recent_k and recent_v go together");
     PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
-                              PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES)) == 0,
+                              PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES |
+                              PQKV_DECODE_ONE_HEAD_PER_CTA)) == 0,
                    "pqkv_decode_attention: unknown flags");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
@@ -1387,8 +1467,13 @@ extern "C" int pqkv_decode_attention(
     a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
     a.early_codes = (flags & PQKV_DECODE_EARLY_CODES) ? 1 : 0;
     const bool pdl = (flags & PQKV_DECODE_PDL) != 0;
-    if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK)
+    if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
+        // even GQA groups: one CTA serves two query heads of a KV head
+        if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA))
+            return launch_fast<true, true, 2, PQKV_GQA2_WARPS>(a, pdl, st,
+                                                               "pqkv_decode_attention");
         return launch_fast<true, true>(a, pdl, st, "pqkv_decode_attention");
+    }
     return launch_fast<true, false>(a, pdl, st, "pqkv_decode_attention");
 }
 

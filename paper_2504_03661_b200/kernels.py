@@ -240,7 +240,7 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
                      codes_v, n_q, cb_v_layout, recent_k=None, recent_v=None, n_recent=None,
                      k_cur=None, v_cur=None, out=None, lse=None, merged=None, pdl: bool = False,
                      static_codebooks: bool = False, early_codes: bool = False,
-                     stream=None) -> None:
+                     one_head_per_cta: bool = False, stream=None) -> None:
     """One fused launch per layer (m64b8): quantized span + dense window +
     fixed-order merge + finalize for every (b, hq); other geometries fall back
     to decode_partials + decode_finish inside the library.
@@ -261,6 +261,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
     flags = (N.DECODE_PDL if pdl else 0) | (N.DECODE_STATIC_CODEBOOKS if static_codebooks else 0)
     if early_codes:
         flags |= N.DECODE_EARLY_CODES
+    if one_head_per_cta:
+        flags |= N.DECODE_ONE_HEAD_PER_CTA
     if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
         flags |= N.DECODE_F16_VALUE_CODEBOOK
     N.call("pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
