@@ -68,7 +68,6 @@ constexpr int RING = PQKV_RING;  // register ring depth (units of 16 tokens per 
 #define PQKV_GROUP 1
 #endif
 constexpr int GROUP = PQKV_GROUP;  // units processed together (key phase, one max update, value phase)
-static_assert(RING % GROUP == 0, "the ring holds whole groups");
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
 // shared-memory map (bytes from the dynamic base)
@@ -516,8 +515,9 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[lut_i
 // of one KV head -- a "virtual head" -- with two key tables (one PRMT per
 // code byte feeds both) and one value gather per code shared by both heads.
 // W warps per CTA.
-template <bool kLutFromQ, bool kHalfCV, int HG, int W>
+template <bool kLutFromQ, bool kHalfCV, int HG, int W, int GROUP>
 __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A) {
+    static_assert(RING % GROUP == 0, "the ring holds whole groups");
     static_assert(HG == 1 || (HG == 2 && kHalfCV && kLutFromQ), "two heads need the fp16 codebook");
     static_assert(W <= PQKV_WARPS_MAX, "the shared-memory map is sized for PQKV_WARPS_MAX warps");
     constexpr int WARPS = W, NT = W * 32, NG = NT / 128;
@@ -1284,12 +1284,22 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
 #ifndef PQKV_GQA2_WARPS
 #define PQKV_GQA2_WARPS 12
 #endif
-template <bool kLutFromQ, bool kHalfCV = false, int HG = 1, int W = fast::WARPS>
+#ifndef PQKV_F16_WARPS
+#define PQKV_F16_WARPS 12
+#endif
+#ifndef PQKV_F16_GROUP
+#define PQKV_F16_GROUP 2
+#endif
+#ifndef PQKV_GQA2_GROUP
+#define PQKV_GQA2_GROUP 2
+#endif
+template <bool kLutFromQ, bool kHalfCV = false, int HG = 1, int W = fast::WARPS,
+          int GROUP = fast::GROUP>
 static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
     static int attr_set[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV, HG, W>;
+    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV, HG, W, GROUP>;
     if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              fast::SMEM_BYTES);
@@ -1470,9 +1480,10 @@ extern "C" int pqkv_decode_attention(
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
         // even GQA groups: one CTA serves two query heads of a KV head
         if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA))
-            return launch_fast<true, true, 2, PQKV_GQA2_WARPS>(a, pdl, st,
-                                                               "pqkv_decode_attention");
-        return launch_fast<true, true>(a, pdl, st, "pqkv_decode_attention");
+            return launch_fast<true, true, 2, PQKV_GQA2_WARPS, PQKV_GQA2_GROUP>(
+                a, pdl, st, "pqkv_decode_attention");
+        return launch_fast<true, true, 1, PQKV_F16_WARPS, PQKV_F16_GROUP>(a, pdl, st,
+                                                                          "pqkv_decode_attention");
     }
     return launch_fast<true, false>(a, pdl, st, "pqkv_decode_attention");
 }
