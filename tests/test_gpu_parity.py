@@ -307,9 +307,11 @@ def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
-    (1, 4, 4, 3000, [3000], [31]),
-    (2, 8, 2, 5000, [4999, 1234], [5, 32]),
-    (3, 2, 1, 700, [0, 1, 7], [0, 3, 0]),
+    (1, 4, 4, 3000, [3000], [31]),                   # MHA: one query head per CTA
+    (2, 8, 2, 5000, [4999, 1234], [5, 32]),          # G = 4: two query heads per CTA
+    (3, 2, 1, 700, [0, 1, 7], [0, 3, 0]),            # G = 2, empty / tiny spans
+    (2, 6, 2, 4100, [4100, 333], [31, 0]),           # G = 3 (odd): one head per CTA
+    (1, 8, 1, 20000, [20000], [7]),                  # G = 8, many CTAs per virtual head
 ])
 def test_f16_value_codebook_mode(B, Hq, Hkv, cap, n_q, n_r):
     """PQKV_DECODE_F16_VALUE_CODEBOOK: the value codebook is stored as fp16
@@ -321,6 +323,31 @@ def test_f16_value_codebook_mode(B, Hq, Hkv, cap, n_q, n_r):
     got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True)
     np.testing.assert_allclose(got, want16, rtol=1e-3, atol=1e-4)
     np.testing.assert_allclose(got, want, rtol=2e-3, atol=2e-4)
+
+
+def test_f16_two_heads_per_cta_matches_one():
+    """The fp16 GQA pairing (a CTA serves two query heads, one value gather per
+    code for both) agrees with the one-head-per-CTA launch within the mode's
+    weight rounding: the split points differ, so the running maxima the fp16
+    weights are rounded against differ (2^-12 relative per weight)."""
+    from paper_2504_03661_b200 import kernels as K
+    B, Hq, Hkv, n, R = 2, 8, 2, 6000, 16
+    x = _fused_inputs(B, Hq, Hkv, n, R, 9)
+    cv16 = K.value_codebook_layout(
+        torch.from_numpy(np.random.default_rng(9).standard_normal((64, 256, 2)).astype(
+            np.float32)).cuda(), 8, half=True)
+    nq = torch.tensor([6000, 2500], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([16, 3], dtype=torch.int32, device="cuda")
+    outs = []
+    for one in (False, True):
+        ws = K.DecodeWorkspace(B, Hq, 128, 64, 8)
+        out = torch.empty((B * Hq, 128), device="cuda")
+        K.decode_attention(ws, Hkv, x["q"], 0.09, x["cbk"], x["ck"], x["cv"], nq, cv16,
+                           recent_k=x["rk"], recent_v=x["rv"], n_recent=nr, k_cur=x["kc"],
+                           v_cur=x["vc"], out=out, one_head_per_cta=one)
+        assert int(ws.counters.abs().sum()) == 0
+        outs.append(out.cpu().numpy())
+    np.testing.assert_allclose(outs[0], outs[1], rtol=1e-3, atol=1e-4)
 
 
 def _fused_inputs(B, Hq, Hkv, n, R, seed):
