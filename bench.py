@@ -47,6 +47,10 @@ CONFIGS = {
     "llama3-gqa-128k": (32, 4, 32, 8, 131072, 31),
 }
 SEQ_SPLIT = {"llama3-gqa-128k"}
+# BASELINE config 3 is KV-head sharded under torchrun: rank r serves KV heads
+# [r Hkv/N, (r+1) Hkv/N) (and their query heads) of every sequence -- no
+# collective, total work fixed (strong scaling)
+HEAD_SHARD = {"llama3-gqa-32k"}
 D, M, NBITS = 128, 64, 8
 METRIC = "decode attention tokens/s at 32K ctx (HBM GB/s of roofline); KV encode tok/s"
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -231,6 +235,14 @@ def run_reference(args):
 
 def config_dict(name, n_gpus):
     L, B, Hq, Hkv, n, R = CONFIGS[name]
+    if name in HEAD_SHARD and n_gpus > 1:
+        return {"workload": name, "layers": L, "batch_per_gpu": B, "global_batch": B,
+                "q_heads": Hq, "kv_heads": Hkv, "q_heads_per_gpu": Hq // n_gpus,
+                "kv_heads_per_gpu": Hkv // n_gpus, "head_dim": D, "ctx_quantized": n,
+                "recent_rows": R, "pq": "m64b8 (M=64, nbits=8, dsub=2)",
+                "code_bytes_per_step_per_gpu": 2 * L * B * (Hkv // n_gpus) * n * M,
+                "parallelism": f"kv-head-sharded x{n_gpus} (no collective)",
+                "l2": "inputs > L2 (code stream per step >> 126 MB); no flush needed"}
     if name in SEQ_SPLIT:
         return {"workload": name, "layers": L, "batch_per_gpu": B, "global_batch": B,
                 "q_heads": Hq, "kv_heads": Hkv, "head_dim": D, "ctx_quantized": n,
@@ -312,6 +324,11 @@ def run_ours(args):
         a_, b_ = shard_tokens(n_full, rank, world)
         n = b_ - a_
     tail = (not seq_split) or rank == world - 1  # owns the recent window + current token
+    head_shard = args.config in HEAD_SHARD and world > 1
+    if head_shard:
+        if Hkv % world:
+            raise SystemExit(f"{args.config}: {Hkv} KV heads do not shard over {world} GPUs")
+        Hq, Hkv = Hq // world, Hkv // world
     cfg = PQConfig(D, M, NBITS)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -405,7 +422,8 @@ def run_ours(args):
             ev1.record(stream)
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    jobs = 1 if seq_split else world  # sequences per rank are independent jobs unless split
+    # ranks serve independent sequences unless they split them (by tokens or heads)
+    jobs = 1 if (seq_split or head_shard) else world
     value = jobs * B * 1e3 / ms
     clocks = clk.summary()
 
@@ -481,7 +499,8 @@ def run_ours(args):
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong" if seq_split else "weak",
+            "higher_is_better": True,
+            "scaling": "strong" if (seq_split or head_shard) else "weak",
             "vs_baseline": None,
             "dtype": "u8 codes / f32 accumulate" + (" (f16 value codebook)" if args.f16_value_codebook else ""), "data": "synthetic (seeded uniform codes, "
             "N(0,1) codebooks, queries and recent rows)",
