@@ -216,17 +216,20 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
     ccmax = ccmax_s;
 
     const int64_t v0 = (int64_t)blockIdx.x * blockDim.x * VPT + threadIdx.x;
-    float xf0[VPT], xf1[VPT], b1[VPT], b2[VPT];
-    int arg[VPT];
+    // best / second-best as sortable keys: the distance's bits (d >= 0, so its
+    // bit pattern orders like the value) with the low mantissa bits replaced
+    // by the centroid index -- one LOP3 + three integer min/max per centroid
+    const uint32_t cmask = (uint32_t)ksub - 1u;  // ksub is a power of two
+    float xf0[VPT], xf1[VPT];
+    uint32_t b1[VPT], b2[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const int64_t v = v0 + (int64_t)k * blockDim.x;
         const int64_t vv = v < n ? v : n - 1;
         xf0[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2);
         xf1[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2 + 1);
-        b1[k] = INFINITY;
-        b2[k] = INFINITY;
-        arg[k] = 0;
+        b1[k] = 0xffffffffu;
+        b2[k] = 0xffffffffu;
     }
 #pragma unroll 2
     for (int c = 0; c < ksub; ++c) {
@@ -234,10 +237,9 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
             const float dx = xf0[k] - cv.x, dy = xf1[k] - cv.y;
-            const float d = fmaf(dy, dy, dx * dx);
-            arg[k] = d < b1[k] ? c : arg[k];
-            b2[k] = fminf(b2[k], fmaxf(b1[k], d));
-            b1[k] = fminf(b1[k], d);
+            const uint32_t key = (__float_as_uint(fmaf(dy, dy, dx * dx)) & ~cmask) | (uint32_t)c;
+            b2[k] = min(b2[k], max(b1[k], key));
+            b1[k] = min(b1[k], key);
         }
     }
 #pragma unroll
@@ -245,11 +247,14 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
         const int64_t v = v0 + (int64_t)k * blockDim.x;
         if (v >= n) continue;
         // |d32 - d_true| <= ~4 u d_true (u = 2^-24); the reference's fp64
-        // expanded form is within ~4 * 2^-53 (|x|^2 + 2|x.c| + |c|^2) of d_true
+        // expanded form is within ~4 * 2^-53 (|x|^2 + 2|x.c| + |c|^2) of d_true;
+        // the keys drop log2(ksub) mantissa bits (relative 2^(nbits - 23))
         const float xx = fmaf(xf1[k], xf1[k], xf0[k] * xf0[k]);
-        const float tol = 2e-6f * b1[k] + 1e-13f * (xx + ccmax) + 1e-30f;
-        int a = arg[k];
-        if (!(b2[k] > b1[k] + tol)) {  // near tie: the exact scan
+        const float d1 = __uint_as_float(b1[k] & ~cmask), d2k = __uint_as_float(b2[k] & ~cmask);
+        const float trunc = __uint_as_float(0x3f800000u | cmask) - 1.f;  // ksub * 2^-23
+        const float tol = (2e-6f + 2.f * trunc) * d1 + 1e-13f * (xx + ccmax) + 1e-30f;
+        int a = (int)(b1[k] & cmask);
+        if (!(d2k > d1 + tol)) {  // near tie: the exact scan        if (!(b2[k] > b1[k] + tol)) {  // near tie: the exact scan
             const double x0 = (double)xf0[k], x1 = (double)xf1[k];
             const double xxd = __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1));
             double best = INFINITY;
