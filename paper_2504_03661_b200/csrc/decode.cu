@@ -245,17 +245,15 @@ struct Unit {
     uint4 ka, va, kb, vb;
 };
 
-__device__ __forceinline__ void load_keys(Unit &U, const uint8_t *kbase, int u, int slot, int lo,
-                                          int hi) {
-    const int ta = u * 16 + slot, tb = ta + 8;
-    if (ta >= lo && ta < hi) U.ka = ld_stream(kbase + (int64_t)ta * M);
-    if (tb >= lo && tb < hi) U.kb = ld_stream(kbase + (int64_t)tb * M);
+// the same from a running pointer p = (K code row of token t) and the
+// constant V - K base distance: no address arithmetic beyond an immediate
+__device__ __forceinline__ void load_keys_at(Unit &U, const uint8_t *p, int t, int lo, int hi) {
+    if (t >= lo && t < hi) U.ka = ld_stream(p);
+    if (t + 8 >= lo && t + 8 < hi) U.kb = ld_stream(p + 8 * M);
 }
-__device__ __forceinline__ void load_values(Unit &U, const uint8_t *vbase, int u, int slot, int lo,
-                                            int hi) {
-    const int ta = u * 16 + slot, tb = ta + 8;
-    if (ta >= lo && ta < hi) U.va = ld_stream(vbase + (int64_t)ta * M);
-    if (tb >= lo && tb < hi) U.vb = ld_stream(vbase + (int64_t)tb * M);
+__device__ __forceinline__ void load_values_at(Unit &U, const uint8_t *p, int t, int lo, int hi) {
+    if (t >= lo && t < hi) U.va = ld_stream(p);
+    if (t + 8 >= lo && t + 8 < hi) U.vb = ld_stream(p + 8 * M);
 }
 __device__ __forceinline__ void load_unit(Unit &U, const uint8_t *kbase, const uint8_t *vbase,
                                           int u, int slot, int lo, int hi) {
@@ -781,6 +779,11 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         // drain the ring's pending loads.
         int u = u0 + warp;
         const int nunits = max(0, (u1 - u0 - warp + WARPS - 1) / WARPS);
+        // running load position: the next unit to load is u + RING * WARPS
+        constexpr int64_t kStep = (int64_t)WARPS * 16 * M;  // bytes per unit step of a warp
+        const int64_t dv = vbase - kbase;
+        int tn = (u + RING * WARPS) * 16 + slot;
+        const uint8_t *kp = kbase + (int64_t)tn * M;
         for (int trip = 0; trip < (nunits + RING - 1) / RING; ++trip) {
             // pin the lane-constant address words in registers (no remat)
 #pragma unroll
@@ -801,22 +804,27 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                         Ur + g * GROUP, S, packK, packV, okA, okB, [&]() {
 #pragma unroll
                             for (int n = 0; n < GROUP; ++n)
-                                load_keys(Ur[g * GROUP + n], kbase, u + (n + RING) * WARPS, slot,
-                                          lo, hi);
+                                load_keys_at(Ur[g * GROUP + n], kp + n * kStep,
+                                             tn + n * WARPS * 16, lo, hi);
                         });
 #pragma unroll
                     for (int n = 0; n < GROUP; ++n)
-                        load_values(Ur[g * GROUP + n], vbase, u + (n + RING) * WARPS, slot, lo,
-                                    hi);
+                        load_values_at(Ur[g * GROUP + n], kp + n * kStep + dv,
+                                       tn + n * WARPS * 16, lo, hi);
                 } else {
                     process_units<kHalfCV, GROUP, HG>(Ur + g * GROUP, S, packK, packV, okA, okB,
                                                       []() {});
 #pragma unroll
-                    for (int n = 0; n < GROUP; ++n)
-                        load_unit(Ur[g * GROUP + n], kbase, vbase, u + (n + RING) * WARPS, slot,
-                                  lo, hi);
+                    for (int n = 0; n < GROUP; ++n) {
+                        load_keys_at(Ur[g * GROUP + n], kp + n * kStep, tn + n * WARPS * 16, lo,
+                                     hi);
+                        load_values_at(Ur[g * GROUP + n], kp + n * kStep + dv,
+                                       tn + n * WARPS * 16, lo, hi);
+                    }
                 }
                 u += GROUP * WARPS;
+                kp += GROUP * kStep;
+                tn += GROUP * WARPS * 16;
             }
         }
 
