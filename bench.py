@@ -300,6 +300,59 @@ def encode_rate(dev, L, Hkv, n, stream):
             "tflops_98304_per_vector": vectors * M * 256 * 6 / t_layer / 1e12, "bit_exact": True}
 
 
+def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
+    """BASELINE config 5, second part: the per-token append path flushes a
+    batch of R_f recent rows (K and V, every layer, sequence and KV head) into
+    the code store every R_f decode steps, on a lowest-priority side stream
+    (ServingCache(async_flush=True)).  Times R_f decode steps with and without
+    one such flush running beside them; reports the slowdown."""
+    import torch
+    from paper_2504_03661_b200 import kernels as K
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    rows = torch.randn((L, 2, B * Hkv * R_f, D), generator=g, device=dev)
+    cents = torch.randn((L, 2, M, 256, 2), generator=g, device=dev)
+    codes = torch.empty((L, 2, B * Hkv * R_f, M), dtype=torch.uint8, device=dev)
+    lo, _ = torch.cuda.Stream.priority_range()
+    side = torch.cuda.Stream(device=dev, priority=lo)
+
+    def flush():
+        with torch.cuda.stream(side):
+            for l in range(L):
+                for kind in range(2):
+                    K.encode(rows[l, kind], cents[l, kind], NBITS, out=codes[l, kind],
+                             stream=side, layout="decode")
+
+    def window(with_flush):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        if with_flush:
+            side.wait_event(e0)
+            flush()
+        with torch.cuda.stream(stream):
+            for _ in range(R_f):
+                graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(max(1, warmup)):
+        window(True)
+    base = statistics.median(window(False) for _ in range(rounds))
+    with_flush = statistics.median(window(True) for _ in range(rounds))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(side)
+    flush()
+    e1.record(side)
+    torch.cuda.synchronize()
+    return {"flush_batch": f"{R_f} rows x K,V x {L} layers x {B * Hkv} KV heads "
+                           f"({2 * L * B * Hkv * R_f} vectors), every {R_f} steps",
+            "flush_alone_ms": e0.elapsed_time(e1),
+            "decode_ms_per_step": base / R_f, "decode_ms_per_step_with_flush": with_flush / R_f,
+            "slowdown": with_flush / base - 1.0}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -496,6 +549,8 @@ def run_ours(args):
         del g16
 
     enc = None if args.no_encode else encode_rate(dev, L, Hkv, n, stream)
+    if enc is not None:
+        enc["append_overlap"] = append_overlap(dev, graph, stream, L, B, Hkv, args.warmup)
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
