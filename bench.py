@@ -310,18 +310,17 @@ def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
     from paper_2504_03661_b200 import kernels as K
     g = torch.Generator(device=dev)
     g.manual_seed(11)
-    rows = torch.randn((L, 2, B * Hkv * R_f, D), generator=g, device=dev)
-    cents = torch.randn((L, 2, M, 256, 2), generator=g, device=dev)
-    codes = torch.empty((L, 2, B * Hkv * R_f, M), dtype=torch.uint8, device=dev)
+    rows = torch.randn((2, L, B * Hkv * R_f, D), generator=g, device=dev)  # [K|V][layer]
+    cents = torch.randn((2, L, M, 256, 2), generator=g, device=dev)
+    codes = torch.empty((2, L, B * Hkv * R_f, M), dtype=torch.uint8, device=dev)
     lo, _ = torch.cuda.Stream.priority_range()
     side = torch.cuda.Stream(device=dev, priority=lo)
 
-    def flush():
+    def flush():  # ServingCache._encode_all: one batched launch per kind over all layers
         with torch.cuda.stream(side):
-            for l in range(L):
-                for kind in range(2):
-                    K.encode(rows[l, kind], cents[l, kind], NBITS, out=codes[l, kind],
-                             stream=side, layout="decode")
+            for kind in range(2):
+                K.encode_batched(rows[kind], cents[kind], NBITS, out=codes[kind], stream=side,
+                                 layout="decode")
 
     def window(with_flush):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -63,6 +63,17 @@ int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
                 const float *centroids, int M, int nbits, void *codes,
                 int64_t ld_codes, int64_t rot_base, void *stream);
 
+/* pqkv_encode over `batches` independent problems in one launch (e.g. the
+ * layers of a cache flush, each with its own codebook): batch z reads rows at
+ * x + z * x_bstride (elements), centroids at centroids + z * c_bstride and
+ * writes codes at codes + z * codes_bstride (cells).  Same results as
+ * `batches` pqkv_encode calls (which it falls back to off the fp32 dsub = 2
+ * fast path). */
+int pqkv_encode_batched(const void *x, int x_dtype, int batches, int64_t n, int d,
+                        int64_t ld_x, int64_t x_bstride, const float *centroids,
+                        int64_t c_bstride, int M, int nbits, void *codes, int64_t ld_codes,
+                        int64_t codes_bstride, int64_t rot_base, void *stream);
+
 /* Convert n rows between the row layout and the decode layout (to_decode = 1:
  * rows -> decode, 0: decode -> rows); row 0 is token index t_first. */
 int pqkv_relayout_codes(const void *src, int64_t ld_src, void *dst,

@@ -31,6 +31,8 @@ SIGNATURES = {
     "pqkv_version": (_I, []),
     "pqkv_last_error": (ctypes.c_char_p, []),
     "pqkv_encode": (_I, [_P, _I, _I64, _I, _I64, _P, _I, _I, _P, _I64, _I64, _P]),
+    "pqkv_encode_batched": (_I, [_P, _I, _I, _I64, _I, _I64, _I64, _P, _I64, _I, _I, _P, _I64,
+                                 _I64, _I64, _P]),
     "pqkv_relayout_codes": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P]),
     "pqkv_reconstruct": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
     "pqkv_build_lut": (_I, [_P, _I64, _I, _P, _I, _I, _F, _P, _P]),

@@ -192,7 +192,13 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
                                                            int64_t ld_x,
                                                            const float *__restrict__ cents,
                                                            int ksub, CT *__restrict__ codes,
-                                                           int64_t ld_codes, int64_t rot_base) {
+                                                           int64_t ld_codes, int64_t rot_base,
+                                                           int64_t x_bs, int64_t c_bs,
+                                                           int64_t codes_bs) {
+    // batch blockIdx.z (e.g. one layer each): its own rows, codebook and codes
+    x += blockIdx.z * x_bs;
+    cents += blockIdx.z * c_bs;
+    codes += blockIdx.z * codes_bs;
     extern __shared__ double sm[];
     double2 *c_s = reinterpret_cast<double2 *>(sm);                   // [ksub]
     double *cc_s = sm + 2 * (size_t)ksub;                              // [ksub]
@@ -275,7 +281,8 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
 template <typename TX, typename CT>
 int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
                         int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
-                        cudaStream_t st) {
+                        cudaStream_t st, int batches = 1, int64_t x_bs = 0, int64_t c_bs = 0,
+                        int64_t codes_bs = 0) {
     constexpr int VPT = PQKV_ENC_VPT;
     const size_t smem = (size_t)ksub * (3 * sizeof(double) + sizeof(float2));
     auto k = encode_dsub2_filter<TX, CT, VPT>;
@@ -284,9 +291,9 @@ int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cen
                                              (int)smem);
         if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
     }
-    dim3 grid((unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)M);
+    dim3 grid((unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)M, (unsigned)batches);
     k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes,
-                               rot_base);
+                               rot_base, x_bs, c_bs, codes_bs);
     return launch_status("pqkv_encode");
 }
 
@@ -407,6 +414,40 @@ int dispatch_cell(const void *x, int64_t n, int d, int64_t ld_x, const float *ce
 }  // namespace pqkv
 
 using namespace pqkv;
+
+extern "C" int pqkv_encode_batched(const void *x, int x_dtype, int batches, int64_t n, int d,
+                                   int64_t ld_x, int64_t x_bstride, const float *centroids,
+                                   int64_t c_bstride, int M, int nbits, void *codes,
+                                   int64_t ld_codes, int64_t codes_bstride, int64_t rot_base,
+                                   void *stream) {
+    PQKV_CHECK_ARG(batches >= 0 && batches <= 65535, "pqkv_encode_batched: bad batch count");
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits), "pqkv_encode_batched: bad geometry");
+    PQKV_CHECK_ARG(x_bstride >= 0 && c_bstride >= 0 && codes_bstride >= 0,
+                   "pqkv_encode_batched: negative batch stride");
+    if (batches == 0 || n == 0) return PQKV_OK;
+    const int ksub = 1 << nbits, esz = x_dtype == PQKV_DTYPE_F32 ? 4 : 2, csz = nbits <= 8 ? 1 : 2;
+    // one launch for the batch on the dsub = 2 fast path (f32 rows); else per batch
+    if (d == 2 * M && x_dtype == PQKV_DTYPE_F32 && PQKV_ENC_VPT > 0 && PQKV_ENC_FILTER &&
+        ksub * 32 <= 160 * 1024 && x && centroids && codes && ld_x >= d && ld_codes >= M &&
+        n <= (int64_t)65535 * 256 * PQKV_ENC_VPT &&
+        (rot_base < 0 || is_fast_geometry(d, M, nbits))) {
+        cudaStream_t st = as_stream(stream);
+        return nbits <= 8
+                   ? launch_dsub2_filter<float, uint8_t>(x, n, ld_x, centroids, M, ksub, codes,
+                                                         ld_codes, rot_base, st, batches,
+                                                         x_bstride, c_bstride, codes_bstride)
+                   : launch_dsub2_filter<float, uint16_t>(x, n, ld_x, centroids, M, ksub, codes,
+                                                          ld_codes, rot_base, st, batches,
+                                                          x_bstride, c_bstride, codes_bstride);
+    }
+    for (int b = 0; b < batches; ++b) {
+        int rc = pqkv_encode((const char *)x + b * x_bstride * esz, x_dtype, n, d, ld_x,
+                             centroids + b * c_bstride, M, nbits,
+                             (char *)codes + b * codes_bstride * csz, ld_codes, rot_base, stream);
+        if (rc) return rc;
+    }
+    return PQKV_OK;
+}
 
 extern "C" int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
                            const float *centroids, int M, int nbits, void *codes,

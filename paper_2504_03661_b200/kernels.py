@@ -57,6 +57,30 @@ def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tens
     return out
 
 
+def encode_batched(x: torch.Tensor, centroids: torch.Tensor, nbits: int,
+                   out: torch.Tensor | None = None, stream=None, layout: str = "rows",
+                   t_first: int = 0) -> torch.Tensor:
+    """encode() over a batch of independent problems in one launch: x (Z, n, d),
+    centroids (Z, M, ksub, dsub) -> (Z, n, M) -- e.g. every layer of a cache
+    flush, each with its own codebook."""
+    _dev_check(x, centroids)
+    Z, M, ksub, dsub = centroids.shape
+    d = M * dsub
+    if x.dim() != 3 or x.shape[0] != Z or x.shape[2] != d:
+        raise ValueError(f"X must be ({Z}, n, {d}), got {tuple(x.shape)}")
+    x = _contig(x.float())
+    n = x.shape[1]
+    cents = _contig(centroids.float())
+    if out is None:
+        out = torch.empty((Z, n, M), dtype=code_dtype(nbits), device=x.device)
+    if tuple(out.shape) != (Z, n, M) or not out.is_contiguous():
+        raise ValueError("codes output must be a contiguous (Z, n, M) tensor")
+    N.call("pqkv_encode_batched", N.ptr(x), N.DTYPE_CODE[torch.float32], Z, n, d, d, n * d,
+           N.ptr(cents), M * ksub * dsub, M, nbits, N.ptr(out), M, n * M,
+           _rot_base(layout, t_first), N.stream_ptr(stream))
+    return out
+
+
 def _rot_base(layout: str, t_first: int) -> int:
     if layout == "rows":
         return -1

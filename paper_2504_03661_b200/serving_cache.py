@@ -67,6 +67,8 @@ class ServingCache:
 
         self.cents_k = [cents(c) for c in centroids_k]
         self.cents_v = [cents(c) for c in centroids_v]
+        self.cents_k_all = torch.stack(self.cents_k)  # (L, M, ksub, dsub): batched flushes
+        self.cents_v_all = torch.stack(self.cents_v)
         # decode-kernel codebook layouts (static: prepared once, at load time)
         self.cb_k = [K.key_codebook_layout(c, config.nbits) for c in self.cents_k]
         self.cb_v = [K.value_codebook_layout(c, config.nbits) for c in self.cents_v]
@@ -124,6 +126,20 @@ class ServingCache:
                                  out=store[l, b, h, t_first:t_first + n], stream=stream,
                                  layout="decode", t_first=t_first)
 
+    def _encode_all(self, rows_k, rows_v, t_first: int, stream=None) -> None:
+        """rows (L, B, Hkv, n, d), n a multiple of 8 -> codes[:, :, :, t_first:+n]:
+        one batched encode launch per kind for every layer (row v = (b, h, t)
+        carries index t_first + v == t_first + t mod 8, see _encode), then one
+        strided copy into the store."""
+        L, B, Hkv, n, d = rows_k.shape
+        M = self.config.M
+        for rows, cents, store in ((rows_k, self.cents_k_all, self.codes_k),
+                                   (rows_v, self.cents_v_all, self.codes_v)):
+            tmp = K.encode_batched(rows.reshape(L, B * Hkv * n, d), cents, self.config.nbits,
+                                   stream=stream, layout="decode", t_first=t_first)
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                store[:, :, :, t_first:t_first + n] = tmp.view(L, B, Hkv, n, M)
+
     def prefill(self, K_rows: torch.Tensor, V_rows: torch.Tensor) -> None:
         """K/V (L, B, Hkv, n, d): encode all but the trailing min(R, n) rows,
         keep those full precision (prefill_ingest, kv_cache.py:152-181)."""
@@ -136,12 +152,11 @@ class ServingCache:
         n_enc = n - keep
         if n_enc > self.capacity:
             raise ValueError("prefill exceeds the code capacity")
-        for l in range(L):
-            if n_enc:
-                self._encode(l, K_rows[l, :, :, :n_enc].float().contiguous(),
-                             V_rows[l, :, :, :n_enc].float().contiguous(), 0)
-            self.recent_k[l, :, :, :keep] = K_rows[l, :, :, n_enc:]
-            self.recent_v[l, :, :, :keep] = V_rows[l, :, :, n_enc:]
+        if n_enc:
+            self._encode_layers(K_rows[:, :, :, :n_enc].float().contiguous(),
+                                V_rows[:, :, :, :n_enc].float().contiguous(), 0)
+        self.recent_k[:, :, :, :keep] = K_rows[:, :, :, n_enc:]
+        self.recent_v[:, :, :, :keep] = V_rows[:, :, :, n_enc:]
         self._nq, self._nr = n_enc, keep
         self.n_q.fill_(n_enc)
         self.n_recent.fill_(keep)
@@ -171,6 +186,13 @@ class ServingCache:
                 return
 
     # -- flush machinery -----------------------------------------------------------
+    def _encode_layers(self, rows_k, rows_v, t_first: int, stream=None) -> None:
+        if rows_k.shape[3] % 8 == 0:
+            self._encode_all(rows_k, rows_v, t_first, stream)
+        else:
+            for l in range(self.L):
+                self._encode(l, rows_k[l], rows_v[l], t_first, stream)
+
     def _flush(self) -> None:
         batch = self.R_f
         if self._nq + batch > self.capacity:
@@ -179,8 +201,7 @@ class ServingCache:
         rows_k = self.recent_k[:, :, :, :batch].clone()  # snapshot on the main stream
         rows_v = self.recent_v[:, :, :, :batch].clone()
         if self._side is None:
-            for l in range(self.L):
-                self._encode(l, rows_k[l], rows_v[l], self._nq)
+            self._encode_layers(rows_k, rows_v, self._nq)
             self._pending = (None, batch)
             self._publish(block=True)
             return
@@ -190,8 +211,7 @@ class ServingCache:
         with torch.cuda.stream(self._side):
             rows_k.record_stream(self._side)
             rows_v.record_stream(self._side)
-            for l in range(self.L):
-                self._encode(l, rows_k[l], rows_v[l], self._nq, stream=self._side)
+            self._encode_layers(rows_k, rows_v, self._nq, stream=self._side)
         done = torch.cuda.Event()
         done.record(self._side)
         self._pending = (done, batch)

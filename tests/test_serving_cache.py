@@ -80,3 +80,16 @@ def test_serving_cache_codes_equal_direct_encode():
             want_v = K.encode(Vs[0, b, h, :n].contiguous(), cv, 8, layout="decode")
             assert torch.equal(cache.codes_k[0, b, h, :n], want_k)
             assert torch.equal(cache.codes_v[0, b, h, :n], want_v)
+
+
+def test_encode_batched_equals_per_problem():
+    """pqkv_encode_batched == one pqkv_encode per batch (row and decode layouts)."""
+    from paper_2504_03661_b200 import kernels as K
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    x = torch.randn((5, 200, 128), generator=g, device="cuda")
+    c = torch.randn((5, 64, 256, 2), generator=g, device="cuda")
+    for layout, t0 in (("rows", 0), ("decode", 24)):
+        got = K.encode_batched(x, c, 8, layout=layout, t_first=t0)
+        for z in range(5):
+            assert torch.equal(got[z], K.encode(x[z], c[z], 8, layout=layout, t_first=t0))
