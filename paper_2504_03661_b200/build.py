@@ -38,10 +38,10 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build the sm_100a library")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(INCLUDE, "pqkv_sm100.h"))
     deps.append(os.path.abspath(__file__))
@@ -52,8 +52,8 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB,
           defines: tuple = ()) -> str:
     """Compile every .cu for sm_100a and link libpqkv_sm100.so; return its path.
     `defines` (e.g. ("PQKV_TRACE",)) builds a diagnostic variant into `lib`."""
-    if not force and lib == LIB and not _stale():
-        return LIB
+    if not force and not _stale(lib):
+        return lib
     os.makedirs(OUT_DIR, exist_ok=True)
     objs = []
     tag = "_".join(defines)

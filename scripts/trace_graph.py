@@ -7,8 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2504_03661_b200 import build as B
 lib = os.environ.get("TRACE_LIB") or os.path.join(B.OUT_DIR, "libpqkv_sm100_trace.so")
-if not os.path.exists(lib):
-    B.build(force=True, lib=lib, defines=("PQKV_TRACE",))
+if not os.environ.get("TRACE_LIB"):
+    B.build(lib=lib, defines=("PQKV_TRACE",))  # rebuilt when older than the sources
 os.environ["PQKV_SM100_LIB"] = lib
 import torch
 from paper_2504_03661_b200 import kernels as K, _native as N
