@@ -93,3 +93,32 @@ def test_encode_batched_equals_per_problem():
         got = K.encode_batched(x, c, 8, layout=layout, t_first=t0)
         for z in range(5):
             assert torch.equal(got[z], K.encode(x[z], c[z], 8, layout=layout, t_first=t0))
+
+
+def test_serving_cache_edges():
+    """Short prefill (n < R keeps every row full precision), capacity checks,
+    prefill-once, shape checks."""
+    from paper_2504_03661_b200.pq_core import PQConfig
+    from paper_2504_03661_b200.serving_cache import ServingCache
+    cfg = PQConfig(128, 64, 8)
+    c = torch.randn((64, 256, 2), device="cuda")
+    cache = ServingCache(1, 1, 1, cfg, [c], [c], capacity=40, async_flush=False)
+    x = torch.randn((1, 1, 1, 10, 128), device="cuda")
+    cache.prefill(x, x)
+    assert cache.n_quantized == 0 and cache.n_recent_rows == 10
+    with pytest.raises(RuntimeError):
+        cache.prefill(x, x)
+    for _ in range(22):  # 32 rows -> one flush of 32
+        cache.append(torch.randn((1, 1, 1, 128), device="cuda"),
+                     torch.randn((1, 1, 1, 128), device="cuda"))
+    assert cache.n_quantized == 32 and cache.n_recent_rows == 0
+    with pytest.raises(RuntimeError):  # the next flush would exceed capacity 40
+        for _ in range(32):
+            cache.append(torch.randn((1, 1, 1, 128), device="cuda"),
+                         torch.randn((1, 1, 1, 128), device="cuda"))
+    with pytest.raises(ValueError):
+        ServingCache(2, 1, 1, cfg, [c], [c], capacity=8)
+    bad = ServingCache(1, 1, 1, cfg, [c], [c], capacity=8)
+    with pytest.raises(ValueError):
+        bad.prefill(torch.randn((1, 1, 2, 4, 128), device="cuda"),
+                    torch.randn((1, 1, 2, 4, 128), device="cuda"))
