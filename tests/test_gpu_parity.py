@@ -491,6 +491,77 @@ def test_batched_decoder_config2_layer_vs_c_oracle():
     np.testing.assert_allclose(out, want, rtol=RTOL, atol=ATOL)
 
 
+# ---------------------------------------------- full-size properties (config 2) --
+
+def _full_layer(seed=13, H=32, n=32768, R=31):
+    """One config-2 layer as device tensors (decode layout) + a decoder."""
+    from paper_2504_03661_b200 import kernels as K
+    from paper_2504_03661_b200.engine import PQDecoder
+    import paper_2504_03661_b200 as P
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    x = dict(q=torch.randn((1, H, 128), generator=g, device="cuda"),
+             ck=torch.randint(0, 256, (1, H, n, 64), generator=g, device="cuda",
+                              dtype=torch.uint8),
+             cv=torch.randint(0, 256, (1, H, n, 64), generator=g, device="cuda",
+                              dtype=torch.uint8),
+             cents_k=torch.randn((64, 256, 2), generator=g, device="cuda"),
+             cents_v=torch.randn((64, 256, 2), generator=g, device="cuda"),
+             rk=torch.randn((1, H, R, 128), generator=g, device="cuda"),
+             rv=torch.randn((1, H, R, 128), generator=g, device="cuda"),
+             kc=torch.randn((1, H, 128), generator=g, device="cuda"),
+             vc=torch.randn((1, H, 128), generator=g, device="cuda"),
+             nq=torch.tensor([n], dtype=torch.int32, device="cuda"),
+             nr=torch.tensor([R], dtype=torch.int32, device="cuda"))
+    dec = PQDecoder(1, H, H, P.PQConfig(128, 64, 8))
+
+    def run(ck=None, cv=None, cents_v=None, rv=None, vc=None):
+        ck = x["ck"] if ck is None else ck
+        cv = x["cv"] if cv is None else cv
+        return dec(x["q"], K.relayout(ck, True), K.relayout(cv, True), x["nq"],
+                   K.key_codebook_layout(x["cents_k"], 8),
+                   K.value_codebook_layout(x["cents_v"] if cents_v is None else cents_v, 8),
+                   x["rk"], x["rv"] if rv is None else rv, x["nr"], x["kc"],
+                   x["vc"] if vc is None else vc)
+    return x, run
+
+
+def test_full_layer_constant_values_pass_through():
+    """All 32K value codes of every subspace on one centroid, and the recent /
+    current value rows equal to that centroid's reconstruction: the output is
+    that vector whatever the scores (a convex combination of one point)."""
+    x, run = _full_layer()
+    cv = torch.full_like(x["cv"], 7)
+    v7 = x["cents_v"][:, 7, :].reshape(-1)  # (128,)
+    H = x["q"].shape[1]
+    out = run(cv=cv, rv=v7.expand_as(x["rv"]).contiguous(), vc=v7.expand_as(x["vc"]).contiguous())
+    np.testing.assert_allclose(out.cpu().numpy(), v7.expand(1, H, 128).cpu().numpy(),
+                               rtol=1e-5, atol=1e-5)
+
+
+def test_full_layer_token_permutation_invariance():
+    """Permuting the quantized tokens (K and V codes together) leaves the
+    output unchanged: the kernel's split points see different tokens, the
+    softmax does not care (fp32 reassociation only)."""
+    x, run = _full_layer(seed=17)
+    perm = torch.randperm(x["ck"].shape[2], device="cuda")
+    a = run().cpu().numpy()
+    b = run(ck=x["ck"][:, :, perm].contiguous(), cv=x["cv"][:, :, perm].contiguous()).cpu().numpy()
+    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+def test_full_layer_affine_in_values():
+    """out(a C_V + b, a V_recent + b, a v_n + b) = a out(...) + b: the output
+    is a softmax-weighted average of value rows, the weights depend on keys
+    only."""
+    x, run = _full_layer(seed=19)
+    a_, b_ = 1.75, -0.5
+    base = run().cpu().numpy()
+    out = run(cents_v=a_ * x["cents_v"] + b_, rv=a_ * x["rv"] + b_,
+              vc=a_ * x["vc"] + b_).cpu().numpy()
+    np.testing.assert_allclose(out, a_ * base + b_, rtol=1e-5, atol=1e-5)
+
+
 def test_sequence_split_merge_equals_full():
     """Sequence split (config 4 pattern) on one GPU: W token ranges decoded to
     partial records, merged in rank order == the unsplit decode."""
