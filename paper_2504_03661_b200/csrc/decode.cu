@@ -10,16 +10,20 @@
 //   finalize           attention.py:207-211
 //   decode_step        attention.py:214-287 (block split -> our CTA split)
 //
-// decode_partials_m64b8 (the fast path, d=128 M=64 nbits=8):
-//   * persistent grid, one 512-thread CTA per SM; the flattened token space
-//     of all heads is cut into equal chunks (common.cuh CostMap);
+// decode_partials_m64b8 (the fast path, d=128 M=64 nbits=8), one fused
+// launch per layer (pqkv_decode_attention), PDL-chained:
+//   * persistent grid, one CTA per SM (16 warps on the exact path); the
+//     flattened token space of all heads is cut into equal chunks
+//     (common.cuh CostMap); a (CTA, head) overlap is a segment;
 //   * shared memory: the head's key LUT, centroid-major [256][64] fp32
 //     (64 KiB), and the value codebook as two [256][32] float2 halves
 //     (128 KiB, loaded once per CTA);
-//   * a warp handles 16 tokens per step (two independent 8-token halves, one
+//   * a warp handles 16 tokens per unit (two independent 8-token halves, one
 //     merged softmax update): lane = (token slot, 16-subspace quarter) loads
 //     the 16 K-code and 16 V-code bytes of its quarter with one 128-bit load
-//     each (coalesced: the warp reads 4 x 512 contiguous B);
+//     each (coalesced: the warp reads 4 x 512 contiguous B) into a static
+//     RING-unit register ring driven by running pointers; the loop body is
+//     straight-line (masked tail units) so no branch drains the ring;
 //   * codes are stored in the decode layout (common.cuh): each quarter is
 //     pre-rotated by its lane constant r, so at every unrolled step the 32
 //     lanes touch 32 distinct subspaces mod 32 without any in-register
@@ -32,7 +36,13 @@
 //     each token slot keeps its own online-softmax state (m, l) and 32 fp32
 //     value accumulators (its quarter's 16 subspaces x dsub 2);
 //   * epilogue: slot partials are rescaled to the CTA max and summed through
-//     shared memory into one (m, l, acc[128]) record per segment.
+//     shared memory into one (m, l, acc[128]) record per segment; the CTA
+//     holding a head's last tokens adds the dense record (recent rows +
+//     current token); the last CTA to arrive (acq_rel counter) merges the
+//     head's records in CTA order and finalizes;
+//   * fp16 value-codebook mode: 4-byte value gathers + mixed f16 x f16 + f32
+//     FMAs; with an even GQA group a CTA serves HG = 2 query heads (two key
+//     tables, one value gather per code shared by both).
 #include <algorithm>
 #include <cstdlib>
 
