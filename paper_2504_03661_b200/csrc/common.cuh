@@ -42,22 +42,45 @@ inline bool is_fast_geometry(int d, int M, int nbits) {
 }
 
 // ---------------------------------------------------------- decode layout ---
-// m64b8 decode layout of a 64-byte code row: the decode kernel's lane
-// (slot s = t & 7, quarter q) reads bytes [16q, 16q+16) and processes them in
-// the order j = 0..15 against subspace 16q + ((j + r) & 15), where
-// r = ((lane & 15) + (lane >> 4)) & 15 for lane = 4s + q.  Storing subspace i
-// of token t at byte 16q + ((i - r) & 15) lets every lane take its bytes in
-// register order while the 32 lanes of a warp still hit 32 distinct
-// subspaces (= shared-memory banks) at every step -- no in-register
-// rotation.  A bijection per row, so uniform random codes stay uniform.
-// `slot` is the token index (only its low three bits matter).
+// m64b8 decode layout of a 64-byte code row.  The decode kernel's lane owns
+// SPL consecutive subspaces ("part" p) of one token slot s and reads its SPL
+// bytes in register order; byte j is subspace decode_lane_subspace(lane, j).
+// The per-lane byte rotation makes the 32 lanes of a warp touch 32 distinct
+// subspaces mod 32 at every step (the key table's banks) and 16 distinct
+// subspaces mod 16 per half-warp (the 8-byte value-codebook slots) -- bank
+// conflict free for ANY code values, with no in-register shuffling.  A
+// bijection per row, so uniform random codes stay uniform.
+//   PQKV_LANE8 = 0: SPL = 16, lane = 4 s + p (s = t & 7),
+//                   byte j <-> 16 p + ((j + r) & 15), r = ((lane & 15) + (lane >> 4)) & 15
+//   PQKV_LANE8 = 1: SPL = 8, lane = 8 s + p (s = t & 3),
+//                   byte j <-> 8 p + ((j + 2 s + g(p)) & 7), g = 0 2 4 6 1 3 5 7
+#ifndef PQKV_LANE8
+#define PQKV_LANE8 0
+#endif
 __host__ __device__ __forceinline__ int decode_lane_rot(int lane) {
     return ((lane & 15) + (lane >> 4)) & 15;
 }
-__host__ __device__ __forceinline__ int decode_layout_pos(int i, int slot) {
+__host__ __device__ __forceinline__ int lane8_rot(int s, int p) {
+    return (2 * s + (((p & 3) << 1) | (p >> 2))) & 7;
+}
+__host__ __device__ __forceinline__ int decode_lane_subspace(int lane, int j) {
+#if PQKV_LANE8
+    const int p = lane & 7, s = lane >> 3;
+    return 8 * p + ((j + lane8_rot(s, p)) & 7);
+#else
+    return 16 * (lane & 3) + ((j + decode_lane_rot(lane)) & 15);
+#endif
+}
+// byte position of subspace i in the decode-layout row of token t
+__host__ __device__ __forceinline__ int decode_layout_pos(int i, int64_t t) {
+#if PQKV_LANE8
+    const int p = i >> 3, s = (int)(t & 3);
+    return 8 * p + (((i & 7) - lane8_rot(s, p)) & 7);
+#else
     const int q = i >> 4;
-    const int r = decode_lane_rot(4 * (slot & 7) + q);
+    const int r = decode_lane_rot(4 * (int)(t & 7) + q);
     return 16 * q + (((i & 15) - r) & 15);
+#endif
 }
 
 constexpr float kLog2e = 1.4426950408889634f;

@@ -81,18 +81,26 @@ constexpr int RING = PQKV_RING;  // register ring depth (units of 16 tokens per 
 #define PQKV_GROUP 1
 #endif
 constexpr int GROUP = PQKV_GROUP;  // units processed together (key phase, one max update, value phase)
+// Lane geometry (common.cuh decode layout): a lane owns SPL consecutive
+// subspaces (code bytes) of a token; TL lanes per token, TS token slots per
+// warp instruction, a unit = UT = 2 TS tokens per warp (halves A and B).
+constexpr int SPL = PQKV_LANE8 ? 8 : 16;
+constexpr int TL = M / SPL;
+constexpr int TS = 32 / TL;
+constexpr int UT = 2 * TS;
+constexpr int NPK = SPL / 2;  // lane-constant pack words per kind
 constexpr int LUT_BYTES = KSUB * M * 4;     // 65536
 constexpr int CV_BYTES = KSUB * M * 2 * 4;  // 131072
 // shared-memory map (bytes from the dynamic base)
 // sized for up to PQKV_WARPS_MAX warps and two heads per CTA
-#define PQKV_WARPS_MAX 16
+#define PQKV_WARPS_MAX 24
 constexpr int WMAX = PQKV_WARPS_MAX;
 constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                 // red_m[2][W], red_l[2][W]
 constexpr int OFF_COL = OFF_RED + 4 * WMAX * 4;               // colsum[2 * NG][128]
-constexpr int OFF_DNS = OFF_COL + 8 * D * 4;                  // dense m[W], l[W], acc[W][128]
+constexpr int OFF_DNS = OFF_COL + 2 * (WMAX / 4) * D * 4;     // dense m[W], l[W], acc[W][128]
 constexpr int OFF_BAR = OFF_DNS + (2 * WMAX + WMAX * D) * 4;  // 2 mbarriers
-constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [4]
-constexpr int SMEM_BYTES = OFF_FLAG + 16;
+constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [W / 4]
+constexpr int SMEM_BYTES = OFF_FLAG + 4 * (WMAX / 4);
 
 #ifdef PQKV_TRACE
 // debug-only timeline: per (launch mod 64, CTA) [smid, t_entry, t_ready,
@@ -135,6 +143,13 @@ struct Args {
     int trace_id;  // PQKV_TRACE builds: launch sequence number
 };
 
+__device__ __forceinline__ uint2 ld_stream8(const uint8_t *p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -251,30 +266,41 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // 16u + s (A) and 16u + 8 + s (B), one 128-bit K load and one V load each.
 // The codes are in the decode layout (common.cuh), so the lane uses its bytes
 // in register order.
+#if PQKV_LANE8
+using CodeVec = uint2;  // a lane's 8 code bytes of one token
+__device__ __forceinline__ CodeVec ld_codes(const uint8_t *p) { return ld_stream8(p); }
+__device__ __forceinline__ uint32_t cword(const uint2 v, int k) { return k == 0 ? v.x : v.y; }
+#else
+using CodeVec = uint4;  // a lane's 16 code bytes of one token
+__device__ __forceinline__ CodeVec ld_codes(const uint8_t *p) { return ld_stream(p); }
+__device__ __forceinline__ uint32_t cword(const uint4 v, int k) {
+    return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+#endif
 struct Unit {
-    uint4 ka, va, kb, vb;
+    CodeVec ka, va, kb, vb;
 };
 
 // the same from a running pointer p = (K code row of token t) and the
 // constant V - K base distance: no address arithmetic beyond an immediate
 __device__ __forceinline__ void load_keys_at(Unit &U, const uint8_t *p, int t, int lo, int hi) {
-    if (t >= lo && t < hi) U.ka = ld_stream(p);
-    if (t + 8 >= lo && t + 8 < hi) U.kb = ld_stream(p + 8 * M);
+    if (t >= lo && t < hi) U.ka = ld_codes(p);
+    if (t + TS >= lo && t + TS < hi) U.kb = ld_codes(p + TS * M);
 }
 __device__ __forceinline__ void load_values_at(Unit &U, const uint8_t *p, int t, int lo, int hi) {
-    if (t >= lo && t < hi) U.va = ld_stream(p);
-    if (t + 8 >= lo && t + 8 < hi) U.vb = ld_stream(p + 8 * M);
+    if (t >= lo && t < hi) U.va = ld_codes(p);
+    if (t + TS >= lo && t + TS < hi) U.vb = ld_codes(p + TS * M);
 }
 __device__ __forceinline__ void load_unit(Unit &U, const uint8_t *kbase, const uint8_t *vbase,
                                           int u, int slot, int lo, int hi) {
-    const int ta = u * 16 + slot, tb = ta + 8;
+    const int ta = u * UT + slot, tb = ta + TS;
     if (ta >= lo && ta < hi) {
-        U.ka = ld_stream(kbase + (int64_t)ta * M);
-        U.va = ld_stream(vbase + (int64_t)ta * M);
+        U.ka = ld_codes(kbase + (int64_t)ta * M);
+        U.va = ld_codes(vbase + (int64_t)ta * M);
     }
     if (tb >= lo && tb < hi) {
-        U.kb = ld_stream(kbase + (int64_t)tb * M);
-        U.vb = ld_stream(vbase + (int64_t)tb * M);
+        U.kb = ld_codes(kbase + (int64_t)tb * M);
+        U.vb = ld_codes(vbase + (int64_t)tb * M);
     }
 }
 
@@ -283,17 +309,16 @@ __device__ __forceinline__ void load_unit(Unit &U, const uint8_t *kbase, const u
 template <int HG>
 struct SlotState {
     float m[HG], l[HG];
-    unsigned long long acc[HG][16];  // float2 per (rotated) subspace of this lane's quarter
+    unsigned long long acc[HG][SPL];  // float2 per (rotated) subspace of this lane's share
 };
 
 template <int HG>
-__device__ __forceinline__ void lut_score(const uint4 k, const uint32_t (&packK)[8],
+__device__ __forceinline__ void lut_score(const CodeVec k, const uint32_t (&packK)[NPK],
                                           float (&out)[HG]) {
-    const uint32_t w[4] = {k.x, k.y, k.z, k.w};
     float sp[HG][4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const uint32_t a = __byte_perm(w[j >> 2], packK[j >> 1], sel_for(j));
+    for (int j = 0; j < SPL; ++j) {
+        const uint32_t a = __byte_perm(cword(k, j >> 2), packK[j >> 1], sel_for(j));
 #pragma unroll
         for (int h = 0; h < HG; ++h) {
             const float x = h == 0 ? lds_f32<0x400>(a) : lds_f32<0x10400>(a);
@@ -317,8 +342,8 @@ __device__ __forceinline__ void lut_score(const uint4 k, const uint32_t (&packK)
 // registers there, half a unit earlier than the value registers).
 template <bool kHalfCV, int NU, int HG, typename AfterKeys>
 __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
-                                              const uint32_t (&packK)[8],
-                                              const uint32_t (&packV)[8], const bool *okA,
+                                              const uint32_t (&packK)[NPK],
+                                              const uint32_t (&packV)[NPK], const bool *okA,
                                               const bool *okB, AfterKeys after_keys) {
     float sa[NU][HG], sb[NU][HG];
 #pragma unroll
@@ -327,7 +352,7 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
         lut_score<HG>(U[n].kb, packK, sb[n]);
     }
 #pragma unroll
-    for (int off = 1; off <= 2; off <<= 1)
+    for (int off = 1; off < TL; off <<= 1)  // the TL lanes of a token
 #pragma unroll
         for (int n = 0; n < NU; ++n)
 #pragma unroll
@@ -348,7 +373,7 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
             const float f = fast_exp2((S.m[h] - mx) * kLog2e);
             S.l[h] *= f;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) fmul2(S.acc[h][k], f);
+            for (int k = 0; k < SPL; ++k) fmul2(S.acc[h][k], f);
             S.m[h] = mx;
         }
 #pragma unroll
@@ -366,13 +391,12 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
     }
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
-        const uint32_t wa[4] = {U[n].va.x, U[n].va.y, U[n].va.z, U[n].va.w};
-        const uint32_t wb[4] = {U[n].vb.x, U[n].vb.y, U[n].vb.z, U[n].vb.w};
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < SPL; ++j) {
+            const uint32_t wa = cword(U[n].va, j >> 2), wb = cword(U[n].vb, j >> 2);
             if (kHalfCV) {  // 4-byte gathers, shared by the HG heads
-                const uint32_t ca = lds_cv32<HG>(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
-                const uint32_t cb = lds_cv32<HG>(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+                const uint32_t ca = lds_cv32<HG>(__byte_perm(wa, packV[j >> 1], sel_for(j)));
+                const uint32_t cb = lds_cv32<HG>(__byte_perm(wb, packV[j >> 1], sel_for(j)));
 #pragma unroll
                 for (int h = 0; h < HG; ++h) {
                     fhfma2(S.acc[h][j], pa16[n][h], ca);
@@ -380,9 +404,9 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
                 }
             } else {
                 const unsigned long long ca =
-                    lds_cv<HG>(__byte_perm(wa[j >> 2], packV[j >> 1], sel_for(j)));
+                    lds_cv<HG>(__byte_perm(wa, packV[j >> 1], sel_for(j)));
                 const unsigned long long cb =
-                    lds_cv<HG>(__byte_perm(wb[j >> 2], packV[j >> 1], sel_for(j)));
+                    lds_cv<HG>(__byte_perm(wb, packV[j >> 1], sel_for(j)));
 #pragma unroll
                 for (int h = 0; h < HG; ++h) {
                     ffma2(S.acc[h][j], pa[n][h], ca);
@@ -574,8 +598,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     const uint32_t bar_lut = sbase + OFF_BAR + 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int q4 = lane & 3, slot = lane >> 2;
-    const int r = decode_lane_rot(lane);
+    const int part = lane % TL, slot = lane / TL;  // SPL-subspace share, token slot
 
     // value codebook: one TMA bulk copy per CTA, overlapped with the first
     // segment's code prefetch and LUT build -- and, when the codebook is static
@@ -603,7 +626,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // latency overlaps the build.
     Unit Ur[RING];
 #pragma unroll
-    for (int rr = 0; rr < RING; ++rr) Ur[rr].ka = Ur[rr].va = Ur[rr].kb = Ur[rr].vb = make_uint4(0, 0, 0, 0);
+    for (int rr = 0; rr < RING; ++rr) Ur[rr].ka = Ur[rr].va = Ur[rr].kb = Ur[rr].vb = CodeVec{};
     CostMap cm;
     Segment s0;
     bool have_s0 = false;
@@ -617,11 +640,12 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         if (have_s0) {
             const int b = s0.bh / Hqv, hkv = (s0.bh - b * Hqv) * HG / group;
             const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
-            const int u0 = s0.lo >> 4;
+            const int u0 = s0.lo / UT;
 #pragma unroll
             for (int rr = 0; rr < RING; ++rr)
-                load_unit(Ur[rr], A.codes_k + head_off + q4 * 16, A.codes_v + head_off + q4 * 16,
-                          u0 + warp + rr * WARPS, slot, s0.lo, s0.hi);
+                load_unit(Ur[rr], A.codes_k + head_off + part * SPL,
+                          A.codes_v + head_off + part * SPL, u0 + warp + rr * WARPS, slot, s0.lo,
+                          s0.hi);
         }
     };
     if (A.early_codes) first_ring();
@@ -644,21 +668,22 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     }
 
     // lane-constant address bytes (see header comment)
-    uint32_t packK[8], packV[8];
+    uint32_t packK[NPK], packV[NPK];
+    const int vhalf = decode_lane_subspace(lane, 0) >> 5;  // this lane's subspace half
 #pragma unroll
-    for (int jp = 0; jp < 8; ++jp) {
+    for (int jp = 0; jp < NPK; ++jp) {
         uint32_t pk = 0, pv = 0;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int j = 2 * jp + e;
-            const int i = 16 * q4 + ((j + r) & 15);
+            const int i = decode_lane_subspace(lane, j);
             pk |= (uint32_t)(i * 4) << (8 * e);
             // fp32: [half][c][32] float2 -> half << 16 | code << 8 | slot * 8;
             // fp16: [c][half][32] half2 -> code << 8 | half << 7 | slot * 4
-            pv |= (uint32_t)(kHalfCV ? (q4 >> 1) * 128 + (i & 31) * 4 : (i & 31) * 8) << (8 * e);
+            pv |= (uint32_t)(kHalfCV ? vhalf * 128 + (i & 31) * 4 : (i & 31) * 8) << (8 * e);
         }
         packK[jp] = pk | cta_byte;
-        packV[jp] = pv | (kHalfCV ? 0u : (uint32_t)(q4 >> 1) << 16) | cta_byte;
+        packV[jp] = pv | (kHalfCV ? 0u : (uint32_t)vhalf << 16) | cta_byte;
     }
 
     bool cv_ready = false;
@@ -671,10 +696,10 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
         const int bh0 = b * A.Hq + hq0;
         const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
-        const uint8_t *kbase = A.codes_k + head_off + q4 * 16;
-        const uint8_t *vbase = A.codes_v + head_off + q4 * 16;
+        const uint8_t *kbase = A.codes_k + head_off + part * SPL;
+        const uint8_t *vbase = A.codes_v + head_off + part * SPL;
         const int lo = sg.lo, hi = sg.hi;             // token range of this segment
-        const int u0 = lo >> 4, u1 = (hi + 15) >> 4;  // 16-token units (absolute)
+        const int u0 = lo / UT, u1 = (hi + UT - 1) / UT;  // UT-token units (absolute)
 
         // code prefetch: these loads fly while the LUT is built
         if (!ring_loaded) {
@@ -790,22 +815,22 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         int u = u0 + warp;
         const int nunits = max(0, (u1 - u0 - warp + WARPS - 1) / WARPS);
         // running load position: the next unit to load is u + RING * WARPS
-        constexpr int64_t kStep = (int64_t)WARPS * 16 * M;  // bytes per unit step of a warp
+        constexpr int64_t kStep = (int64_t)WARPS * UT * M;  // bytes per unit step of a warp
         const int64_t dv = vbase - kbase;
-        int tn = (u + RING * WARPS) * 16 + slot;
+        int tn = (u + RING * WARPS) * UT + slot;
         const uint8_t *kp = kbase + (int64_t)tn * M;
         for (int trip = 0; trip < (nunits + RING - 1) / RING; ++trip) {
             // pin the lane-constant address words in registers (no remat)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
+            for (int k = 0; k < NPK; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
 #pragma unroll
             for (int g = 0; g < RING / GROUP; ++g) {
                 bool okA[GROUP], okB[GROUP];
 #pragma unroll
                 for (int n = 0; n < GROUP; ++n) {
-                    const int ta = ((u + n * WARPS) << 4) + slot;
+                    const int ta = (u + n * WARPS) * UT + slot;
                     okA[n] = ta >= lo && ta < hi;
-                    okB[n] = ta + 8 >= lo && ta + 8 < hi;
+                    okB[n] = ta + TS >= lo && ta + TS < hi;
                 }
                 if constexpr (!kHalfCV && PQKV_EARLY_KEYS) {
                     // exact path: refill the key registers as soon as the key
@@ -815,26 +840,26 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 #pragma unroll
                             for (int n = 0; n < GROUP; ++n)
                                 load_keys_at(Ur[g * GROUP + n], kp + n * kStep,
-                                             tn + n * WARPS * 16, lo, hi);
+                                             tn + n * WARPS * UT, lo, hi);
                         });
 #pragma unroll
                     for (int n = 0; n < GROUP; ++n)
                         load_values_at(Ur[g * GROUP + n], kp + n * kStep + dv,
-                                       tn + n * WARPS * 16, lo, hi);
+                                       tn + n * WARPS * UT, lo, hi);
                 } else {
                     process_units<kHalfCV, GROUP, HG>(Ur + g * GROUP, S, packK, packV, okA, okB,
                                                       []() {});
 #pragma unroll
                     for (int n = 0; n < GROUP; ++n) {
-                        load_keys_at(Ur[g * GROUP + n], kp + n * kStep, tn + n * WARPS * 16, lo,
+                        load_keys_at(Ur[g * GROUP + n], kp + n * kStep, tn + n * WARPS * UT, lo,
                                      hi);
                         load_values_at(Ur[g * GROUP + n], kp + n * kStep + dv,
-                                       tn + n * WARPS * 16, lo, hi);
+                                       tn + n * WARPS * UT, lo, hi);
                     }
                 }
                 u += GROUP * WARPS;
                 kp += GROUP * kStep;
-                tn += GROUP * WARPS * 16;
+                tn += GROUP * WARPS * UT;
             }
         }
 
@@ -858,15 +883,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 #pragma unroll
             for (int w = 1; w < WARPS; ++w) Mx[h] = fmaxf(Mx[h], red_m[h * WARPS + w]);
             const float f = (S.m[h] == -INFINITY) ? 0.f : fast_exp2((S.m[h] - Mx[h]) * kLog2e);
-            float lw = (q4 == 0) ? S.l[h] * f : 0.f;
+            float lw = (part == 0) ? S.l[h] * f : 0.f;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
             if (lane == 0) red_l[h * WARPS + warp] = lw;
-            // head h's slot rows: [WARPS * 8][128] fp32 in the (now free) key tables
-            float *rows = lut_s + (h * WARPS * 8 + warp * 8 + slot) * D;
+            // head h's slot rows: [WARPS * TS][128] fp32 in the (now free) key tables
+            float *rows = lut_s + (h * WARPS * TS + warp * TS + slot) * D;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int i = 16 * q4 + ((j + r) & 15);  // decode layout: byte j <-> this subspace
+            for (int j = 0; j < SPL; ++j) {
+                const int i = decode_lane_subspace(lane, j);  // byte j <-> this subspace
                 const float2 a = unpack2(S.acc[h][j]);
                 rows[2 * i] = a.x * f;
                 rows[2 * i + 1] = a.y * f;
@@ -874,14 +899,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         }
         __syncthreads();
         {
-            const int col = tid & (D - 1), part = tid >> 7;  // NG parts of 32 rows per head
+            constexpr int RPP = WARPS * TS / NG;  // slot rows per 128-thread part
+            const int col = tid & (D - 1), prt = tid >> 7;
 #pragma unroll
             for (int h = 0; h < HG; ++h) {
                 float cs = 0.f;
-                const float *rows = lut_s + h * WARPS * 8 * D;
+                const float *rows = lut_s + h * WARPS * TS * D;
 #pragma unroll 8
-                for (int rr = part * 32; rr < part * 32 + 32; ++rr) cs += rows[rr * D + col];
-                colsum[h * NG + part][col] = cs;
+                for (int rr = prt * RPP; rr < prt * RPP + RPP; ++rr) cs += rows[rr * D + col];
+                colsum[h * NG + prt][col] = cs;
             }
         }
         __syncthreads();

@@ -27,7 +27,7 @@ namespace {
 // of a row is stored rotated by its decode lane's constant (see common.cuh).
 __device__ __forceinline__ int64_t code_cell(int64_t v, int i, int64_t ld_codes, int64_t rot_base) {
     if (rot_base < 0) return v * ld_codes + i;
-    return v * ld_codes + decode_layout_pos(i, (int)((rot_base + v) & 7));
+    return v * ld_codes + decode_layout_pos(i, rot_base + v);
 }
 
 template <typename TX>

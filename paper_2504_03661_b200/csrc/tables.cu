@@ -83,7 +83,7 @@ __global__ void relayout_kernel(const uint8_t *__restrict__ src, int64_t ld_src,
     if (idx >= n * 64) return;
     const int64_t v = idx >> 6;
     const int i = (int)(idx & 63);
-    const int pos = decode_layout_pos(i, (int)((t_first + v) & 7));
+    const int pos = decode_layout_pos(i, t_first + v);
     if (to_decode)
         dst[v * ld_dst + pos] = src[v * ld_src + i];
     else
