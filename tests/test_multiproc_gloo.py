@@ -79,3 +79,57 @@ def test_sequence_split_gloo_world2():
         assert p.exitcode == 0
     errs = dict(q.get(timeout=5) for _ in range(2))
     assert max(errs.values()) < 1e-12
+
+
+def _gpu_worker(rank, world, port, q):
+    """Both ranks on the one GPU of the box: engine.sequence_parallel_decode
+    with the real kernels (PQDecoder merged records, all-gather over gloo,
+    rank-ordered device merge) == the unsplit decode."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_03661_b200 import kernels as K
+        from paper_2504_03661_b200.engine import PQDecoder, sequence_parallel_decode, shard_tokens
+        from paper_2504_03661_b200.pq_core import PQConfig
+        rng = np.random.default_rng(3)  # same data on every rank
+        B, Hq, Hkv, n = 2, 8, 2, 9000
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        cbk = K.key_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8)
+        cbv = K.value_codebook_layout(t(rng.standard_normal((64, 256, 2)).astype(np.float32)), 8)
+        q_ = t(rng.standard_normal((B, Hq, 128)).astype(np.float32))
+        ckr = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+        cvr = t(rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8))
+        rk = t(rng.standard_normal((B, Hkv, 8, 128)).astype(np.float32))
+        rv = t(rng.standard_normal((B, Hkv, 8, 128)).astype(np.float32))
+        nr = t(np.array([8, 5], np.int32))
+        kc = t(rng.standard_normal((B, Hkv, 128)).astype(np.float32))
+        vc = t(rng.standard_normal((B, Hkv, 128)).astype(np.float32))
+        dec = PQDecoder(B, Hq, Hkv, PQConfig(128, 64, 8))
+        full = dec(q_, K.relayout(ckr, True), K.relayout(cvr, True),
+                   t(np.array([n, n], np.int32)), cbk, cbv, rk, rv, nr, kc, vc)
+        a, b = shard_tokens(n, rank, world)
+        tail = rank == world - 1
+        out = sequence_parallel_decode(
+            dec, None, q_, K.relayout(ckr[:, :, a:b], True), K.relayout(cvr[:, :, a:b], True),
+            t(np.array([b - a] * B, np.int32)), cbk, cbv, rk if tail else None,
+            rv if tail else None, nr if tail else None, kc if tail else None,
+            vc if tail else None)
+        torch.cuda.synchronize()
+        q.put((rank, float((out - full).abs().max().item())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sequence_parallel_decode_gloo_world2_gpu():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    errs = dict(q.get(timeout=5) for _ in range(2))
+    assert max(errs.values()) < 1e-5, errs
