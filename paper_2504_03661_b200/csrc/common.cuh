@@ -116,10 +116,34 @@ constexpr int kSwitchCost = PQKV_SWITCH_COST;  // tokens-equivalent of a head sw
 #endif
 constexpr int kDenseCost = PQKV_DENSE_COST;
 
+// The last kTailCtas CTAs of a launch get kTailPenalty fewer cost units: in a
+// PDL-chained sequence of launches they land on the SMs freed last by the
+// previous launch (its last-arriver finishers) and start late.
+#ifndef PQKV_TAIL_CTAS
+#define PQKV_TAIL_CTAS 0
+#endif
+#ifndef PQKV_TAIL_PENALTY
+#define PQKV_TAIL_PENALTY 0
+#endif
+constexpr int kTailCtas = PQKV_TAIL_CTAS, kTailPenalty = PQKV_TAIL_PENALTY;
+
 struct CostMap {
     int64_t total;
-    int64_t chunk;
+    int64_t chunk;   // cost units of CTAs [0, nfirst)
+    int64_t chunk2;  // cost units of CTAs [nfirst, num_ctas)
+    int nfirst;
 };
+
+// first cost position of CTA c (c == num_ctas: past the end)
+__device__ __forceinline__ int64_t cta_begin(const CostMap &cm, int c) {
+    return c < cm.nfirst ? (int64_t)c * cm.chunk
+                         : (int64_t)cm.nfirst * cm.chunk + (int64_t)(c - cm.nfirst) * cm.chunk2;
+}
+// CTA holding cost position pos
+__device__ __forceinline__ int cta_of(const CostMap &cm, int64_t pos) {
+    const int64_t split = (int64_t)cm.nfirst * cm.chunk;
+    return pos < split ? (int)(pos / cm.chunk) : cm.nfirst + (int)((pos - split) / cm.chunk2);
+}
 
 __device__ __forceinline__ int64_t head_span(int n) {
     return kSwitchCost + (int64_t)max(n, 1) + kDenseCost;
@@ -129,10 +153,13 @@ __device__ __forceinline__ CostMap cost_map(const int32_t *__restrict__ n_q, int
                                             int num_ctas) {
     int64_t tot = 0;
     for (int b = 0; b < B; ++b) tot += (int64_t)Hq * head_span(n_q[b]);
-    int64_t chunk = (tot + num_ctas - 1) / num_ctas;
+    const int tail = (num_ctas > 2 * kTailCtas) ? kTailCtas : 0;
+    int64_t chunk = (tot + (int64_t)tail * kTailPenalty + num_ctas - 1) / num_ctas;
     chunk = (chunk + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
     if (chunk < kChunkAlign) chunk = kChunkAlign;
-    return {tot, chunk};
+    int64_t chunk2 = chunk - (tail ? kTailPenalty : 0);
+    chunk2 = max(chunk2 / kChunkAlign * kChunkAlign, (int64_t)kChunkAlign);
+    return {tot, chunk, chunk2, num_ctas - tail};
 }
 
 // Cost-axis position of token 0 of head bh; *len = n_q[b] (>= 0).
@@ -148,10 +175,10 @@ __device__ __forceinline__ int64_t head_token0(const int32_t *__restrict__ n_q, 
 
 // CTAs [*c_first, *c_last] hold the segments of head bh.
 __device__ __forceinline__ void head_ctas(const int32_t *__restrict__ n_q, int Hq, int bh,
-                                          int64_t chunk, int *c_first, int *c_last, int *len) {
+                                          const CostMap &cm, int *c_first, int *c_last, int *len) {
     const int64_t t0 = head_token0(n_q, Hq, bh, len);
-    *c_first = (int)(t0 / chunk);
-    *c_last = (int)((t0 + max(*len, 1) + kDenseCost - 1) / chunk);
+    *c_first = cta_of(cm, t0);
+    *c_last = cta_of(cm, t0 + max(*len, 1) + kDenseCost - 1);
 }
 
 struct Segment {

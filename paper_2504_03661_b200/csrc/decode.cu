@@ -633,8 +633,8 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     int64_t pos = 0, end = 0;
     auto first_ring = [&]() {
         cm = cost_map(A.n_q, A.B, Hqv, A.num_ctas);
-        pos = (int64_t)cta * cm.chunk;
-        end = min(pos + cm.chunk, cm.total);
+        pos = cta_begin(cm, cta);
+        end = min(cta_begin(cm, cta + 1), cm.total);
         int64_t p0 = pos;
         have_s0 = next_segment(A.n_q, A.B, Hqv, &p0, end, &s0);
         if (have_s0) {
@@ -946,12 +946,12 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     if (A.counters != nullptr) {
         __syncthreads();  // every record (and dense record) write of this CTA is done
         const int grp = tid >> 7, gt = tid & (D - 1);
-        int64_t p2 = (int64_t)cta * cm.chunk;
+        int64_t p2 = cta_begin(cm, cta);
         Segment s2;
         for (int k = 0; next_segment(A.n_q, A.B, Hqv, &p2, end, &s2); ++k) {
             if (k % NG != grp) continue;
             int c_first, c_last, len;
-            head_ctas(A.n_q, Hqv, s2.bh, cm.chunk, &c_first, &c_last, &len);
+            head_ctas(A.n_q, Hqv, s2.bh, cm, &c_first, &c_last, &len);
             if (gt == 0) {
                 // acq_rel at gpu scope: releases this CTA's records (ordered
                 // before by the barrier, fences are cumulative) and, for the
@@ -1007,8 +1007,8 @@ __global__ void __launch_bounds__(GT)
     const int dsub = d / M;
     const CostMap cm = cost_map(n_q, B, Hq, num_ctas);
     const int cta = blockIdx.x;
-    int64_t pos = (int64_t)cta * cm.chunk;
-    const int64_t end = min(pos + cm.chunk, cm.total);
+    int64_t pos = cta_begin(cm, cta);
+    const int64_t end = min(cta_begin(cm, cta + 1), cm.total);
     const int group = Hq / Hkv;
 
     Segment sg;
@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(FT)
     if (parts != nullptr && n_q != nullptr) {
         const CostMap cm = cost_map(n_q, B, Hq, num_ctas);
         int c_first, c_last, len;
-        head_ctas(n_q, Hq, bh, cm.chunk, &c_first, &c_last, &len);
+        head_ctas(n_q, Hq, bh, cm, &c_first, &c_last, &len);
         if (len > 0) {  // an empty head's single record is empty: skip it (may be unwritten)
             for (int c0 = c_first; c0 <= c_last; c0 += 8) {
                 const int cnt = min(8, c_last - c0 + 1);
