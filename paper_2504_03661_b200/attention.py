@@ -149,6 +149,27 @@ def _step_workspace(cfg, dev) -> "K.DecodeWorkspace":
     return cache[key]
 
 
+class _Staging:
+    """decode_step's pinned host <-> device staging (q, k_n, v_n, lengths)."""
+
+    def __init__(self, d, dev):
+        self.host = torch.empty(3 * d + 2, dtype=torch.float32).pin_memory()
+        self.host_i = self.host.view(torch.int32)
+        self.dev = torch.empty(3 * d + 2, dtype=torch.float32, device=dev)
+        self.dev_i = self.dev.view(torch.int32)
+        self.out = torch.empty(d, dtype=torch.float32).pin_memory()
+
+
+def _step_staging(d, dev) -> _Staging:
+    cache = getattr(_tls, "staging", None)
+    if cache is None:
+        cache = _tls.staging = {}
+    key = (str(dev), d)
+    if key not in cache:
+        cache[key] = _Staging(d, dev)
+    return cache[key]
+
+
 def _n_tensor(n: int, device) -> torch.Tensor:
     return torch.tensor([n], dtype=torch.int32, device=device)
 
@@ -284,19 +305,41 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         ck_raw = _decode_codes(snap.codes_K.device_codes(dev), cfg) if n_q else None
         cv_raw = _decode_codes(snap.codes_V.device_codes(dev), cfg) if n_q else None
         rk, rv = snap.recent_K, snap.recent_V
-    q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
-                  torch.float32, dev)
-    if q.shape[0] != cfg.d:
-        raise ValueError(f"query width {q.shape[0]} != codebook d {cfg.d}")
-    kc = to_device(k_n if _is_tensor(k_n) else np.asarray(k_n, dtype=np.float32),
-                   torch.float32, dev).reshape(-1)
-    vc = to_device(v_n if _is_tensor(v_n) else np.asarray(v_n, dtype=np.float32),
-                   torch.float32, dev).reshape(-1)
+    fast = (timings is None and hasattr(cache, "raw_snapshot")
+            and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits))
+    if host and fast:
+        # one pinned staging transfer for q, k_n, v_n and both lengths
+        qh = np.asarray(q_n, dtype=np.float32).ravel()
+        kh = np.asarray(k_n, dtype=np.float32).ravel()
+        vh = np.asarray(v_n, dtype=np.float32).ravel()
+        if qh.shape[0] != cfg.d:
+            raise ValueError(f"query width {qh.shape[0]} != codebook d {cfg.d}")
+        if kh.shape[0] != cfg.d or vh.shape[0] != cfg.d:
+            raise ValueError(f"k_n/v_n width must be d={cfg.d}")
+        st = _step_staging(cfg.d, dev)
+        d = cfg.d
+        st.host[:d] = torch.from_numpy(qh)
+        st.host[d:2 * d] = torch.from_numpy(kh)
+        st.host[2 * d:3 * d] = torch.from_numpy(vh)
+        st.host_i[3 * d] = n_q
+        st.host_i[3 * d + 1] = int(rk.shape[0])
+        st.dev.copy_(st.host, non_blocking=True)
+        q, kc, vc = st.dev[:d], st.dev[d:2 * d], st.dev[2 * d:3 * d]
+        nq_dev, nr_dev = st.dev_i[3 * d:3 * d + 1], st.dev_i[3 * d + 1:3 * d + 2]
+    else:
+        q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
+                      torch.float32, dev)
+        if q.shape[0] != cfg.d:
+            raise ValueError(f"query width {q.shape[0]} != codebook d {cfg.d}")
+        kc = to_device(k_n if _is_tensor(k_n) else np.asarray(k_n, dtype=np.float32),
+                       torch.float32, dev).reshape(-1)
+        vc = to_device(v_n if _is_tensor(v_n) else np.asarray(v_n, dtype=np.float32),
+                       torch.float32, dev).reshape(-1)
+        nq_dev = nr_dev = None
     if kc.shape[0] != cfg.d or vc.shape[0] != cfg.d:
         raise ValueError(f"k_n/v_n width must be d={cfg.d}")
 
-    if (timings is None and hasattr(cache, "raw_snapshot")
-            and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits)):
+    if fast:
         # one fused launch (quantized span + recent rows + current token, merge,
         # finalize) with a per-thread cached workspace
         ws = _step_workspace(cfg, dev)
@@ -308,18 +351,25 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         else:  # nothing quantized yet: any valid buffer (no code is read)
             ck = cv = torch.zeros((1, 1, 1, cfg.M), dtype=torch.uint8, device=dev)
         K.decode_attention(ws, 1, q.view(1, -1), sc, cb_K.device_key_layout(dev), ck, cv,
-                           _n_tensor(n_q, dev), cb_V.device_value_layout(dev),
+                           nq_dev if nq_dev is not None else _n_tensor(n_q, dev),
+                           cb_V.device_value_layout(dev),
                            recent_k=rk.view(1, 1, r, cfg.d) if r else None,
                            recent_v=rv.view(1, 1, r, cfg.d) if r else None,
-                           n_recent=_n_tensor(r, dev) if r else None,
+                           n_recent=(nr_dev if nr_dev is not None else _n_tensor(r, dev))
+                           if r else None,
                            k_cur=kc.view(1, 1, -1), v_cur=vc.view(1, 1, -1), out=out)
         if counters is not None:
             counters.lut_lookups += n_q * cfg.M
             counters.adds += n_q * cfg.M
             counters.code_bytes_read += 2 * n_q * cfg.M * cfg.cell_width
             counters.dense_bytes_read += 2 * (r + 1) * cfg.d * 4
+        if host:
+            st.out.copy_(out[0], non_blocking=True)
+            cache.append_decode(kc, vc)  # the device rows already uploaded
+            torch.cuda.current_stream(dev).synchronize()
+            return st.out.numpy().astype(np.float64)
         cache.append_decode(k_n, v_n)
-        return out[0].double().cpu().numpy() if host else out[0]
+        return out[0]
 
     t0 = time.perf_counter()
     ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
