@@ -100,7 +100,9 @@ constexpr int OFF_COL = OFF_RED + 4 * WMAX * 4;               // colsum[2 * NG][
 constexpr int OFF_DNS = OFF_COL + 2 * (WMAX / 4) * D * 4;     // dense m[W], l[W], acc[W][128]
 constexpr int OFF_BAR = OFF_DNS + (2 * WMAX + WMAX * D) * 4;  // 2 mbarriers
 constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [W / 4]
-constexpr int SMEM_BYTES = OFF_FLAG + 4 * (WMAX / 4);
+constexpr int OFF_NQ = OFF_FLAG + 4 * (WMAX / 4);               // n_q copy [kNqCache]
+constexpr int kNqCache = 256;  // batches whose lengths are kept in shared memory
+constexpr int SMEM_BYTES = OFF_NQ + 4 * kNqCache;
 
 #ifdef PQKV_TRACE
 // debug-only timeline: per (launch mod 64, CTA) [smid, t_entry, t_ready,
@@ -591,6 +593,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     float *dn_l = dn_m + WARPS;
     float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + WARPS);
     int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
+    int *nq_s = reinterpret_cast<int *>(smem + OFF_NQ);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     if ((sbase & 0xFFFFFFu) != kDynBase) __trap();  // layout assumption (see lds_f32)
     const uint32_t cta_byte = sbase & 0xFF000000u;
@@ -631,12 +634,17 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     Segment s0;
     bool have_s0 = false;
     int64_t pos = 0, end = 0;
+    // the lengths are read from global memory once, here; the segment walks
+    // below (after a barrier) use the shared-memory copy
+    const bool nq_cached = A.B <= kNqCache;
     auto first_ring = [&]() {
         cm = cost_map(A.n_q, A.B, Hqv, A.num_ctas);
         pos = cta_begin(cm, cta);
         end = min(cta_begin(cm, cta + 1), cm.total);
         int64_t p0 = pos;
         have_s0 = next_segment(A.n_q, A.B, Hqv, &p0, end, &s0);
+        if (nq_cached)
+            for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = A.n_q[bb];
         if (have_s0) {
             const int b = s0.bh / Hqv, hkv = (s0.bh - b * Hqv) * HG / group;
             const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
@@ -689,9 +697,11 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     bool cv_ready = false;
     uint32_t lut_phase = 0;
 
+    const int32_t *nq = nq_cached ? nq_s : A.n_q;
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
+    if (nq_cached) __syncthreads();  // nq_s is written
     Segment sg;
-    while (next_segment(A.n_q, A.B, Hqv, &pos, end, &sg)) {
+    while (next_segment(nq, A.B, Hqv, &pos, end, &sg)) {
         const int vh = sg.bh;  // virtual head: query heads hq0 .. hq0 + HG - 1
         const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
         const int bh0 = b * A.Hq + hq0;
@@ -948,10 +958,10 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         const int grp = tid >> 7, gt = tid & (D - 1);
         int64_t p2 = cta_begin(cm, cta);
         Segment s2;
-        for (int k = 0; next_segment(A.n_q, A.B, Hqv, &p2, end, &s2); ++k) {
+        for (int k = 0; next_segment(nq, A.B, Hqv, &p2, end, &s2); ++k) {
             if (k % NG != grp) continue;
             int c_first, c_last, len;
-            head_ctas(A.n_q, Hqv, s2.bh, cm, &c_first, &c_last, &len);
+            head_ctas(nq, Hqv, s2.bh, cm, &c_first, &c_last, &len);
             if (gt == 0) {
                 // acq_rel at gpu scope: releases this CTA's records (ordered
                 // before by the barrier, fences are cumulative) and, for the
