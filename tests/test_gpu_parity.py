@@ -350,6 +350,35 @@ def test_f16_two_heads_per_cta_matches_one():
     np.testing.assert_allclose(outs[0], outs[1], rtol=1e-3, atol=1e-4)
 
 
+@pytest.mark.parametrize("half", [False, True])
+def test_static_codebook_staging_bit_identical(half):
+    """With static codebooks and early codes (PQKV_DECODE_STATIC_CODEBOOKS |
+    EARLY_CODES, PDL) the value codebook and the first code ring are loaded
+    before the grid-dependency wait; the result is bit-identical to the plain
+    launch."""
+    from paper_2504_03661_b200 import kernels as K
+    B, Hq, Hkv, n, R = 2, 8, 8, 7000, 20
+    x = _fused_inputs(B, Hq, Hkv, n, R, 21)
+    cbv = x["cbv"]
+    if half:
+        cbv = K.value_codebook_layout(
+            torch.from_numpy(np.random.default_rng(21).standard_normal((64, 256, 2)).astype(
+                np.float32)).cuda(), 8, half=True)
+    nq = torch.tensor([7000, 1234], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([20, 0], dtype=torch.int32, device="cuda")
+    outs = []
+    for static in (False, True, True):
+        ws = K.DecodeWorkspace(B, Hq, 128, 64, 8)
+        out = torch.empty((B * Hq, 128), device="cuda")
+        K.decode_attention(ws, Hkv, x["q"], 0.09, x["cbk"], x["ck"], x["cv"], nq, cbv,
+                           recent_k=x["rk"], recent_v=x["rv"], n_recent=nr, k_cur=x["kc"],
+                           v_cur=x["vc"], out=out, pdl=static, static_codebooks=static,
+                           early_codes=static)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
 def _fused_inputs(B, Hq, Hkv, n, R, seed):
     from paper_2504_03661_b200 import kernels as K
     rng = np.random.default_rng(seed)
