@@ -294,10 +294,24 @@ def encode_rate(dev, L, Hkv, n, stream):
         e1.synchronize()
     t_layer = e0.elapsed_time(e1) / reps * 1e-3
     vectors = 2 * Hkv * n
+    # the filter scan's bound: per (vector, centroid pair) 4 packed f32x2 ops
+    # (fma pipe) and 7 alu-pipe ops (2 key LOP3 + 5 integer min/max, one of
+    # them three-input); the alu pipe retires 64 lanes/clk/SM vs 128 for the
+    # fma pipe and issue (scripts/micro/fma_peak.cu): 64 / 3.5 = 18.3
+    # candidates/clk/SM
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cand = vectors * M * 256 / t_layer
+    peak = sms * (64 / 3.5) * 1.965e9
     return {"value": n / (t_layer * L), "unit": "tokens/s (all layers, K+V, all KV heads)",
             "workload": f"{n}-token prefill x {Hkv} KV heads x K,V, one layer timed, x{L} layers",
             "ms_per_layer": t_layer * 1e3, "vectors_per_s": vectors / t_layer,
-            "tflops_98304_per_vector": vectors * M * 256 * 6 / t_layer / 1e12, "bit_exact": True}
+            "tflops_98304_per_vector": vectors * M * 256 * 6 / t_layer / 1e12, "bit_exact": True,
+            "roofline": {"bound": "alu pipe (distance-key min/max)", "achieved": cand,
+                         "peak": peak, "unit": "candidates/s (vector x centroid)",
+                         "frac": cand / peak,
+                         "peak_basis": "18.3 candidates/clk/SM (3.5 alu ops each) x SMs x "
+                                       "1965 MHz; alu pipe 64 lanes/clk/SM measured "
+                                       "(scripts/micro/fma_peak.cu)"}}
 
 
 def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):

@@ -187,6 +187,12 @@ __global__ void __launch_bounds__(256) encode_dsub2(const TX *__restrict__ x, in
 // reference's argmin (no other centroid can reach it, and no exact fp64 tie
 // is possible); otherwise -- near ties, exact ties, x on a centroid -- the
 // (vector, subspace) is re-scanned with the exact FP64 formula above.
+#ifndef PQKV_ENC_FILTER_VPT
+#define PQKV_ENC_FILTER_VPT 8  // vectors per thread of the filter scan (4: -3%)
+#endif
+#ifndef PQKV_ENC_PAIR
+#define PQKV_ENC_PAIR 2  // 0: one centroid per step in scalar fp32 (measured 20% slower)
+#endif
 template <typename TX, typename CT, int VPT>
 __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict__ x, int64_t n,
                                                            int64_t ld_x,
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
     double *cc_s = sm + 2 * (size_t)ksub;                              // [ksub]
     float2 *cf_s = reinterpret_cast<float2 *>(sm + 3 * (size_t)ksub);  // [ksub]
     __shared__ float ccmax_s;
-    const int i = blockIdx.y;
+    const int i = blockIdx.x;  // subspace fastest: the M blocks of a row block share its x sectors and code lines in L2
     const float2 *ci = reinterpret_cast<const float2 *>(cents + (size_t)i * ksub * 2);
     if (threadIdx.x == 0) ccmax_s = 0.f;
     __syncthreads();
@@ -214,14 +220,21 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
         const double a = f.x, b = f.y;
         c_s[c] = make_double2(a, b);
         cc_s[c] = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+#if PQKV_ENC_PAIR == 2
+        // centroid pairs as (-x_2p, -x_2p+1, -y_2p, -y_2p+1): packed f32x2 operands
+        float *cp = reinterpret_cast<float *>(cf_s) + 4 * (c >> 1) + (c & 1);
+        cp[0] = -f.x;
+        cp[2] = -f.y;
+#else
         cf_s[c] = f;
+#endif
         ccmax = fmaxf(ccmax, (float)cc_s[c]);
     }
     atomicMax(reinterpret_cast<int *>(&ccmax_s), __float_as_int(ccmax));  // non-negative floats
     __syncthreads();
     ccmax = ccmax_s;
 
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x * VPT + threadIdx.x;
+    const int64_t v0 = (int64_t)blockIdx.y * blockDim.x * VPT + threadIdx.x;
     // best / second-best as sortable keys: the distance's bits (d >= 0, so its
     // bit pattern orders like the value) with the low mantissa bits replaced
     // by the centroid index -- one LOP3 + three integer min/max per centroid
@@ -237,6 +250,39 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
         b1[k] = 0xffffffffu;
         b2[k] = 0xffffffffu;
     }
+#if PQKV_ENC_PAIR == 2
+    // two centroids per step, their distances in packed f32x2 arithmetic (the
+    // same roundings as the scalar form, so the same keys), and the three-input
+    // min update below
+    const float4 *cf4 = reinterpret_cast<const float4 *>(cf_s);
+    unsigned long long xp0[VPT], xp1[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        asm("mov.b64 %0, {%1,%1};" : "=l"(xp0[k]) : "f"(xf0[k]));
+        asm("mov.b64 %0, {%1,%1};" : "=l"(xp1[k]) : "f"(xf1[k]));
+    }
+    for (int c = 0; c < ksub; c += 2) {
+        const float4 cv = cf4[c >> 1];
+        unsigned long long ncx, ncy;
+        asm("mov.b64 %0, {%1,%2};" : "=l"(ncx) : "f"(cv.x), "f"(cv.y));
+        asm("mov.b64 %0, {%1,%2};" : "=l"(ncy) : "f"(cv.z), "f"(cv.w));
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            unsigned long long dx, dy, dd;
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(xp0[k]), "l"(ncx));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(xp1[k]), "l"(ncy));
+            asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(dd) : "l"(dx));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(dd) : "l"(dy));
+            uint32_t da, db;
+            asm("mov.b64 {%0,%1}, %2;" : "=r"(da), "=r"(db) : "l"(dd));
+            const uint32_t ka = (da & ~cmask) | (uint32_t)c;
+            const uint32_t kb = (db & ~cmask) | (uint32_t)(c + 1);
+            const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+            b2[k] = min(min(b2[k], hi), max(b1[k], lo));
+            b1[k] = min(b1[k], lo);
+        }
+    }
+#else
 #pragma unroll 2
     for (int c = 0; c < ksub; ++c) {
         const float2 cv = cf_s[c];
@@ -248,6 +294,7 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
             b1[k] = min(b1[k], key);
         }
     }
+#endif
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const int64_t v = v0 + (int64_t)k * blockDim.x;
@@ -278,12 +325,11 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
     }
 }
 
-template <typename TX, typename CT>
-int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
-                        int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
-                        cudaStream_t st, int batches = 1, int64_t x_bs = 0, int64_t c_bs = 0,
-                        int64_t codes_bs = 0) {
-    constexpr int VPT = PQKV_ENC_VPT;
+template <typename TX, typename CT, int VPT>
+int launch_dsub2_filter_vpt(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
+                            int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
+                            cudaStream_t st, int batches, int64_t x_bs, int64_t c_bs,
+                            int64_t codes_bs) {
     const size_t smem = (size_t)ksub * (3 * sizeof(double) + sizeof(float2));
     auto k = encode_dsub2_filter<TX, CT, VPT>;
     if (smem > 48 * 1024) {
@@ -291,10 +337,25 @@ int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cen
                                              (int)smem);
         if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
     }
-    dim3 grid((unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)M, (unsigned)batches);
+    dim3 grid((unsigned)M, (unsigned)((n + 256 * VPT - 1) / (256 * VPT)), (unsigned)batches);
     k<<<grid, 256, smem, st>>>((const TX *)x, n, ld_x, cents, ksub, (CT *)codes, ld_codes,
                                rot_base, x_bs, c_bs, codes_bs);
     return launch_status("pqkv_encode");
+}
+
+// 8 vectors per thread for large inputs (prefill); 4 for small batches (the
+// append path's 32-row flushes), where 8 would leave half the lanes idle
+template <typename TX, typename CT>
+int launch_dsub2_filter(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
+                        int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
+                        cudaStream_t st, int batches = 1, int64_t x_bs = 0, int64_t c_bs = 0,
+                        int64_t codes_bs = 0) {
+    if (n >= 256 * PQKV_ENC_FILTER_VPT * 4)
+        return launch_dsub2_filter_vpt<TX, CT, PQKV_ENC_FILTER_VPT>(
+            x, n, ld_x, cents, M, ksub, codes, ld_codes, rot_base, st, batches, x_bs, c_bs,
+            codes_bs);
+    return launch_dsub2_filter_vpt<TX, CT, 4>(x, n, ld_x, cents, M, ksub, codes, ld_codes,
+                                             rot_base, st, batches, x_bs, c_bs, codes_bs);
 }
 
 template <typename TX, typename CT>
@@ -379,7 +440,7 @@ int dispatch_encode(const void *x, int64_t n, int d, int64_t ld_x, const float *
             case 2:
 #if PQKV_ENC_VPT > 0
 #if PQKV_ENC_FILTER
-                if (ksub * 32 <= 160 * 1024)
+                if (ksub * 32 <= 160 * 1024 && n <= (int64_t)65535 * 256 * PQKV_ENC_FILTER_VPT)
                     return launch_dsub2_filter<TX, CT>(x, n, ld_x, cents, M, ksub, codes,
                                                        ld_codes, rot_base, st);
 #endif
