@@ -145,6 +145,7 @@ struct Args {
     int trace_id;  // PQKV_TRACE builds: launch sequence number
 };
 
+#if PQKV_LANE8
 __device__ __forceinline__ uint2 ld_stream8(const uint8_t *p) {
     uint2 r;
     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
@@ -152,6 +153,7 @@ __device__ __forceinline__ uint2 ld_stream8(const uint8_t *p) {
                  : "l"(p));
     return r;
 }
+#endif
 __device__ __forceinline__ uint4 ld_stream(const uint8_t *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

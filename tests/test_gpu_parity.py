@@ -74,19 +74,19 @@ def test_encode_large_m64b8_vs_c_oracle():
     np.testing.assert_array_equal(got, want)
 
 
-@pytest.mark.parametrize("scale", [1.0, 1e-3, 1e3])
-def test_encode_near_ties_vs_oracle(scale):
+@pytest.mark.parametrize("scale,n", [(1.0, 3072), (1e-3, 3072), (1e3, 3072), (1.0, 12289)])
+def test_encode_near_ties_vs_oracle(scale, n):
     """The fp32 filter of the dsub=2 encoder hands near ties to the exact fp64
     scan: vectors on centroids, on midpoints between centroid pairs (exact and
     rounded ties), and nudged by a few ulps off midpoints -- bit-exact against
-    the fp64 restatement of assign_codes at three magnitudes."""
+    the fp64 restatement of assign_codes at three magnitudes, on both the
+    4- and the 8-vectors-per-thread scan (n >= 8192) with a ragged tail."""
     from paper_2504_03661_b200 import kernels as K
     rng = np.random.default_rng(11)
     M, ksub = 64, 256
     cents = (rng.standard_normal((M, ksub, 2)) * scale).astype(np.float32)
     # exact duplicate centroids: ties in fp64 -> lowest index
     cents[:, 200] = cents[:, 17]
-    n = 3072
     X = np.empty((n, 2 * M), dtype=np.float32)
     for i in range(M):
         a = rng.integers(0, ksub, n)
