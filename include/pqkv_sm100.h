@@ -182,9 +182,6 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                        const float *v_cur, float *out, float *lse,
                        float *merged, void *stream);
 
-/* Merge n_parts partial records per head in index order (merge_partials,
- * attention.py:193-204; the cross-GPU log-sum-exp merge of a sequence
- * split) and optionally finalize.  parts: [n_parts][n_heads][d+4]. */
 /* Flags of pqkv_decode_attention. */
 #define PQKV_DECODE_PDL 1 /* programmatic dependent launch: the grid may start
                              while the previous kernel on the stream drains;
@@ -210,7 +207,7 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
 /* One fused launch per layer: decode_step (attention.py:214-287) for every
  * (b, hq) -- pqkv_decode_partials' quantized span, the dense partial of the
  * recent rows + current token (dense_partial :169-190, computed by the CTA
- * holding the head's first quantized tokens), and, by the last CTA to finish
+ * holding the head's last quantized tokens), and, by the last CTA to finish
  * each head (an arrival counter), the fixed-order merge_partials (:193-204)
  * and finalize (:207-211).  Arguments as pqkv_decode_partials plus those of
  * pqkv_decode_finish, and
@@ -231,6 +228,9 @@ int pqkv_decode_attention(const float *q, float scale, const float *cb_k,
                           float *partials, int32_t *counters, float *out,
                           float *lse, float *merged, int flags, void *stream);
 
+/* Merge n_parts partial records per head in index order (merge_partials,
+ * attention.py:193-204; the cross-GPU log-sum-exp merge of a sequence
+ * split) and optionally finalize.  parts: [n_parts][n_heads][d+4]. */
 int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_heads,
                         int d, float *out, float *lse, float *merged,
                         void *stream);
