@@ -176,3 +176,38 @@ def test_shard_tokens_cover_exactly_once():
             spans = [shard_tokens(n, r, w) for r in range(w)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+
+
+def test_plain_c_consumer_links_and_runs(lib, tmp_path):
+    """A C99 host includes the header and links libpqkv_sm100.so directly (the
+    serving-engine integration of INTEGRATION.md): version, argument errors
+    with messages, no GPU needed for either."""
+    import shutil
+    import subprocess
+    from paper_2504_03661_b200 import _native as N
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "host.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <string.h>
+#include "pqkv_sm100.h"
+int main(void) {
+    if (pqkv_version() != 1) return 10;
+    int rc = pqkv_decode_attention(NULL, 0.1f, NULL, NULL, 1, 6, 4, NULL, NULL, 0, NULL, NULL,
+                                   128, 64, 8, NULL, NULL, 0, NULL, NULL, NULL, 1, NULL, NULL,
+                                   NULL, NULL, NULL, PQKV_DECODE_PDL, NULL);
+    if (rc != PQKV_EINVAL) return 11;
+    if (strstr(pqkv_last_error(), "multiple") == NULL) return 12;
+    printf("ok %s\n", pqkv_last_error());
+    return 0;
+}
+''')
+    libdir = os.path.dirname(N.library_path())
+    exe = tmp_path / "host"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-o", str(exe), "-L", libdir, "-l:" + os.path.basename(
+                        N.library_path()), "-Wl,-rpath," + libdir], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert r.stdout.startswith("ok")
