@@ -171,7 +171,8 @@ def _step_staging(d, dev) -> _Staging:
 
 
 def _n_tensor(n: int, device) -> torch.Tensor:
-    return torch.tensor([n], dtype=torch.int32, device=device)
+    # a fill launch with the value as its argument: no host->device copy, no sync
+    return torch.full((1,), n, dtype=torch.int32, device=device)
 
 
 def _partial_from_record(rec: torch.Tensor, host: bool) -> SoftmaxPartial:
@@ -296,7 +297,11 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
     sc = _scale(cfg.d, scale)
     host = not _is_tensor(q_n)
     dev = getattr(cache, "device", None) or default_device()
-    if hasattr(cache, "raw_snapshot"):       # this package's GPU cache: no copies
+    fast = (timings is None and hasattr(cache, "raw_snapshot")
+            and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits))
+    if fast and hasattr(cache, "raw_view"):  # one fused launch: views, stream-ordered
+        ck_raw, cv_raw, rk, rv, n_q, _ = cache.raw_view()
+    elif hasattr(cache, "raw_snapshot"):     # this package's GPU cache: no layout copies
         ck_raw, cv_raw, rk, rv, n_q, _ = cache.raw_snapshot()
         ck_raw, cv_raw = ck_raw.contiguous(), cv_raw.contiguous()
     else:                                    # any object with the reference snapshot()
@@ -305,8 +310,6 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         ck_raw = _decode_codes(snap.codes_K.device_codes(dev), cfg) if n_q else None
         cv_raw = _decode_codes(snap.codes_V.device_codes(dev), cfg) if n_q else None
         rk, rv = snap.recent_K, snap.recent_V
-    fast = (timings is None and hasattr(cache, "raw_snapshot")
-            and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits))
     if host and fast:
         # one pinned staging transfer for q, k_n, v_n and both lengths
         qh = np.asarray(q_n, dtype=np.float32).ravel()

@@ -328,6 +328,19 @@ class LayerKVCache:
             rv = self._rv[self._r0: self._r0 + self._rlen].clone()
             return (self._store_k[:n_q], self._store_v[:n_q], rk, rv, n_q, self._n_total)
 
+    def raw_view(self):
+        """raw_snapshot without the copies of the recent rows: views valid for
+        work enqueued on the current stream before the next append (every
+        write to the recent ring -- append, compaction -- is enqueued on the
+        caller's stream, so it is ordered after that work).  decode_step's
+        fused path."""
+        with self._lock:
+            self._publish_completed()
+            n_q = self._n_q
+            rk = self._rk[self._r0: self._r0 + self._rlen]
+            rv = self._rv[self._r0: self._r0 + self._rlen]
+            return (self._store_k[:n_q], self._store_v[:n_q], rk, rv, n_q, self._n_total)
+
     @property
     def code_layout(self) -> str:
         return self._layout
