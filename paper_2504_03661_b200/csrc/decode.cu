@@ -142,6 +142,9 @@ struct Args {
     float *out, *lse, *merged;
     int early_cv;     // codebooks may be read before the grid-dependency wait
     int early_codes;  // n_q and the codes below it may be read before it, too
+    int share;        // P > 1: CTAs c = P j + k (k < P) split the same token ranges of the
+                      // P virtual heads of one KV head (P j .. P j + P - 1), concurrently,
+                      // so each code line is fetched from DRAM once and hit in L2 P - 1 times
     int trace_id;  // PQKV_TRACE builds: launch sequence number
 };
 
@@ -490,10 +493,13 @@ __device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb,
 // (merge_partials :193-204, finalize :207-211).  Threads tid < D, one output
 // dimension each.  Out of line: runs once per head.
 // Records of (split c, virtual head vh, head h of HG) live at HG (c + vh) + h;
-// bh is the query head (dense record dense_base + bh, outputs row bh).
+// bh is the query head (dense record dense_base + bh, outputs row bh).  With
+// a shared code stream (Args::share = P) c and vh count CTA groups and
+// virtual-head groups, and member `half` of the group is at
+// HG ((c + vh) P + half) + h.
 __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base, int hg, int vh,
                                          int h, int bh, int c_first, int c_last, int tid,
-                                         float *out, float *lse, float *merged) {
+                                         float *out, float *lse, float *merged, int P, int half) {
     const float *drec = parts + (dense_base + bh) * (D + kPS);
     // the dense record and the first batch are in flight before any is consumed
     const float dm = __ldcg(drec), dl = __ldcg(drec + 1), da = __ldcg(drec + kPS + tid);
@@ -504,7 +510,8 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (k < cnt) {
-                const float *rec = parts + ((int64_t)hg * (c0 + k + vh) + h) * (D + kPS);
+                const float *rec =
+                    parts + ((int64_t)hg * ((int64_t)(c0 + k + vh) * P + half) + h) * (D + kPS);
                 rm[k] = __ldcg(rec);
                 rl[k] = __ldcg(rec + 1);
                 ra[k] = __ldcg(rec + kPS + tid);
@@ -624,6 +631,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // 64 live registers across it spill the main loop -- measured)
     const int cta = blockIdx.x;
     const int group = A.Hq / A.Hkv;
+    // shared code stream: the cost map runs over CTA groups and virtual-head
+    // groups of P; member `half` of a CTA group serves member `half` of each
+    // virtual-head group it holds
+    const int P = A.share > 1 ? A.share : 1;
+    const int pc = cta / P, half = cta - pc * P, Hqp = Hqv / P;
+    auto vhead = [&](int ph) {
+        const int bb = ph / Hqp;
+        return bb * Hqv + (ph - bb * Hqp) * P + half;
+    };
     // The first segment's code ring.  With early_codes (n_q and the codes
     // below it were written before the previous kernel on the stream started)
     // the cost map and these loads are issued before the grid-dependency wait;
@@ -640,15 +656,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // below (after a barrier) use the shared-memory copy
     const bool nq_cached = A.B <= kNqCache;
     auto first_ring = [&]() {
-        cm = cost_map(A.n_q, A.B, Hqv, A.num_ctas);
-        pos = cta_begin(cm, cta);
-        end = min(cta_begin(cm, cta + 1), cm.total);
+        cm = cost_map(A.n_q, A.B, Hqp, A.num_ctas / P);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
         int64_t p0 = pos;
-        have_s0 = next_segment(A.n_q, A.B, Hqv, &p0, end, &s0);
+        have_s0 = next_segment(A.n_q, A.B, Hqp, &p0, end, &s0);
         if (nq_cached)
             for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = A.n_q[bb];
         if (have_s0) {
-            const int b = s0.bh / Hqv, hkv = (s0.bh - b * Hqv) * HG / group;
+            const int vh0 = vhead(s0.bh);
+            const int b = vh0 / Hqv, hkv = (vh0 - b * Hqv) * HG / group;
             const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
             const int u0 = s0.lo / UT;
 #pragma unroll
@@ -703,8 +720,8 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
     if (nq_cached) __syncthreads();  // nq_s is written
     Segment sg;
-    while (next_segment(nq, A.B, Hqv, &pos, end, &sg)) {
-        const int vh = sg.bh;  // virtual head: query heads hq0 .. hq0 + HG - 1
+    while (next_segment(nq, A.B, Hqp, &pos, end, &sg)) {
+        const int vh = vhead(sg.bh);  // virtual head: query heads hq0 .. hq0 + HG - 1
         const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
         const int bh0 = b * A.Hq + hq0;
         const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
@@ -926,7 +943,8 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         if (tid < D) {
 #pragma unroll
             for (int h = 0; h < HG; ++h) {
-                float *rec = A.parts + ((int64_t)HG * (cta + vh) + h) * (D + kPS);
+                float *rec =
+                    A.parts + ((int64_t)HG * ((int64_t)(pc + sg.bh) * P + half) + h) * (D + kPS);
                 float a = colsum[h * NG][tid];
 #pragma unroll
                 for (int pp = 1; pp < NG; ++pp) a += colsum[h * NG + pp][tid];
@@ -958,12 +976,13 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     if (A.counters != nullptr) {
         __syncthreads();  // every record (and dense record) write of this CTA is done
         const int grp = tid >> 7, gt = tid & (D - 1);
-        int64_t p2 = cta_begin(cm, cta);
+        int64_t p2 = cta_begin(cm, pc);
         Segment s2;
-        for (int k = 0; next_segment(nq, A.B, Hqv, &p2, end, &s2); ++k) {
+        for (int k = 0; next_segment(nq, A.B, Hqp, &p2, end, &s2); ++k) {
             if (k % NG != grp) continue;
             int c_first, c_last, len;
-            head_ctas(nq, Hqv, s2.bh, cm, &c_first, &c_last, &len);
+            head_ctas(nq, Hqp, s2.bh, cm, &c_first, &c_last, &len);
+            const int vh2 = vhead(s2.bh);
             if (gt == 0) {
                 // acq_rel at gpu scope: releases this CTA's records (ordered
                 // before by the barrier, fences are cumulative) and, for the
@@ -971,21 +990,22 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 int old;
                 asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;"
                              : "=r"(old)
-                             : "l"(A.counters + s2.bh)
+                             : "l"(A.counters + vh2)
                              : "memory");
                 const bool last = (old == c_last - c_first);
-                if (last) A.counters[s2.bh] = 0;  // ready for the next launch
+                if (last) A.counters[vh2] = 0;  // ready for the next launch
                 flag_s[grp] = last ? 1 : 0;
             }
             named_bar_sync(1 + grp, D);  // this group's 128 threads
             const bool last = flag_s[grp] != 0;
             named_bar_sync(1 + grp, D);  // flag_s[grp] is read before its reuse
             if (last) {
-                const int b2 = s2.bh / Hqv, bq0 = b2 * A.Hq + (s2.bh - b2 * Hqv) * HG;
+                const int b2 = vh2 / Hqv, bq0 = b2 * A.Hq + (vh2 - b2 * Hqv) * HG;
 #pragma unroll
                 for (int h = 0; h < HG; ++h)
                     finish_head(A.parts, (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq, HG,
-                                s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged);
+                                s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged,
+                                P, half);
             }
         }
     }
@@ -1372,6 +1392,9 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
     return PQKV_OK;
 }
 
+#ifndef PQKV_SHARE
+#define PQKV_SHARE 1
+#endif
 #ifndef PQKV_GQA2_WARPS
 #define PQKV_GQA2_WARPS 12
 #endif
@@ -1568,6 +1591,17 @@ extern "C" int pqkv_decode_attention(
     a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
     a.early_codes = (flags & PQKV_DECODE_EARLY_CODES) ? 1 : 0;
     const bool pdl = (flags & PQKV_DECODE_PDL) != 0;
+    // GQA: the CTAs serving the virtual heads of one KV head stream its codes
+    // concurrently (one DRAM fetch, L2 hits for the others) -- P = virtual
+    // heads per KV head, reduced until it divides the grid
+    {
+        const int group = Hq / Hkv;
+        const bool two = (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) && group % 2 == 0 &&
+                         !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA);
+        int P = PQKV_SHARE ? group / (two ? 2 : 1) : 1;
+        while (P > 1 && (num_ctas % P != 0 || P > 16)) P = (P % 2 == 0) ? P / 2 : 1;
+        a.share = P;
+    }
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
         // even GQA groups: one CTA serves two query heads of a KV head
         if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA))

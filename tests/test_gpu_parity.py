@@ -306,6 +306,15 @@ def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("num_ctas", [7, 148, 150, 1000])
+def test_gqa_shared_stream_grids(num_ctas):
+    """GQA 8:1 exact: the 8 CTAs of a group split the same token ranges of one
+    KV head's 8 query heads (shared code stream); grids not divisible by 8
+    fall back to groups of 4, 2 or 1 -- all match the oracle."""
+    got, want = _batched_case(2, 16, 2, 6000, [6000, 2500], [9, 31], num_ctas=num_ctas)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
 @pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
     (1, 4, 4, 3000, [3000], [31]),                   # MHA: one query head per CTA
     (2, 8, 2, 5000, [4999, 1234], [5, 32]),          # G = 4: two query heads per CTA
@@ -397,9 +406,12 @@ def _fused_inputs(B, Hq, Hkv, n, R, seed):
 
 @pytest.mark.parametrize("pdl", [False, True])
 def test_fused_launch_matches_two_launch_path(pdl):
-    """pqkv_decode_attention (one launch: dense window by the first CTA of a
-    head, last-arriver merge) == pqkv_decode_partials + pqkv_decode_finish,
-    for out, lse and the merged record; counters return to zero."""
+    """pqkv_decode_attention (one launch: dense window by the CTA holding a
+    head's last tokens, last-arriver merge) == pqkv_decode_partials +
+    pqkv_decode_finish, for out, lse and the merged record; counters return to
+    zero.  The fused launch splits GQA heads differently (the CTAs of one KV
+    head's query heads share token ranges), so the partial sums associate
+    differently: fp32 reassociation tolerance."""
     from paper_2504_03661_b200 import kernels as K
     B, Hq, Hkv, n, R = 3, 8, 4, 9000, 32
     x = _fused_inputs(B, Hq, Hkv, n, R, 5)
@@ -420,9 +432,9 @@ def test_fused_launch_matches_two_launch_path(pdl):
                            pdl=pdl, static_codebooks=pdl)
     torch.cuda.synchronize()
     assert int(ws.counters.abs().sum()) == 0
-    np.testing.assert_allclose(o2.cpu().numpy(), o1.cpu().numpy(), rtol=2e-6, atol=1e-6)
+    np.testing.assert_allclose(o2.cpu().numpy(), o1.cpu().numpy(), rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(l2.cpu().numpy(), l1.cpu().numpy(), rtol=1e-6, atol=1e-6)
-    np.testing.assert_allclose(m2.cpu().numpy(), m1.cpu().numpy(), rtol=2e-6, atol=1e-6)
+    np.testing.assert_allclose(m2.cpu().numpy(), m1.cpu().numpy(), rtol=1e-5, atol=1e-5)
 
 
 def test_fused_graph_replay_deterministic():
