@@ -18,5 +18,6 @@ from .attention import (Lut, SoftmaxPartial, Counters, empty_partial, build_key_
                         decode_step)
 from .fileio import (FormatError, read_codebook, write_codebook, read_cache_dump,
                      write_cache_dump, dump_cache, read_tensor, write_tensor)
+from .training import kmeans_train, train_codebooks
 
 __version__ = "0.1.0"

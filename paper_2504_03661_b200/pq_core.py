@@ -51,8 +51,8 @@ def to_device(x, dtype=None, device=None) -> torch.Tensor:
 
 @dataclass(frozen=True)
 class PQConfig:
-    """Subspace geometry (pq_core.py:31-75).  kmeans_* / seed are kept for
-    signature compatibility; training is offline and not part of this path."""
+    """Subspace geometry (pq_core.py:31-75).  kmeans_* / seed drive the
+    offline codebook training (training.py)."""
 
     d: int
     M: int

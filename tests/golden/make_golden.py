@@ -228,16 +228,47 @@ def make_synth(harness):
     np.savez_compressed(os.path.join(OUT, "synth.npz"), **out)
 
 
+def make_kmeans(pq_core, harness):
+    """kmeans_train / train_codebooks (pq_core.py:171-266): separated blobs,
+    a Gaussian cloud, fewer distinct points than k, duplicated rows, and a
+    train_codebooks run on synth_kv keys (m8b4, d=16)."""
+    out = {}
+    rng = np.random.default_rng(21)
+    centers = np.array([[0, 0], [8, 0], [0, 8], [8, 8]], np.float64)
+    blobs = (centers[rng.integers(0, 4, 400)] + 0.3 * rng.standard_normal((400, 2)))
+    cases = {
+        "blobs": (blobs.astype(np.float32), 4, 25, 1e-4, 0),
+        "gauss": (rng.standard_normal((2000, 2)).astype(np.float32), 16, 25, 1e-4, 3),
+        "few": (np.repeat(np.array([[1, 2], [3, 4], [5, 6]], np.float32), 4, axis=0), 5, 10,
+                1e-4, 1),
+        "dups": (np.round(rng.standard_normal((300, 2)) * 2).astype(np.float32), 8, 30, 0.0, 2),
+        "oned": (rng.standard_normal(500).astype(np.float32), 6, 25, 1e-4, 4),
+    }
+    for name, (X, k, iters, tol, seed) in cases.items():
+        C, hist = pq_core.kmeans_train(X, k, iters=iters, tol=tol, seed=seed)
+        out[f"{name}_X"], out[f"{name}_C"], out[f"{name}_hist"] = X, C, np.array(hist)
+        out[f"{name}_args"] = np.array([k, iters, tol, seed], np.float64)
+    K, _ = harness.synth_kv(harness.SynthSpec(n_tokens=600, d=16, seed=5))
+    cfg = pq_core.PQConfig(d=16, M=8, nbits=4, kmeans_iters=12, seed=7)
+    cb = pq_core.train_codebooks(K, cfg, kind="key")
+    out["train_X"], out["train_C"] = K.astype(np.float32), cb.centroids
+    np.savez_compressed(os.path.join(OUT, "kmeans.npz"), **out)
+
+
 def main():
     pq_core, attention, kv_cache, fileio, harness = _ref()
     if "--synth-only" in sys.argv:
         make_synth(harness)
+        return
+    if "--kmeans-only" in sys.argv:
+        make_kmeans(pq_core, harness)
         return
     make_synth(harness)
     make_encode(pq_core, harness)
     make_attention(pq_core, attention, kv_cache)
     make_fileio(pq_core, fileio)
     make_cache(pq_core, kv_cache)
+    make_kmeans(pq_core, harness)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -105,3 +105,25 @@ def test_cli_verify_bench_breakdown_gpu(tmp_path):
     assert r.exit_code == 0, r.output
     assert (tmp_path / "breakdown.csv").read_text().splitlines()[0] == \
         ",".join(cli.BREAKDOWN_CSV_COLUMNS)
+
+
+@pytest.mark.gpu
+def test_cli_train_matches_reference_training(tmp_path):
+    """`train` (cli.py:108-155) on the golden training samples writes the
+    reference's codebook bit for bit (tests/golden/kmeans.npz, made by running
+    the reference's train_codebooks)."""
+    import os
+    from click.testing import CliRunner
+    from paper_2504_03661_b200 import cli, fileio
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "kmeans.npz"))
+    fileio.write_tensor(tmp_path / "k.f32", g["train_X"])
+    fileio.write_tensor(tmp_path / "v.f32", g["train_X"])
+    r = CliRunner().invoke(cli.main, ["train", "--keys", str(tmp_path / "k.f32"), "--values",
+                                      str(tmp_path / "v.f32"), "--m", "8", "--nbits", "4",
+                                      "--kmeans-iters", "12", "--seed", "7",
+                                      "--out", str(tmp_path)])
+    assert r.exit_code == 0, r.output
+    assert "bits_per_value" in r.output and "per-subspace distortion" in r.output
+    cb = fileio.read_codebook(tmp_path / "cb_key.pqkv")
+    np.testing.assert_array_equal(cb.centroids, g["train_C"])
+    assert fileio.read_codebook(tmp_path / "cb_value.pqkv").kind == "value"
