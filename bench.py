@@ -523,10 +523,73 @@ def run_ours(args):
     h2d = io_h.numel() * 4
     d2h = o_h.numel() * 4
 
-    def e2e_step():
+    def e2e_serial():
         io.copy_(io_h, non_blocking=True)
         graph.replay()
         o_h.copy_(out, non_blocking=True)
+
+    def capture_e2e(split=4, tail=4):
+        """The same step with its host copies inside the graph, pipelined: the
+        first `split` layers' inputs on the launch stream, the rest on a copy
+        stream behind them (joined before layer `split`), and the outputs of
+        all but the last `tail` layers read back on the copy stream while
+        those run.  Every copy stays inside the timed step."""
+        cs = torch.cuda.Stream(device=dev)
+        qh, kh = io_h[:nq_].view(L, B, Hq, D), io_h[nq_:nq_ + nk_].view(L, B, Hkv, D)
+        vh = io_h[nq_ + nk_:].view(L, B, Hkv, D)
+
+        def body():
+            for dst, src in ((q, qh), (kc, kh), (vc, vh)):
+                dst[:split].copy_(src[:split], non_blocking=True)
+            e_fork = torch.cuda.Event()
+            e_fork.record(stream)
+            cs.wait_event(e_fork)
+            with torch.cuda.stream(cs):
+                for dst, src in ((q, qh), (kc, kh), (vc, vh)):
+                    dst[split:].copy_(src[split:], non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(cs)
+            e_back = None
+            for l in range(L):
+                if l == split:
+                    stream.wait_event(e_in)
+                dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv[l], rk[l], rv[l], n_r,
+                    kc[l], vc[l], out=out[l])
+                if l == L - tail - 1:
+                    e_mid = torch.cuda.Event()
+                    e_mid.record(stream)
+                    cs.wait_event(e_mid)
+                    with torch.cuda.stream(cs):
+                        o_h[:L - tail].copy_(out[:L - tail], non_blocking=True)
+                        e_back = torch.cuda.Event()
+                        e_back.record(cs)
+            o_h[L - tail:].copy_(out[L - tail:], non_blocking=True)
+            stream.wait_event(e_back)
+
+        with torch.cuda.stream(stream):
+            body()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            body()
+        return gr
+
+    e2e_mode = "serial copies around the step graph"
+    e2e_step = e2e_serial
+    if not seq_split and not args.e2e_serial and L > 8:
+        with torch.cuda.stream(stream):
+            e2e_serial()
+        torch.cuda.synchronize()
+        o_ref = o_h.clone()
+        g_e2e = capture_e2e()
+        with torch.cuda.stream(stream):
+            g_e2e.replay()
+        torch.cuda.synchronize()
+        if not torch.equal(o_h, o_ref):
+            raise RuntimeError("pipelined end-to-end step disagrees with the serial one")
+        e2e_step = g_e2e.replay
+        e2e_mode = "copies pipelined inside the step graph (inputs of layers >= 4 behind " \
+                   "layers 0-3, outputs of layers < L-4 behind the last 4)"
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -584,7 +647,8 @@ def run_ours(args):
                          "kernel_share_of_step": share},
             "e2e": {"value": jobs * B * 1e3 / e2e_ms, "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "paper_2504_03661_b200.engine.PQDecoder (graph-replayed step)"},
+                    "api": "paper_2504_03661_b200.engine.PQDecoder (graph-replayed step)",
+                    "copies": e2e_mode},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "code_stream_gbs_step": 2 * L * B * Hkv * n * M / (ms * 1e-3) / 1e9}
@@ -612,6 +676,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="end-to-end copies before / after the step graph, not pipelined")
     ap.add_argument("--no-encode", action="store_true")
     ap.add_argument("--no-l2-persist", action="store_true",
                     help="do not pin the codebooks in L2 (persisting access-policy window)")
