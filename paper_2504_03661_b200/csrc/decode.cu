@@ -42,7 +42,10 @@
 //     head's records in CTA order and finalizes;
 //   * fp16 value-codebook mode: 4-byte value gathers + mixed f16 x f16 + f32
 //     FMAs; with an even GQA group a CTA serves HG = 2 query heads (two key
-//     tables, one value gather per code shared by both).
+//     tables, one value gather per code shared by both);
+//   * GQA shared code stream (Args::share = P): the P CTAs serving the P
+//     virtual heads of one KV head split the same token ranges at the same
+//     time, so each code line is fetched from DRAM once.
 #include <algorithm>
 #include <cstdlib>
 
