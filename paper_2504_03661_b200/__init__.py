@@ -19,5 +19,6 @@ from .attention import (Lut, SoftmaxPartial, Counters, empty_partial, build_key_
 from .fileio import (FormatError, read_codebook, write_codebook, read_cache_dump,
                      write_cache_dump, dump_cache, read_tensor, write_tensor)
 from .training import kmeans_train, train_codebooks
+from .baselines import IntQuantParams, integer_quantize, integer_dequantize, prefill_attention
 
 __version__ = "0.1.0"

@@ -255,6 +255,27 @@ def make_kmeans(pq_core, harness):
     np.savez_compressed(os.path.join(OUT, "kmeans.npz"), **out)
 
 
+def make_baselines(pq_core, attention):
+    """integer_quantize / integer_dequantize (pq_core.py:312-354) and
+    prefill_attention (attention.py:290-311)."""
+    out = {}
+    rng = np.random.default_rng(31)
+    X = (rng.standard_normal((64, 48)) * 3).astype(np.float32)
+    X[0, :4] = [0.5, 1.5, 2.5, -0.5]  # ties for round-half-to-even
+    for nb in (2, 4, 8):
+        for mode in ("symmetric", "asymmetric"):
+            Q, prm = pq_core.integer_quantize(X, nb, mode)
+            out[f"iq_{mode}_{nb}_Q"] = Q
+            out[f"iq_{mode}_{nb}_sz"] = np.array([prm.s, prm.z], np.float64)
+            out[f"iq_{mode}_{nb}_Xh"] = pq_core.integer_dequantize(Q, prm)
+    out["iq_X"] = X
+    Qp, Kp, Vp = (rng.standard_normal((n, 64)) for n in (7, 19, 19))
+    out["pf_Q"], out["pf_K"], out["pf_V"] = Qp, Kp, Vp
+    out["pf_causal"] = attention.prefill_attention(Qp, Kp, Vp)
+    out["pf_full"] = attention.prefill_attention(Qp, Kp, Vp, causal=False, scale=0.3)
+    np.savez_compressed(os.path.join(OUT, "baselines.npz"), **out)
+
+
 def main():
     pq_core, attention, kv_cache, fileio, harness = _ref()
     if "--synth-only" in sys.argv:
@@ -263,12 +284,16 @@ def main():
     if "--kmeans-only" in sys.argv:
         make_kmeans(pq_core, harness)
         return
+    if "--baselines-only" in sys.argv:
+        make_baselines(pq_core, attention)
+        return
     make_synth(harness)
     make_encode(pq_core, harness)
     make_attention(pq_core, attention, kv_cache)
     make_fileio(pq_core, fileio)
     make_cache(pq_core, kv_cache)
     make_kmeans(pq_core, harness)
+    make_baselines(pq_core, attention)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
