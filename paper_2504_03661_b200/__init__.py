@@ -20,5 +20,7 @@ from .fileio import (FormatError, read_codebook, write_codebook, read_cache_dump
                      write_cache_dump, dump_cache, read_tensor, write_tensor)
 from .training import kmeans_train, train_codebooks
 from .baselines import IntQuantParams, integer_quantize, integer_dequantize, prefill_attention
+from .analysis import (ChannelStats, SensitivityReport, channel_stats, isolate_outliers,
+                       sensitivity_study, compare_quantizers)
 
 __version__ = "0.1.0"

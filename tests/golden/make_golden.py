@@ -276,6 +276,30 @@ def make_baselines(pq_core, attention):
     np.savez_compressed(os.path.join(OUT, "baselines.npz"), **out)
 
 
+def make_analysis(pq_core, harness):
+    """channel_stats / isolate_outliers / sensitivity_study / compare_quantizers
+    (analysis.py:59-192) on synth_kv keys with outlier channels."""
+    from pqkv import analysis
+    out = {}
+    K, _ = harness.synth_kv(harness.SynthSpec(n_tokens=700, d=32, seed=9,
+                                              outlier_channels=[3, 20]))
+    out["X"] = K
+    st = analysis.channel_stats(K)
+    out["cs_mean"], out["cs_std"], out["cs_absmax"] = st.mean, st.std, st.absmax
+    out["cs_misc"] = np.array([st.global_absmax, st.outlier_threshold])
+    out["cs_outliers"] = np.array(st.outlier_channels)
+    entries, filt = analysis.isolate_outliers(K, 0.01)
+    out["io_entries"] = np.array(entries)
+    out["io_filtered"] = filt
+    cfg = pq_core.PQConfig(d=32, M=16, nbits=4, kmeans_iters=8, seed=2)
+    cq = analysis.compare_quantizers(K, cfg, 4)
+    out["cq"] = np.array([cq[k] for k in sorted(cq)])
+    for q in ("pq", "int"):
+        r = analysis.sensitivity_study(K, cfg, fraction=0.01, quantizer=q)
+        out[f"ss_{q}"] = np.array([r.err_full, r.err_filtered, r.sensitivity])
+    np.savez_compressed(os.path.join(OUT, "analysis.npz"), **out)
+
+
 def main():
     pq_core, attention, kv_cache, fileio, harness = _ref()
     if "--synth-only" in sys.argv:
@@ -287,6 +311,9 @@ def main():
     if "--baselines-only" in sys.argv:
         make_baselines(pq_core, attention)
         return
+    if "--analysis-only" in sys.argv:
+        make_analysis(pq_core, harness)
+        return
     make_synth(harness)
     make_encode(pq_core, harness)
     make_attention(pq_core, attention, kv_cache)
@@ -294,6 +321,7 @@ def main():
     make_cache(pq_core, kv_cache)
     make_kmeans(pq_core, harness)
     make_baselines(pq_core, attention)
+    make_analysis(pq_core, harness)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
