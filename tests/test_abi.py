@@ -211,3 +211,25 @@ int main(void) {
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert r.stdout.startswith("ok")
+
+
+@pytest.mark.gpu
+def test_integration_ctypes_binding_snippet():
+    """The ctypes binding INTEGRATION.md shows a pqkv maintainer (a drop-in for
+    _kernels.score_codes) runs against the built library and agrees with the
+    reference formula on random tables and codes."""
+    import re
+    import torch
+    from paper_2504_03661_b200 import _native as N
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# pqkv/_kernels_sm100\.py.*?)```", doc, re.S).group(1)
+    code = code.replace('ctypes.CDLL("libpqkv_sm100.so")', f'ctypes.CDLL({N.library_path()!r})')
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    rng = np.random.default_rng(3)
+    lut = rng.standard_normal((16, 256))           # reference Lut.table: (M, ksub)
+    codes = rng.integers(0, 256, (500, 16), dtype=np.uint8)
+    got = ns["score_codes"](lut, codes)
+    want = lut[np.arange(16)[None, :], codes].sum(axis=1)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
+    assert torch.cuda.is_available()
