@@ -112,6 +112,7 @@ constexpr int SMEM_BYTES = OFF_NQ + 4 * kNqCache;
 // t_loop0_end, t_exit, nseg, t_segs_done, t_post_wait, t_lut_pre, t_cv_ready]
 constexpr int kTraceLaunches = 64, kTraceCtas = 256;
 __device__ unsigned long long g_trace[kTraceLaunches * kTraceCtas * 16];
+__device__ unsigned long long g_wtrace[kTraceLaunches * kTraceCtas * 32];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -897,6 +898,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
 #ifdef PQKV_TRACE
+        if (nseg_ == 0 && lane == 0 && blockIdx.x < kTraceCtas)  // per-warp loop end
+            g_wtrace[((A.trace_id % kTraceLaunches) * kTraceCtas + blockIdx.x) * 32 + warp] =
+                gtime();
         if (nseg_++ == 0) PQKV_TR(3, gtime());
 #endif
 #pragma unroll
@@ -1374,6 +1378,11 @@ extern "C" int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas) {
 #ifdef PQKV_TRACE
 extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {  // n <= 64 * 256 * 16
     return cudaMemcpyFromSymbol(host, fast::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
+               ? 0 : 2;
+}
+extern "C" int pqkv_debug_wtrace(unsigned long long *host, int n) {  // n <= 64 * 256 * 32
+    return cudaMemcpyFromSymbol(host, fast::g_wtrace, sizeof(unsigned long long) * n) ==
+                   cudaSuccess
                ? 0 : 2;
 }
 #endif

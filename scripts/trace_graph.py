@@ -70,3 +70,16 @@ for name, c in (("post_wait", 7), ("cost_map", 10), ("lut_pre", 8), ("ring_issue
     print(f"  {name:10s} median {v:6.2f} us after the layer's first post-wait")
 print(f"per CTA (median over layers/CTAs): entry->ready {np.median(ready):.2f} us, ready->segs_done {np.median(loop):.2f} us, segs_done->exit {np.median(fin):.2f} us")
 np.save(os.path.join(ROOT, "gpurun_out", "trace_graph.npy"), T)
+# per-warp main-loop end (first segment): spread within each CTA
+Wt = np.zeros(64 * 256 * 32, dtype=np.uint64)
+N.load().pqkv_debug_wtrace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+if N.load().pqkv_debug_wtrace(Wt.ctypes.data, Wt.size) == 0:
+    Wt = Wt.reshape(64, 256, 32)[sl, :dec.ws.num_ctas, :16].astype(np.int64)
+    nseg = T[:, :, 5]
+    one = (nseg == 1)
+    spread = (Wt.max(axis=2) - Wt.min(axis=2)) / 1e3
+    order = np.argsort(np.median(((Wt - Wt.min(axis=2, keepdims=True)) / 1e3)[4:][one[4:]], axis=0))
+    print(f"warp loop-end spread within a CTA (1-segment CTAs): median {np.median(spread[4:][one[4:]]):.2f} us, "
+          f"p90 {np.percentile(spread[4:][one[4:]], 90):.2f} us")
+    lag = np.median(((Wt - Wt.min(axis=2, keepdims=True)) / 1e3)[4:][one[4:]], axis=0)
+    print("median lag per warp (us):", " ".join(f"{x:.2f}" for x in lag))
