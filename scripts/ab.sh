@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B the decode library variants built into paper_2504_03661_b200/_lib/ab_*.so
+# (scripts/build_variants.py)
 # usage (under gpurun): bash scripts/ab.sh <tag> [bench args...]
 T=${1:-ab}; shift; mkdir -p gpurun_out/$T
 for lib in paper_2504_03661_b200/_lib/ab_*.so; do
