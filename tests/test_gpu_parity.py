@@ -703,3 +703,27 @@ def test_codebook_file_to_device(golden, tmp_path):
     np.testing.assert_array_equal(cb.device_centroids().cpu().numpy(), g["f0_cents"])
     P.write_codebook(tmp_path / "back.pqkv", cb)
     assert (tmp_path / "back.pqkv").read_bytes() == raw
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomized_batched_configs(seed):
+    """Seeded random shapes through the fused path (PQDecoder): batch 1-3,
+    GQA groups 1/2/3/4/8, ragged and empty lengths, recent windows 0-32,
+    grids from 5 CTAs to 2 waves, exact and fp16 value-codebook modes."""
+    rng = np.random.default_rng(1000 + seed)
+    G = int(rng.choice([1, 2, 3, 4, 8]))
+    Hkv = int(rng.integers(1, 3))
+    B = int(rng.integers(1, 4))
+    cap = int(rng.integers(300, 3000))
+    n_q = [int(rng.integers(0, cap + 1)) for _ in range(B)]
+    n_r = [int(rng.integers(0, 33)) for _ in range(B)]
+    num_ctas = int(rng.choice([5, 37, 148, 296]))
+    half = bool(seed % 2)
+    res = _batched_case(B, G * Hkv, Hkv, cap, n_q, n_r, seed=seed, num_ctas=num_ctas,
+                        half_cv=half)
+    if half:
+        got, want, want16 = res
+        np.testing.assert_allclose(got, want16, rtol=1e-3, atol=1e-4)
+    else:
+        got, want = res
+        np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
