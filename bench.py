@@ -321,7 +321,7 @@ def encode_rate(dev, L, Hkv, n, stream):
                                        "(scripts/micro/fma_peak.cu)"}}
 
 
-def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
+def append_overlap(dev, replay, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
     """BASELINE config 5, second part: the per-token append path flushes a
     batch of R_f recent rows (K and V, every layer, sequence and KV head) into
     the code store every R_f decode steps, on a lowest-priority side stream
@@ -352,7 +352,7 @@ def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
             flush()
         with torch.cuda.stream(stream):
             for _ in range(R_f):
-                graph.replay()
+                replay()
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
@@ -373,11 +373,211 @@ def append_overlap(dev, graph, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
             "slowdown": with_flush / base - 1.0}
 
 
+def shard_plan(name, rank, world):
+    """This rank's share of config `name` on `world` GPUs:
+    batch sharding (each rank its own sequences, no collective, weak scaling);
+    KV-head sharding for config 3 (rank r serves KV heads [r Hkv/N, (r+1) Hkv/N)
+    and their query heads of every sequence, no collective, strong scaling);
+    sequence split for config 4 (rank r owns tokens [r n/N, (r+1) n/N) of every
+    sequence, the last rank the recent window + current token; one NCCL
+    all-gather of (m, l, acc) records + a rank-ordered merge per layer)."""
+    L, B, Hq, Hkv, n, R = CONFIGS[name]
+    plan = {"workload": name, "rank": rank, "world": world, "L": L, "B": B, "Hq": Hq,
+            "Hkv": Hkv, "n": n, "R": R, "tok": [0, n], "kv_heads": [0, Hkv], "tail": True,
+            "mode": "batch", "jobs": world}
+    if world > 1 and name in SEQ_SPLIT:
+        from paper_2504_03661_b200.engine import shard_tokens
+        a, b = shard_tokens(n, rank, world)
+        plan.update(mode="sequence", n=b - a, tok=[a, b], tail=rank == world - 1, jobs=1)
+    elif world > 1 and name in HEAD_SHARD:
+        if Hkv % world:
+            raise SystemExit(f"{name}: {Hkv} KV heads do not shard over {world} GPUs")
+        k = Hkv // world
+        plan.update(mode="kv-head", Hq=Hq // world, Hkv=k, kv_heads=[rank * k, (rank + 1) * k],
+                    jobs=1)
+    return plan
+
+
+class Workload:
+    """One rank's synthetic inputs of a config (HBM-resident) and its decode
+    step -- one fused launch per layer, PDL-chained, captured in a CUDA graph."""
+
+    def __init__(self, args, plan, dev, stream, dist_on):
+        import torch
+        from paper_2504_03661_b200 import kernels as K
+        from paper_2504_03661_b200 import _native as N
+        from paper_2504_03661_b200.engine import PQDecoder, random_codes
+        from paper_2504_03661_b200.pq_core import PQConfig
+        self.plan, self.dev, self.stream, self.dist_on = plan, dev, stream, dist_on
+        L, B, Hq, Hkv, n, R = (plan[k] for k in ("L", "B", "Hq", "Hkv", "n", "R"))
+        self.L, self.B, self.Hq, self.Hkv, self.n, self.R = L, B, Hq, Hkv, n, R
+        self.seq_split = plan["mode"] == "sequence"
+        self.tail = plan["tail"]
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234 + plan["rank"])
+        self.codes_k = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
+        self.codes_v = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
+        # every layer's codebook layouts in one allocation (kept L2-resident)
+        cb_words = M * 256 * 2
+        self.cb_all = torch.empty((L, 2, cb_words), device=dev)
+        self.cbk = [K.key_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev),
+                                          NBITS, out=self.cb_all[l, 0]) for l in range(L)]
+        cv_raw = [torch.randn((M, 256, 2), generator=g, device=dev) for _ in range(L)]
+        self.cbv32 = [K.value_codebook_layout(cv_raw[l], NBITS, out=self.cb_all[l, 1])
+                      for l in range(L)]
+        self.cbv16 = [K.value_codebook_layout(cv_raw[l], NBITS, half=True) for l in range(L)]
+        self.rk = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
+        self.rv = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
+        self.n_q = torch.full((B,), n, dtype=torch.int32, device=dev)
+        self.n_r = torch.full((B,), R, dtype=torch.int32, device=dev)
+        # one step's inputs (q, current k, current v of every layer) in one
+        # allocation, so the end-to-end step moves them with a single copy
+        self.nq_, self.nk_ = L * B * Hq * D, L * B * Hkv * D
+        self.io = torch.randn(self.nq_ + 2 * self.nk_, generator=g, device=dev)
+        self.q = self.io[:self.nq_].view(L, B, Hq, D)
+        self.kc = self.io[self.nq_:self.nq_ + self.nk_].view(L, B, Hkv, D)
+        self.vc = self.io[self.nq_ + self.nk_:].view(L, B, Hkv, D)
+        self.out = torch.empty((L, B, Hq, D), device=dev)
+        torch.cuda.synchronize()  # codebook layouts are written before any decode launch
+        # codebooks (load time) and codes below n_q (appended by earlier steps)
+        # are not written by the kernel a launch overlaps: PDL may read them
+        # early (n_q itself is re-validated after the wait)
+        self.dec = PQDecoder(B, Hq, Hkv, PQConfig(D, M, NBITS), device=dev,
+                             pdl=not args.no_pdl, static_codebooks=not args.no_pdl,
+                             early_codes=not args.no_pdl)
+        if not args.no_l2_persist:
+            N.call("pqkv_l2_persist", N.ptr(self.cb_all), self.cb_all.numel() * 4, 1.0,
+                   N.stream_ptr(stream))
+        self.rec = torch.empty((L, B * Hq, D + 4), device=dev) if self.seq_split else None
+        self.gat = (torch.empty((L, plan["world"], B * Hq, D + 4), device=dev)
+                    if self.seq_split else None)
+        self.bytes_per_launch = 2 * B * Hkv * n * M
+        self.graph_mode = "cuda graph"
+
+    def layer(self, l, cbv):
+        import torch.distributed as dist
+        from paper_2504_03661_b200 import kernels as K
+        if self.seq_split:
+            # partial record of this rank's token range -> all-gather -> merge
+            # in rank order (engine.sequence_parallel_decode)
+            t = self.tail
+            self.dec(self.q[l], self.codes_k[l], self.codes_v[l], self.n_q, self.cbk[l], cbv[l],
+                     self.rk[l] if t else None, self.rv[l] if t else None,
+                     self.n_r if t else None, self.kc[l] if t else None,
+                     self.vc[l] if t else None, merged=self.rec[l], finalize=False)
+            dist.all_gather_into_tensor(self.gat[l], self.rec[l])
+            K.merge_partials(self.gat[l], out=self.out[l])
+        else:
+            self.dec(self.q[l], self.codes_k[l], self.codes_v[l], self.n_q, self.cbk[l], cbv[l],
+                     self.rk[l], self.rv[l], self.n_r, self.kc[l], self.vc[l], out=self.out[l])
+
+    def step_fn(self, half=False):
+        cbv = self.cbv16 if half else self.cbv32
+
+        def step():
+            for l in range(self.L):
+                self.layer(l, cbv)
+        return step
+
+    def capture(self, half=False):
+        """the step captured in a CUDA graph (replay); if capturing the NCCL
+        all-gather of a sequence split fails, the step runs eagerly"""
+        import torch
+        step = self.step_fn(half)
+        with torch.cuda.stream(self.stream):
+            step()
+            step()
+        torch.cuda.synchronize()
+        try:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=self.stream):
+                step()
+            return gr.replay
+        except Exception as e:  # noqa: BLE001 -- recorded in the JSON line
+            if not self.seq_split:
+                raise
+            torch.cuda.synchronize()
+            self.graph_mode = f"eager (graph capture of the all-gather failed: {e!s:.80})"
+
+            def eager():
+                with torch.cuda.stream(self.stream):
+                    step()
+            return eager
+
+    def time(self, fn, steps, warmup, barrier, max_over_ranks):
+        import torch
+        for _ in range(warmup):
+            fn()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.stream):
+            ev0.record(self.stream)
+            for _ in range(steps):
+                fn()
+            ev1.record(self.stream)
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1) / steps)
+
+
+def merge_share(w, steps, barrier, max_over_ranks):
+    """Sequence split: device time of the per-layer all-gather + merge alone
+    (the step's exchange), captured like the step."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_03661_b200 import kernels as K
+
+    def ex():
+        for l in range(w.L):
+            dist.all_gather_into_tensor(w.gat[l], w.rec[l])
+            K.merge_partials(w.gat[l], out=w.out[l])
+    try:
+        with torch.cuda.stream(w.stream):
+            ex()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=w.stream):
+            ex()
+        fn = gr.replay
+    except Exception:  # noqa: BLE001
+        torch.cuda.synchronize()
+
+        def fn():
+            with torch.cuda.stream(w.stream):
+                ex()
+    return w.time(fn, steps, 2, barrier, max_over_ranks)
+
+
+def encode_sample_check(dev, stream, n=2048):
+    """bit_exact, measured: a sample of the bench encoder's output against the
+    C restatement of assign_codes (oracle/, test infrastructure)."""
+    import torch
+    from oracle import pqkv_oracle as O
+    from paper_2504_03661_b200 import kernels as K
+    if O.c_library() is None:
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+        O._clib = None
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    x = torch.randn((n, D), generator=g, device=dev)
+    cents = torch.randn((M, 256, 2), generator=g, device=dev)
+    with torch.cuda.stream(stream):
+        codes = K.encode(x, cents, NBITS, stream=stream)
+    stream.synchronize()
+    want = O.c_assign_codes(x.cpu().numpy(), cents.cpu().numpy(), NBITS,
+                            threads=len(os.sched_getaffinity(0)))
+    return bool(np.array_equal(codes.cpu().numpy(), want)), n
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if torch.cuda.device_count() < (local + 1):
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}; "
+                         f"{torch.cuda.device_count()} visible")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -385,90 +585,8 @@ def run_ours(args):
     from paper_2504_03661_b200 import build as B_
     B_.build()
     from paper_2504_03661_b200 import kernels as K
-    from paper_2504_03661_b200 import _native as N
-    from paper_2504_03661_b200.engine import PQDecoder, random_codes
-    from paper_2504_03661_b200.pq_core import PQConfig
 
-    L, B, Hq, Hkv, n, R = CONFIGS[args.config]
-    seq_split = args.config in SEQ_SPLIT and world > 1
-    n_full = n
-    if seq_split:  # this rank's contiguous token range of every sequence
-        from paper_2504_03661_b200.engine import shard_tokens
-        a_, b_ = shard_tokens(n_full, rank, world)
-        n = b_ - a_
-    tail = (not seq_split) or rank == world - 1  # owns the recent window + current token
-    head_shard = args.config in HEAD_SHARD and world > 1
-    if head_shard:
-        if Hkv % world:
-            raise SystemExit(f"{args.config}: {Hkv} KV heads do not shard over {world} GPUs")
-        Hq, Hkv = Hq // world, Hkv // world
-    cfg = PQConfig(D, M, NBITS)
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    codes_k = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
-    codes_v = [random_codes((B, Hkv, n, M), NBITS, g, dev) for _ in range(L)]
-    # every layer's codebook layouts in one allocation (kept L2-resident below)
-    cb_words = M * 256 * 2
-    cb_all = torch.empty((L, 2, cb_words), device=dev)
-    cbk = [K.key_codebook_layout(torch.randn((M, 256, 2), generator=g, device=dev), NBITS,
-                                 out=cb_all[l, 0]) for l in range(L)]
-    cv_raw = [torch.randn((M, 256, 2), generator=g, device=dev) for _ in range(L)]
-    cbv32 = [K.value_codebook_layout(cv_raw[l], NBITS, out=cb_all[l, 1]) for l in range(L)]
-    cbv16 = [K.value_codebook_layout(cv_raw[l], NBITS, half=True) for l in range(L)]
-    cbv = cbv16 if args.f16_value_codebook else cbv32
-    rk = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
-    rv = torch.randn((L, B, Hkv, R, D), generator=g, device=dev)
-    n_q = torch.full((B,), n, dtype=torch.int32, device=dev)
-    n_r = torch.full((B,), R, dtype=torch.int32, device=dev)
-    # one step's inputs (q, current k, current v of every layer) in one
-    # allocation, so the end-to-end step moves them with a single copy
-    nq_, nk_ = L * B * Hq * D, L * B * Hkv * D
-    io = torch.randn(nq_ + 2 * nk_, generator=g, device=dev)
-    q = io[:nq_].view(L, B, Hq, D)
-    kc = io[nq_:nq_ + nk_].view(L, B, Hkv, D)
-    vc = io[nq_ + nk_:].view(L, B, Hkv, D)
-    out = torch.empty((L, B, Hq, D), device=dev)
-    torch.cuda.synchronize()  # codebook layouts are written before any decode launch
-    # one fused launch per layer; PDL lets layer l+1 load its value codebook
-    # while layer l's last CTAs drain (codebooks are static: prepared above)
-    # codebooks (load time) and codes below n_q (appended by earlier steps) are
-    # not written by the kernel a launch overlaps: PDL may read them early
-    dec = PQDecoder(B, Hq, Hkv, cfg, device=dev, pdl=not args.no_pdl,
-                    static_codebooks=not args.no_pdl, early_codes=not args.no_pdl)
     stream = torch.cuda.Stream(device=dev)
-    if not args.no_l2_persist:
-        N.call("pqkv_l2_persist", N.ptr(cb_all), cb_all.numel() * 4, 1.0, N.stream_ptr(stream))
-
-    rec = torch.empty((L, B * Hq, D + 4), device=dev) if seq_split else None
-    gat = torch.empty((L, world, B * Hq, D + 4), device=dev) if seq_split else None
-
-    def capture(cbv_l):
-        """one decode step (one fused launch per layer) captured in a CUDA graph"""
-        def step():
-            for l in range(L):
-                if seq_split:
-                    # partial record of this rank's token range -> all-gather ->
-                    # merge in rank order (engine.sequence_parallel_decode)
-                    dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv_l[l],
-                        rk[l] if tail else None, rv[l] if tail else None,
-                        n_r if tail else None, kc[l] if tail else None,
-                        vc[l] if tail else None, merged=rec[l], finalize=False)
-                    dist.all_gather_into_tensor(gat[l], rec[l])
-                    K.merge_partials(gat[l], out=out[l])
-                else:
-                    dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv_l[l], rk[l], rv[l], n_r,
-                        kc[l], vc[l], out=out[l])
-        with torch.cuda.stream(stream):
-            step()
-            step()
-        torch.cuda.synchronize()
-        gr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gr, stream=stream):
-            step()
-        return gr
-
-    graph = capture(cbv)
-    launches_per_step = L
 
     def barrier():
         if world > 1:
@@ -482,21 +600,27 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    plan = shard_plan(args.config, rank, world)
+    w = Workload(args, plan, dev, stream, world > 1)
+    L, B, Hq, Hkv, n = w.L, w.B, w.Hq, w.Hkv, w.n
+    seq_split = w.seq_split
+    jobs = plan["jobs"]
+    replay = w.capture(args.f16_value_codebook)
+    launches_per_step = L
+
     # ---- device-resident timed region ------------------------------------
     for _ in range(args.warmup):
-        graph.replay()
+        replay()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for _ in range(args.steps):
-                graph.replay()
+                replay()
             ev1.record(stream)
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    # ranks serve independent sequences unless they split them (by tokens or heads)
-    jobs = 1 if (seq_split or head_shard) else world
     value = jobs * B * 1e3 / ms
     clocks = clk.summary()
 
@@ -504,36 +628,39 @@ def run_ours(args):
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(L)]
     ktimes = []
+    cbv = w.cbv16 if args.f16_value_codebook else w.cbv32
     with torch.cuda.stream(stream):
         for rep in range(max(2, min(args.steps, 5))):
             for l in range(L):
                 kev[l][0].record(stream)
-                K.decode_attention(dec.ws, Hkv, q[l].view(B * Hq, D), 1 / D ** 0.5, cbk[l],
-                                   codes_k[l], codes_v[l], n_q, cbv[l], rk[l], rv[l], n_r, kc[l],
-                                   vc[l], out=out[l], stream=stream)
+                K.decode_attention(w.dec.ws, Hkv, w.q[l].view(B * Hq, D), 1 / D ** 0.5,
+                                   w.cbk[l], w.codes_k[l], w.codes_v[l], w.n_q, cbv[l],
+                                   w.rk[l], w.rv[l], w.n_r, w.kc[l], w.vc[l], out=w.out[l],
+                                   stream=stream)
                 kev[l][1].record(stream)
             stream.synchronize()
             if rep > 0:
                 ktimes += [a.elapsed_time(b) for a, b in kev]
     iso_ms = statistics.mean(ktimes)
-    # the timed step is L back-to-back launches of this kernel and nothing
-    # else (PDL-overlapped), so its average in-step launch duration is ms / L
-    k_ms = ms / L
-    bytes_per_launch = 2 * B * Hkv * n * M
+    merge_ms = merge_share(w, args.steps, barrier, max_over_ranks) if seq_split else 0.0
+    # the timed step is L back-to-back launches of this kernel (plus, for a
+    # sequence split, the all-gather + merge, timed separately)
+    k_ms = (ms - merge_ms) / L
+    bytes_per_launch = w.bytes_per_launch
     hbm_peak, peak_kind = peaks()
     achieved = bytes_per_launch / (k_ms * 1e-3) / 1e9
-    share = 1.0
+    share = (ms - merge_ms) / ms
 
     # ---- end to end through the public API with host buffers --------------
-    io_h = torch.randn(io.numel()).pin_memory()  # q, k_cur, v_cur of every layer
+    io_h = torch.randn(w.io.numel()).pin_memory()  # q, k_cur, v_cur of every layer
     o_h = torch.empty((L, B, Hq, D)).pin_memory()
     h2d = io_h.numel() * 4
     d2h = o_h.numel() * 4
 
     def e2e_serial():
-        io.copy_(io_h, non_blocking=True)
-        graph.replay()
-        o_h.copy_(out, non_blocking=True)
+        w.io.copy_(io_h, non_blocking=True)
+        replay()
+        o_h.copy_(w.out, non_blocking=True)
 
     def capture_e2e(split=4, tail=4):
         """The same step with its host copies inside the graph, pipelined: the
@@ -542,17 +669,18 @@ def run_ours(args):
         all but the last `tail` layers read back on the copy stream while
         those run.  Every copy stays inside the timed step."""
         cs = torch.cuda.Stream(device=dev)
+        nq_, nk_ = w.nq_, w.nk_
         qh, kh = io_h[:nq_].view(L, B, Hq, D), io_h[nq_:nq_ + nk_].view(L, B, Hkv, D)
         vh = io_h[nq_ + nk_:].view(L, B, Hkv, D)
 
         def body():
-            for dst, src in ((q, qh), (kc, kh), (vc, vh)):
+            for dst, src in ((w.q, qh), (w.kc, kh), (w.vc, vh)):
                 dst[:split].copy_(src[:split], non_blocking=True)
             e_fork = torch.cuda.Event()
             e_fork.record(stream)
             cs.wait_event(e_fork)
             with torch.cuda.stream(cs):
-                for dst, src in ((q, qh), (kc, kh), (vc, vh)):
+                for dst, src in ((w.q, qh), (w.kc, kh), (w.vc, vh)):
                     dst[split:].copy_(src[split:], non_blocking=True)
                 e_in = torch.cuda.Event()
                 e_in.record(cs)
@@ -560,17 +688,16 @@ def run_ours(args):
             for l in range(L):
                 if l == split:
                     stream.wait_event(e_in)
-                dec(q[l], codes_k[l], codes_v[l], n_q, cbk[l], cbv[l], rk[l], rv[l], n_r,
-                    kc[l], vc[l], out=out[l])
+                w.layer(l, cbv)
                 if l == L - tail - 1:
                     e_mid = torch.cuda.Event()
                     e_mid.record(stream)
                     cs.wait_event(e_mid)
                     with torch.cuda.stream(cs):
-                        o_h[:L - tail].copy_(out[:L - tail], non_blocking=True)
+                        o_h[:L - tail].copy_(w.out[:L - tail], non_blocking=True)
                         e_back = torch.cuda.Event()
                         e_back.record(cs)
-            o_h[L - tail:].copy_(out[L - tail:], non_blocking=True)
+            o_h[L - tail:].copy_(w.out[L - tail:], non_blocking=True)
             stream.wait_event(e_back)
 
         with torch.cuda.stream(stream):
@@ -614,34 +741,32 @@ def run_ours(args):
     # ---- the fp16 value-codebook mode (stated tolerance), same step -------
     f16 = None
     if not args.f16_value_codebook and not args.no_f16_mode:
-        g16 = capture(cbv16)
-        for _ in range(args.warmup):
-            g16.replay()
-        barrier()
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
-            for _ in range(args.steps):
-                g16.replay()
-            ev1.record(stream)
-        barrier()
-        ms16 = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        r16 = w.capture(True)
+        ms16 = w.time(r16, args.steps, args.warmup, barrier, max_over_ranks)
         f16 = {"value": jobs * B * 1e3 / ms16, "unit": "tokens/s", "ms_per_step": ms16,
-               "roofline_frac": bytes_per_launch / (ms16 / L * 1e-3) / 1e9 / hbm_peak,
+               "roofline_frac": bytes_per_launch / ((ms16 - merge_ms) / L * 1e-3) / 1e9
+               / hbm_peak,
                "tolerance": "rtol 2e-3, atol 2e-4 vs the fp64 reference "
-                            "(tests/test_gpu_parity.py::test_f16_value_codebook_mode)"}
-        del g16
+                            "(tests/test_gpu_parity.py::test_f16_value_codebook_mode, "
+                            "tests/test_gpu_full_shapes.py)"}
+        del r16
 
-    enc = None if args.no_encode else encode_rate(dev, L, Hkv, n, stream)
+    enc = None if (args.no_encode or world > 1) else encode_rate(dev, L, Hkv, n, stream)
     if enc is not None:
-        enc["append_overlap"] = append_overlap(dev, graph, stream, L, B, Hkv, args.warmup)
+        enc["append_overlap"] = append_overlap(dev, replay, stream, L, B, Hkv, args.warmup)
+        ok, ns = encode_sample_check(dev, stream)
+        enc["bit_exact"] = ok
+        enc["bit_exact_check"] = f"{ns} vectors vs the C restatement of assign_codes"
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "strong" if (seq_split or head_shard) else "weak",
+            "scaling": "strong" if plan["mode"] != "batch" else "weak",
             "vs_baseline": None,
-            "dtype": "u8 codes / f32 accumulate" + (" (f16 value codebook)" if args.f16_value_codebook else ""), "data": "synthetic (seeded uniform codes, "
-            "N(0,1) codebooks, queries and recent rows)",
+            "dtype": "u8 codes / f32 accumulate" + (" (f16 value codebook)"
+                                                    if args.f16_value_codebook else ""),
+            "data": "synthetic (seeded uniform codes, N(0,1) codebooks, queries and recent "
+                    "rows)",
             "config": config_dict(args.config, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
@@ -656,13 +781,41 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "paper_2504_03661_b200.engine.PQDecoder (graph-replayed step)",
                     "copies": e2e_mode},
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step * args.steps * (2 if seq_split else 1),
             "clocks": clocks,
-            "code_stream_gbs_step": 2 * L * B * Hkv * n * M / (ms * 1e-3) / 1e9}
+            "code_stream_gbs_step": bytes_per_launch * L / (ms * 1e-3) / 1e9}
+    if seq_split:
+        line["sequence_split"] = {"merge_ms_per_step": merge_ms, "step_mode": w.graph_mode}
     if enc is not None:
         line["encode"] = enc
     if f16 is not None:
         line["f16_value_codebook_mode"] = f16
+    del replay, w
+    torch.cuda.empty_cache()
+
+    # ---- N > 1: the head-sharded and sequence-split configs beside it -------
+    if world > 1 and args.config == "llama2-32k" and not args.no_extra_configs:
+        for extra in ("llama3-gqa-32k", "llama3-gqa-128k"):
+            try:
+                pe = shard_plan(extra, rank, world)
+                we = Workload(args, pe, dev, stream, True)
+                re_ = we.capture(False)
+                mse = we.time(re_, args.steps, args.warmup, barrier, max_over_ranks)
+                ent = {"value": pe["jobs"] * we.B * 1e3 / mse, "unit": "tokens/s",
+                       "ms_per_step": mse, "config": config_dict(extra, world),
+                       "scaling": "strong", "step_mode": we.graph_mode}
+                if we.seq_split:
+                    ent["merge_ms_per_step"] = merge_share(we, args.steps, barrier,
+                                                           max_over_ranks)
+                ent["roofline_frac"] = (we.bytes_per_launch * we.L /
+                                        ((mse - ent.get("merge_ms_per_step", 0.0)) * 1e-3)
+                                        / 1e9 / hbm_peak)
+                del re_, we
+                torch.cuda.empty_cache()
+            except Exception as e:  # noqa: BLE001 -- the headline line still prints
+                ent = {"error": f"{type(e).__name__}: {e!s:.200}"}
+            line[extra.replace("-", "_")] = ent
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample = cpu_decode_rate(args.config, 1, args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": 1, "kind": "port",
@@ -671,6 +824,52 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dry_run(args):
+    """--dry-run: the launcher and shard plan without a GPU (gloo when no CUDA
+    device is visible) -- every rank's plan gathered to rank 0, one JSON line."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    plans = [shard_plan(c, rank, world) for c in CONFIGS]
+    if world > 1:
+        allp = [None] * world
+        dist.all_gather_object(allp, plans)
+    else:
+        allp = [plans]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "plans": allp,
+                          "configs": {c: config_dict(c, world) for c in CONFIGS}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this script
+    under torch.distributed.run with N ranks (one per GPU), same arguments."""
+    import socket
+    if not args.dry_run:
+        try:
+            import torch
+            have = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            have = 0
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but {have} GPU(s) visible", file=sys.stderr)
+            sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def main():
@@ -692,11 +891,22 @@ def main():
                     help="headline in the fp16 value-codebook mode (stated tolerance, DESIGN.md)")
     ap.add_argument("--no-f16-mode", action="store_true",
                     help="skip the secondary fp16 value-codebook measurement")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="N > 1: skip the head-sharded / sequence-split configs beside config 2")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher + shard plan only (no GPU work; gloo when no GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args)
+    if args.dry_run:
+        dry_run(args)
     else:
         run_ours(args)
 

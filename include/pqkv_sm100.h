@@ -197,12 +197,15 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              keep one query head per CTA (by default a CTA
                              serves two query heads of a KV head and shares
                              the value gathers) */
-#define PQKV_DECODE_EARLY_CODES 8 /* n_q and the codes below it were written
-                             before the previous kernel on the stream started
-                             (the codes of a decode step are appended by an
+#define PQKV_DECODE_EARLY_CODES 8 /* the codes below n_q were written before
+                             the previous kernel on the stream started (the
+                             codes of a decode step are appended by an
                              earlier step), so the work split and the first
                              code loads may precede that kernel's end (with
-                             PQKV_DECODE_PDL) */
+                             PQKV_DECODE_PDL).  n_q itself is re-read after
+                             the grid-dependency wait; if it changed, the
+                             split and the loads are redone (B <= 256; larger
+                             batches ignore this flag) */
 
 /* One fused launch per layer: decode_step (attention.py:214-287) for every
  * (b, hq) -- pqkv_decode_partials' quantized span, the dense partial of the
@@ -242,6 +245,24 @@ int pqkv_score_codes(const float *lut, const void *codes, int64_t n, int M,
                      int nbits, float *scores, void *stream);
 int pqkv_accumulate_mass(const void *codes, const float *p, int64_t n, int M,
                          int nbits, float *h, void *stream);
+
+/* The same seam in float64 with the reference's loop orders, bit-identical
+ * to _score_codes_jit / _accumulate_mass_jit (_kernels.py:27-43):
+ *   scores[t] = sum over i = 0..M-1 of lut[i][code[t,i]]  (lut [M][ksub] f64,
+ *               the reference Lut.table layout; summed in order from 0.0)
+ *   h[i][c]   = sum over t = 0..n-1 of p[t] where code[t,i] == c  (in t order)
+ * Used by the drop-in _kernels module (score_codes, accumulate_mass). */
+int pqkv_score_codes_f64(const double *lut, const void *codes, int64_t n, int M,
+                         int nbits, double *scores, void *stream);
+int pqkv_accumulate_mass_f64(const void *codes, const double *p, int64_t n, int M,
+                             int nbits, double *h, void *stream);
+
+/* Test-only: one kernel that releases a following PDL launch immediately
+ * (griddepcontrol.launch_dependents), waits ns nanoseconds, then writes v to
+ * p[0..n).  Used to check that PQKV_DECODE_EARLY_CODES re-validates the
+ * lengths it read before its grid-dependency wait. */
+int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns,
+                            void *stream);
 
 #ifdef __cplusplus
 }

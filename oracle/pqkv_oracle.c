@@ -188,6 +188,66 @@ int oracle_decode_heads_mt(const double *q, const float *k_n, const float *v_n,
     return j.rc;
 }
 
+/* The batched GQA layout of the GPU path: query head (b, h) reads KV head
+ * (b, h / (Hq / Hkv)); codes [B][Hkv][ld_codes][M], n_q[b] tokens; recent rows
+ * [B][Hkv][ld_recent][d] with n_recent[b] live; k_n / v_n [B][Hkv][d];
+ * q [B][Hq][d] fp64 -> out [B][Hq][d].  Per query head this is the
+ * reference's snapshot -> build_key_lut -> quantized / dense partials ->
+ * merge -> finalize (no append per query head). */
+typedef struct {
+    const double *q; const float *k_n, *v_n; const void *codes_k, *codes_v;
+    int B, Hq, Hkv; const int32_t *n_q; int64_t ld_codes;
+    const float *recent_k, *recent_v; const int32_t *n_recent; int64_t ld_recent;
+    const float *cents_k, *cents_v; int M, nbits, dsub; double scale; int64_t block_size;
+    double *out; int next; int rc; pthread_mutex_t mu;
+} gqa_job_t;
+
+static void *gqa_worker(void *arg) {
+    gqa_job_t *j = (gqa_job_t *)arg;
+    const int d = j->M * j->dsub, G = j->Hq / j->Hkv;
+    const size_t cell = j->nbits <= 8 ? 1 : 2;
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        int hh = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (hh >= j->B * j->Hq) break;
+        const int b = hh / j->Hq, h = hh % j->Hq;
+        const size_t kv = (size_t)b * j->Hkv + h / G;
+        int rc = oracle_decode_head(
+            j->q + (size_t)hh * d, j->k_n + kv * d, j->v_n + kv * d,
+            (const char *)j->codes_k + kv * j->ld_codes * j->M * cell,
+            (const char *)j->codes_v + kv * j->ld_codes * j->M * cell, j->n_q[b],
+            j->recent_k + kv * j->ld_recent * d, j->recent_v + kv * j->ld_recent * d,
+            j->n_recent[b], j->cents_k, j->cents_v, j->M, j->nbits, j->dsub, j->scale,
+            j->block_size, j->out + (size_t)hh * d);
+        if (rc) {
+            pthread_mutex_lock(&j->mu);
+            j->rc = rc;
+            pthread_mutex_unlock(&j->mu);
+        }
+    }
+    return NULL;
+}
+
+int oracle_decode_gqa_mt(const double *q, const float *k_n, const float *v_n,
+                         const void *codes_k, const void *codes_v, int B, int Hq, int Hkv,
+                         const int32_t *n_q, int64_t ld_codes, const float *recent_k,
+                         const float *recent_v, const int32_t *n_recent, int64_t ld_recent,
+                         const float *cents_k, const float *cents_v, int M, int nbits, int dsub,
+                         double scale, int64_t block_size, double *out, int threads) {
+    if (Hkv <= 0 || Hq % Hkv) return 1;
+    gqa_job_t j = {q, k_n, v_n, codes_k, codes_v, B, Hq, Hkv, n_q, ld_codes, recent_k,
+                   recent_v, n_recent, ld_recent, cents_k, cents_v, M, nbits, dsub, scale,
+                   block_size, out, 0, 0, PTHREAD_MUTEX_INITIALIZER};
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    for (int t = 1; t < threads; ++t) pthread_create(&tid[t], NULL, gqa_worker, &j);
+    gqa_worker(&j);
+    for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+    return j.rc;
+}
+
 /* numpy's pairwise float64 row sum (np.sum(..., axis=1), the order used by
  * pq_core.py:163,165): < 8 terms sequential from 0.0; <= 128 terms with 8
  * strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a

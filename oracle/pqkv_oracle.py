@@ -412,6 +412,10 @@ def c_library():
                                                ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                                ctypes.c_int64, P, ctypes.c_int, ctypes.c_int]
         lib.oracle_decode_heads_mt.restype = ctypes.c_int
+        I, I64 = ctypes.c_int, ctypes.c_int64
+        lib.oracle_decode_gqa_mt.argtypes = [P, P, P, P, P, I, I, I, P, I64, P, P, P, I64, P, P,
+                                             I, I, I, ctypes.c_double, I64, P, I]
+        lib.oracle_decode_gqa_mt.restype = ctypes.c_int
         lib.oracle_assign_codes.argtypes = [P, ctypes.c_int64, P, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, P, ctypes.c_int]
         lib.oracle_assign_codes.restype = ctypes.c_int
@@ -460,4 +464,43 @@ def c_decode_head(q, k_n, v_n, codes_k, codes_v, recent_k, recent_v, cents_k, ce
                                 dsub, float(scale), int(block_size), _p(out))
     if rc:
         raise RuntimeError("oracle_decode_head failed")
+    return out
+
+
+def c_decode_batched(q, k_n, v_n, codes_k, codes_v, n_q, recent_k, recent_v, n_recent,
+                     cents_k, cents_v, nbits, scale=None, block_size=8192, threads=None):
+    """C restatement of the per-query-head decode over a batched GQA cache:
+    q (B, Hq, d); codes (B, Hkv, cap, M) in the reference row layout; n_q (B,);
+    recent (B, Hkv, R, d) with n_recent (B,) live rows; k_n / v_n (B, Hkv, d).
+    Returns (B, Hq, d) float64.  All host cores by default."""
+    lib = c_library()
+    if lib is None:
+        raise RuntimeError("oracle C library not built (make -C oracle)")
+    M, ksub, dsub = cents_k.shape
+    d = M * dsub
+    B, Hq, _ = q.shape
+    Hkv = codes_k.shape[1]
+    if scale is None:
+        scale = default_scale(d)
+    if threads is None:
+        threads = len(os.sched_getaffinity(0))
+    cdt = np.uint8 if nbits <= 8 else np.uint16
+    qd = np.ascontiguousarray(q, np.float64)
+    kn = np.ascontiguousarray(k_n, np.float32)
+    vn = np.ascontiguousarray(v_n, np.float32)
+    ck = np.ascontiguousarray(codes_k, cdt)
+    cv = np.ascontiguousarray(codes_v, cdt)
+    rk = np.ascontiguousarray(recent_k, np.float32)
+    rv = np.ascontiguousarray(recent_v, np.float32)
+    nq = np.ascontiguousarray(n_q, np.int32)
+    nr = np.ascontiguousarray(n_recent, np.int32)
+    CK = np.ascontiguousarray(cents_k, np.float32)
+    CV = np.ascontiguousarray(cents_v, np.float32)
+    out = np.empty((B, Hq, d))
+    rc = lib.oracle_decode_gqa_mt(_p(qd), _p(kn), _p(vn), _p(ck), _p(cv), B, Hq, Hkv, _p(nq),
+                                  ck.shape[2], _p(rk), _p(rv), _p(nr), rk.shape[2], _p(CK),
+                                  _p(CV), M, nbits, dsub, float(scale), int(block_size),
+                                  _p(out), int(threads))
+    if rc:
+        raise RuntimeError(f"oracle_decode_gqa_mt failed ({rc})")
     return out

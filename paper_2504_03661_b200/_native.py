@@ -53,6 +53,9 @@ SIGNATURES = {
                                    _P, _P, _I64, _P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _P]),
     "pqkv_score_codes": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_accumulate_mass": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "pqkv_score_codes_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "pqkv_accumulate_mass_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "pqkv_debug_delayed_fill": (_I, [_P, _I, _I, ctypes.c_longlong, _P]),
 }
 
 _lib = None
@@ -108,8 +111,10 @@ def ptr(t) -> int | None:
     return t.data_ptr()
 
 
-def stream_ptr(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def stream_ptr(stream=None, device=None) -> int:
+    """The given stream, else the current stream of `device` (default: the
+    current device)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
 
 

@@ -106,16 +106,22 @@ def _device_table(lut: Lut) -> torch.Tensor:
     return lut.device_table
 
 
+def _check_codes_for_table(tab: torch.Tensor, codes_K: CodesMatrix) -> None:
+    """The reference's range check (attention.py:88-91): only when the cell
+    can hold a value >= ksub."""
+    ksub = tab.shape[0]
+    if codes_K.n_tokens and ksub <= (255 if codes_K.cell_width == 1 else 65535):
+        from .pq_core import _max_code
+        if _max_code(codes_K.codes) >= ksub:
+            raise ValueError("code value out of range for lookup table")
+
+
 def score_tokens(lut: Lut, codes_K: CodesMatrix, counters: Counters | None = None):
     """scores[t] = sum_i lut[i][codes[t][i]] (keys stay quantized)."""
     tab = _device_table(lut)
-    ksub, M = tab.shape
     c = codes_K.codes
     n = codes_K.n_tokens
-    if n and ksub <= (255 if codes_K.cell_width == 1 else 65535):
-        from .pq_core import _max_code
-        if _max_code(c) >= ksub:
-            raise ValueError("code value out of range for lookup table")
+    _check_codes_for_table(tab, codes_K)
     if counters is not None:
         counters.lut_lookups += n * codes_K.M
         counters.adds += n * codes_K.M
@@ -201,10 +207,13 @@ def quantized_partial(lut: Lut, codes_K: CodesMatrix, codes_V: CodesMatrix, cb_V
     tab = _device_table(lut)
     dev = tab.device
     t0 = time.perf_counter()
-    score_tokens(lut, codes_K, counters)  # range check + counters, as the reference
-    if counters is not None:
+    _check_codes_for_table(tab, codes_K)  # score_tokens' range check (:88-91) ...
+    if counters is not None:  # ... and its work accounting (:93-96), then :153-154
+        counters.lut_lookups += n * codes_K.M
+        counters.adds += n * codes_K.M
+        counters.code_bytes_read += n * codes_K.M * codes_K.cell_width
         counters.code_bytes_read += n * cfg.M * codes_V.cell_width
-    ws = K.DecodeWorkspace(1, 1, cfg.d, cfg.M, cfg.nbits, device=dev)
+    ws = _step_workspace(cfg, dev)
     ck = _decode_codes(codes_K.device_codes(dev), cfg).view(1, 1, n, cfg.M)
     cv = _decode_codes(codes_V.device_codes(dev), cfg).view(1, 1, n, cfg.M)
     nq = _n_tensor(n, dev)

@@ -66,7 +66,10 @@ def integer_quantize(X, nbits: int, mode: str = "asymmetric", device=None):
                     IntQuantParams(nbits=nbits, s=1.0, z=z, mode=mode))
         s = (x_max - x_min) / (q_max - q_min)
         z = int(np.round(q_min - x_min / s))
-    Q = torch.clamp(torch.round(t / s + z), q_min, q_max).to(torch.int32)
+    # true division by a device tensor: a Python-float divisor would become a
+    # multiply by its rounded reciprocal (1 ulp off at .5 boundaries)
+    s_t = torch.tensor(s, dtype=torch.float64, device=t.device)
+    Q = torch.clamp(torch.round(t / s_t + z), q_min, q_max).to(torch.int32)
     return out(Q), IntQuantParams(nbits=nbits, s=s, z=z, mode=mode)
 
 

@@ -54,24 +54,32 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB,
     `defines` (e.g. ("PQKV_TRACE",)) builds a diagnostic variant into `lib`."""
     if not force and not _stale(lib):
         return lib
-    os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
+    out_dir = os.path.dirname(os.path.abspath(lib))
+    os.makedirs(out_dir, exist_ok=True)
     tag = "_".join(defines)
-    for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", f"{tag}.o"))
-        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", INCLUDE, "-c",
-               os.path.join(CSRC, src), "-o", obj]
-        if verbose:
-            cmd += ["-Xptxas", "-v"]
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
-    tmp = lib + ".tmp"
-    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                    "-o", tmp, *objs], check=True)
-    os.replace(tmp, lib)
-    for o in objs:
-        os.remove(o)
+    objs, procs = [], []
+    try:
+        # the translation units compile in parallel (decode.cu dominates)
+        for src in SOURCES:
+            obj = os.path.join(out_dir, src.replace(".cu", f"{tag}.o"))
+            cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", INCLUDE, "-c",
+                   os.path.join(CSRC, src), "-o", obj]
+            if verbose:
+                cmd += ["-Xptxas", "-v"]
+                print(" ".join(cmd), flush=True)
+            objs.append(obj)
+            procs.append((src, subprocess.Popen(cmd)))
+        failed = [src for src, p in procs if p.wait() != 0]
+        if failed:
+            raise RuntimeError(f"nvcc failed on {', '.join(failed)}")
+        tmp = lib + ".tmp"
+        subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                        "-o", tmp, *objs], check=True)
+        os.replace(tmp, lib)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return lib
 
 

@@ -102,8 +102,8 @@ constexpr int OFF_RED = LUT_BYTES + CV_BYTES;                 // red_m[2][W], re
 constexpr int OFF_COL = OFF_RED + 4 * WMAX * 4;               // colsum[2 * NG][128]
 constexpr int OFF_DNS = OFF_COL + 2 * (WMAX / 4) * D * 4;     // dense m[W], l[W], acc[W][128]
 constexpr int OFF_BAR = OFF_DNS + (2 * WMAX + WMAX * D) * 4;  // 2 mbarriers
-constexpr int OFF_FLAG = OFF_BAR + 16;                          // finisher flags [W / 4]
-constexpr int OFF_NQ = OFF_FLAG + 4 * (WMAX / 4);               // n_q copy [kNqCache]
+constexpr int OFF_FLAG = OFF_BAR + 16;  // finisher flags [W / 4], then the stale-n_q flag
+constexpr int OFF_NQ = OFF_FLAG + 4 * (WMAX / 4 + 4);           // n_q copy [kNqCache]
 constexpr int kNqCache = 256;  // batches whose lengths are kept in shared memory
 constexpr int SMEM_BYTES = OFF_NQ + 4 * kNqCache;
 
@@ -659,6 +659,8 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // the lengths are read from global memory once, here; the segment walks
     // below (after a barrier) use the shared-memory copy
     const bool nq_cached = A.B <= kNqCache;
+    // early_codes needs the shared-memory copy of n_q to re-validate it
+    const bool early = A.early_codes && nq_cached;
     auto first_ring = [&]() {
         cm = cost_map(A.n_q, A.B, Hqp, A.num_ctas / P);
         pos = cta_begin(cm, pc);
@@ -679,13 +681,24 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                           s0.hi);
         }
     };
-    if (A.early_codes) first_ring();
+    int *stale_s = flag_s + (WMAX / 4);  // 1: the pre-wait n_q was stale
+    if (early) {
+        if (tid == 0) *stale_s = 0;
+        first_ring();
+    }
     pdl_launch_dependents();
     pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
 #ifdef PQKV_TRACE
     PQKV_TR(7, gtime());
 #endif
-    if (!A.early_codes) first_ring();
+    // early: the lengths read before the wait may predate the previous kernel
+    // (e.g. a publication's n_q.fill_ right before this launch).  Re-read them
+    // now -- the load overlaps the first table build -- and, if any changed,
+    // redo the work split and the first ring from the fresh values (below).
+    int nq_fresh = 0;
+    if (early && tid < A.B)
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(nq_fresh) : "l"(A.n_q + tid));
+    if (!early) first_ring();
 #ifdef PQKV_TRACE
     PQKV_TR(10, gtime());  // cost map read, first ring issued
 #endif
@@ -724,6 +737,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
     if (nq_cached) __syncthreads();  // nq_s is written
     Segment sg;
+    bool validate = early;  // first segment of an early launch: check n_q
     while (next_segment(nq, A.B, Hqp, &pos, end, &sg)) {
         const int vh = vhead(sg.bh);  // virtual head: query heads hq0 .. hq0 + HG - 1
         const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
@@ -766,6 +780,22 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 bulk_g2s(sbase + c * 16384,
                          reinterpret_cast<const char *>(A.lut + (int64_t)bh0 * KSUB * M) + c * 16384,
                          16384, bar_lut);
+        }
+        if (validate) {
+            validate = false;
+            if (tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+            __syncthreads();
+            if (*stale_s) {  // rare: restart the CTA's work from the fresh lengths
+                __syncthreads();  // every thread has read the flag
+                if (tid < A.B) nq_s[tid] = nq_fresh;
+                if (tid == 0) *stale_s = 0;
+                __syncthreads();
+                cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P);
+                pos = cta_begin(cm, pc);
+                end = min(cta_begin(cm, pc + 1), cm.total);
+                ring_loaded = false;
+                continue;
+            }
         }
         // dense partial by the CTA holding the head's last tokens (for most CTAs
         // their first segment, so it overlaps the prologue)
@@ -968,9 +998,6 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
             }
         }
     }
-#ifdef PQKV_TRACE
-    PQKV_TR(6, gtime());
-#endif
 #ifdef PQKV_TRACE
     PQKV_TR(6, gtime());
 #endif

@@ -123,10 +123,72 @@ __global__ void accumulate_mass_kernel(const CT *__restrict__ codes, const float
     atomicAdd(h + (int64_t)i * ksub + codes[idx], p[t]);
 }
 
+// The reference's lower seam in float64, with its loop orders
+// (_kernels.py:27-43): score s_t = sum_i lut[i][code[t,i]] summed over i in
+// order from 0.0; mass h[i][c] = sum of p_t over t in token order.  One thread
+// per token (score) / per bin (mass: the block stages a tile of column i's
+// codes and weights, every bin thread scans it in order), so both are
+// bit-identical to the numba loops given the same inputs.
+template <typename CT>
+__global__ void score_codes_f64_kernel(const double *__restrict__ lut, int ksub,
+                                       const CT *__restrict__ codes, int64_t n, int M,
+                                       double *__restrict__ scores) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double s = 0.0;
+    for (int i = 0; i < M; ++i) s += lut[(int64_t)i * ksub + codes[t * M + i]];
+    scores[t] = s;
+}
+
+constexpr int kMassTile = 1024;
+template <typename CT>
+__global__ void accumulate_mass_f64_kernel(const CT *__restrict__ codes,
+                                           const double *__restrict__ p, int64_t n, int M,
+                                           int ksub, double *__restrict__ h) {
+    __shared__ int cs[kMassTile];
+    __shared__ double ps[kMassTile];
+    const int i = blockIdx.y;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    double acc = 0.0;
+    for (int64_t t0 = 0; t0 < n; t0 += kMassTile) {
+        const int cnt = (int)min((int64_t)kMassTile, n - t0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+            cs[k] = codes[(t0 + k) * M + i];
+            ps[k] = p[t0 + k];
+        }
+        __syncthreads();
+        if (c < ksub)
+            for (int k = 0; k < cnt; ++k)
+                if (cs[k] == c) acc += ps[k];
+    }
+    if (c < ksub) h[(int64_t)i * ksub + c] = acc;
+}
+
+// Test-only: lets the next PDL launch start at once, waits ns, then writes v
+// to p[0..n) -- a length update the dependent kernel can only see after its
+// griddepcontrol.wait (exercises the early_codes re-validation).
+__global__ void delayed_fill_kernel(int32_t *p, int n, int32_t v, long long ns) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    } while ((long long)(t - t0) < ns);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+
 }  // namespace
 }  // namespace pqkv
 
 using namespace pqkv;
+
+extern "C" int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns, void *stream) {
+    PQKV_CHECK_ARG(p && n >= 0 && ns >= 0 && ns < 10000000000LL,
+                   "pqkv_debug_delayed_fill: bad arguments");
+    delayed_fill_kernel<<<1, 128, 0, as_stream(stream)>>>(p, n, v, ns);
+    return launch_status("pqkv_debug_delayed_fill");
+}
 
 extern "C" int pqkv_version(void) { return 1; }
 
@@ -260,4 +322,36 @@ extern "C" int pqkv_accumulate_mass(const void *codes, const float *p, int64_t n
         accumulate_mass_kernel<uint16_t><<<blocks, 256, 0, st>>>((const uint16_t *)codes, p, n, M,
                                                                   ksub, h);
     return launch_status("pqkv_accumulate_mass");
+}
+
+extern "C" int pqkv_score_codes_f64(const double *lut, const void *codes, int64_t n, int M,
+                                    int nbits, double *scores, void *stream) {
+    PQKV_CHECK_ARG(M > 0 && nbits >= 1 && nbits <= 16 && n >= 0,
+                   "pqkv_score_codes_f64: bad args");
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(lut && codes && scores, "pqkv_score_codes_f64: null pointer");
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (nbits <= 8)
+        score_codes_f64_kernel<uint8_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            lut, 1 << nbits, (const uint8_t *)codes, n, M, scores);
+    else
+        score_codes_f64_kernel<uint16_t><<<blocks, 256, 0, as_stream(stream)>>>(
+            lut, 1 << nbits, (const uint16_t *)codes, n, M, scores);
+    return launch_status("pqkv_score_codes_f64");
+}
+
+extern "C" int pqkv_accumulate_mass_f64(const void *codes, const double *p, int64_t n, int M,
+                                        int nbits, double *h, void *stream) {
+    PQKV_CHECK_ARG(M > 0 && M <= 65535 && nbits >= 1 && nbits <= 16 && n >= 0,
+                   "pqkv_accumulate_mass_f64: bad args");
+    PQKV_CHECK_ARG(h && (n == 0 || (codes && p)), "pqkv_accumulate_mass_f64: null pointer");
+    const int ksub = 1 << nbits;
+    dim3 grid((unsigned)((ksub + 255) / 256), (unsigned)M);
+    if (nbits <= 8)
+        accumulate_mass_f64_kernel<uint8_t><<<grid, 256, 0, as_stream(stream)>>>(
+            (const uint8_t *)codes, p, n, M, ksub, h);
+    else
+        accumulate_mass_f64_kernel<uint16_t><<<grid, 256, 0, as_stream(stream)>>>(
+            (const uint16_t *)codes, p, n, M, ksub, h);
+    return launch_status("pqkv_accumulate_mass_f64");
 }

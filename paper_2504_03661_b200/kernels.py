@@ -16,6 +16,21 @@ import torch
 from . import _native as N
 
 
+def _call(dev, name, *args):
+    """One C-ABI call with `dev` as the current device, so the library's
+    launches (and its per-device SM count / attributes) target the tensors'
+    GPU even when it is not the caller's current device."""
+    with torch.cuda.device(dev):
+        return N.call(name, *args)
+
+
+def _first_dev(*ts):
+    for t in ts:
+        if t is not None:
+            return t.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
 def _dev_check(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -52,8 +67,8 @@ def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tens
         raise ValueError("codes output must be (n, M) with unit column stride")
     cents = _contig(centroids.float())
     rot = _rot_base(layout, t_first)
-    N.call("pqkv_encode", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0), N.ptr(cents), M,
-           nbits, N.ptr(out), out.stride(0), rot, N.stream_ptr(stream))
+    _call(x.device, "pqkv_encode", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0), N.ptr(cents), M,
+           nbits, N.ptr(out), out.stride(0), rot, N.stream_ptr(stream, x.device))
     return out
 
 
@@ -75,9 +90,9 @@ def encode_batched(x: torch.Tensor, centroids: torch.Tensor, nbits: int,
         out = torch.empty((Z, n, M), dtype=code_dtype(nbits), device=x.device)
     if tuple(out.shape) != (Z, n, M) or not out.is_contiguous():
         raise ValueError("codes output must be a contiguous (Z, n, M) tensor")
-    N.call("pqkv_encode_batched", N.ptr(x), N.DTYPE_CODE[torch.float32], Z, n, d, d, n * d,
+    _call(x.device, "pqkv_encode_batched", N.ptr(x), N.DTYPE_CODE[torch.float32], Z, n, d, d, n * d,
            N.ptr(cents), M * ksub * dsub, M, nbits, N.ptr(out), M, n * M,
-           _rot_base(layout, t_first), N.stream_ptr(stream))
+           _rot_base(layout, t_first), N.stream_ptr(stream, x.device))
     return out
 
 
@@ -103,9 +118,12 @@ def relayout(codes: torch.Tensor, to_decode: bool, t_first: int = 0, out=None, s
     n = src.shape[-2]
     s2 = src.view(lead, n, 64) if lead else src
     o2 = out.view(lead, n, 64) if lead else out
+    if lead > 1 and n % 8 == 0:
+        # the layout depends on the token index mod 8 only: all heads at once
+        s2, o2, n, lead = s2.view(1, lead * n, 64), o2.view(1, lead * n, 64), lead * n, 1
     for h in range(lead):
-        N.call("pqkv_relayout_codes", N.ptr(s2[h]), 64, N.ptr(o2[h]), 64, n, t_first,
-               1 if to_decode else 0, 128, 64, 8, N.stream_ptr(stream))
+        _call(src.device, "pqkv_relayout_codes", N.ptr(s2[h]), 64, N.ptr(o2[h]), 64, n, t_first,
+               1 if to_decode else 0, 128, 64, 8, N.stream_ptr(stream, src.device))
     return out
 
 
@@ -116,8 +134,8 @@ def reconstruct(codes: torch.Tensor, centroids: torch.Tensor, nbits: int, stream
     out = torch.empty((n, M * dsub), dtype=torch.float32, device=codes.device)
     if codes.stride(1) != 1:
         codes = codes.contiguous()
-    N.call("pqkv_reconstruct", N.ptr(codes), n, codes.stride(0), N.ptr(_contig(centroids)),
-           M * dsub, M, nbits, N.ptr(out), N.stream_ptr(stream))
+    _call(codes.device, "pqkv_reconstruct", N.ptr(codes), n, codes.stride(0), N.ptr(_contig(centroids)),
+           M * dsub, M, nbits, N.ptr(out), N.stream_ptr(stream, codes.device))
     return out
 
 
@@ -130,8 +148,8 @@ def build_lut(q: torch.Tensor, cb_k: torch.Tensor, nbits: int, scale: float,
     H = q.shape[0]
     if out is None:
         out = torch.empty((H, ksub, M), dtype=torch.float32, device=q.device)
-    N.call("pqkv_build_lut", N.ptr(q), H, M * dsub, N.ptr(_contig(cb_k)), M, nbits, float(scale),
-           N.ptr(out), N.stream_ptr(stream))
+    _call(q.device, "pqkv_build_lut", N.ptr(q), H, M * dsub, N.ptr(_contig(cb_k)), M, nbits, float(scale),
+           N.ptr(out), N.stream_ptr(stream, q.device))
     return out
 
 
@@ -156,8 +174,8 @@ def key_codebook_layout(cb_k: torch.Tensor, nbits: int, stream=None, out=None) -
     if not is_fast_geometry(M * dsub, M, nbits):
         return cb_k
     out = _layout_out(out, M * ksub * dsub, torch.float32, cb_k.device)
-    N.call("pqkv_prepare_key_codebook", N.ptr(cb_k), M * dsub, M, nbits, N.ptr(out),
-           N.stream_ptr(stream))
+    _call(cb_k.device, "pqkv_prepare_key_codebook", N.ptr(cb_k), M * dsub, M, nbits, N.ptr(out),
+           N.stream_ptr(stream, cb_k.device))
     return out
 
 
@@ -172,14 +190,14 @@ def value_codebook_layout(cb_v: torch.Tensor, nbits: int, stream=None,
         if not is_fast_geometry(M * dsub, M, nbits):
             raise ValueError("the fp16 value-codebook mode exists only for m64b8")
         out = _layout_out(out, M * ksub * dsub, torch.float16, cb_v.device)
-        N.call("pqkv_prepare_value_codebook_f16", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
-               N.stream_ptr(stream))
+        _call(cb_v.device, "pqkv_prepare_value_codebook_f16", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
+               N.stream_ptr(stream, cb_v.device))
         return out
     if not is_fast_geometry(M * dsub, M, nbits):
         return cb_v
     out = _layout_out(out, M * ksub * dsub, torch.float32, cb_v.device)
-    N.call("pqkv_prepare_value_codebook", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
-           N.stream_ptr(stream))
+    _call(cb_v.device, "pqkv_prepare_value_codebook", N.ptr(cb_v), M * dsub, M, nbits, N.ptr(out),
+           N.stream_ptr(stream, cb_v.device))
     return out
 
 
@@ -219,10 +237,10 @@ def decode_partials(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout,
     quantized span of every (b, hq).  q: (B*Hq, d) float32; codes (B, Hkv, cap,
     M); n_q (B,) int32 device; codebooks from key/value_codebook_layout."""
     _check_codes(ws, Hkv, codes_k, codes_v)
-    N.call("pqkv_decode_partials", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
+    _call(codes_k.device, "pqkv_decode_partials", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
            ws.B, ws.Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q),
            N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, ws.num_ctas, N.ptr(ws.partials),
-           N.stream_ptr(stream))
+           N.stream_ptr(stream, codes_k.device))
 
 
 def decode_partials_lut(ws: DecodeWorkspace, Hkv: int, lut, codes_k, codes_v, n_q, cb_v_layout,
@@ -232,9 +250,9 @@ def decode_partials_lut(ws: DecodeWorkspace, Hkv: int, lut, codes_k, codes_v, n_
     lut = _contig(lut)
     if tuple(lut.shape) != (ws.B * ws.Hq, ws.ksub, ws.M):
         raise ValueError("lut must be (B*Hq, ksub, M)")
-    N.call("pqkv_decode_partials_lut", N.ptr(lut), ws.B, ws.Hq, Hkv, N.ptr(codes_k),
+    _call(codes_k.device, "pqkv_decode_partials_lut", N.ptr(lut), ws.B, ws.Hq, Hkv, N.ptr(codes_k),
            N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q), N.ptr(cb_v_layout), ws.d, ws.M,
-           ws.nbits, ws.num_ctas, N.ptr(ws.partials), N.stream_ptr(stream))
+           ws.nbits, ws.num_ctas, N.ptr(ws.partials), N.stream_ptr(stream, codes_k.device))
 
 
 def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, recent_k=None,
@@ -253,11 +271,11 @@ def decode_finish(ws: DecodeWorkspace | None, Hkv: int, n_q, q, scale: float, re
         if recent_k.shape != recent_v.shape or recent_k.dim() != 4:
             raise ValueError("recent_k/recent_v must both be (B, Hkv, R, d)")
         ld_recent = recent_k.shape[2]
-    N.call("pqkv_decode_finish", N.ptr(ws.partials) if ws is not None else None,
+    _call((ws.device if ws is not None else _first_dev(out, merged, lse, q)), "pqkv_decode_finish", N.ptr(ws.partials) if ws is not None else None,
            ws.num_ctas if ws is not None else 0, B, Hq, Hkv, d, N.ptr(n_q), N.ptr(q),
            float(scale), N.ptr(recent_k), N.ptr(recent_v), ld_recent, N.ptr(n_recent),
            N.ptr(k_cur), N.ptr(v_cur), N.ptr(out), N.ptr(lse), N.ptr(merged),
-           N.stream_ptr(stream))
+           N.stream_ptr(stream, (ws.device if ws is not None else _first_dev(out, merged, lse, q))))
 
 
 def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout, codes_k,
@@ -289,35 +307,35 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
         flags |= N.DECODE_ONE_HEAD_PER_CTA
     if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
         flags |= N.DECODE_F16_VALUE_CODEBOOK
-    N.call("pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
+    _call(codes_k.device, "pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),
            ws.B, ws.Hq, Hkv, N.ptr(codes_k), N.ptr(codes_v), codes_k.shape[2], N.ptr(n_q),
            N.ptr(cb_v_layout), ws.d, ws.M, ws.nbits, N.ptr(recent_k), N.ptr(recent_v), ld_recent,
            N.ptr(n_recent), N.ptr(k_cur), N.ptr(v_cur), ws.num_ctas, N.ptr(ws.partials),
            N.ptr(ws.counters), N.ptr(out), N.ptr(lse), N.ptr(merged), flags,
-           N.stream_ptr(stream))
+           N.stream_ptr(stream, codes_k.device))
 
 
 def merge_partials(parts: torch.Tensor, out=None, lse=None, merged=None, stream=None) -> None:
     """parts (n_parts, n_heads, d+4) -> merged in index order / finalized."""
     n_parts, n_heads, w = parts.shape
-    N.call("pqkv_merge_partials", N.ptr(_contig(parts)), n_parts, n_heads, w - N.PARTIAL_HEADER,
-           N.ptr(out), N.ptr(lse), N.ptr(merged), N.stream_ptr(stream))
+    _call(parts.device, "pqkv_merge_partials", N.ptr(_contig(parts)), n_parts, n_heads, w - N.PARTIAL_HEADER,
+           N.ptr(out), N.ptr(lse), N.ptr(merged), N.stream_ptr(stream, parts.device))
 
 
 def score_codes(lut_cm: torch.Tensor, codes: torch.Tensor, nbits: int, stream=None):
     """scores[t] = sum_i lut[code[t,i], i] (lut centroid-major (ksub, M))."""
     n, M = codes.shape
     out = torch.empty(n, dtype=torch.float32, device=codes.device)
-    N.call("pqkv_score_codes", N.ptr(_contig(lut_cm)), N.ptr(_contig(codes)), n, M, nbits,
-           N.ptr(out), N.stream_ptr(stream))
+    _call(codes.device, "pqkv_score_codes", N.ptr(_contig(lut_cm)), N.ptr(_contig(codes)), n, M, nbits,
+           N.ptr(out), N.stream_ptr(stream, codes.device))
     return out
 
 
 def accumulate_mass(codes: torch.Tensor, p: torch.Tensor, nbits: int, stream=None):
     n, M = codes.shape
     h = torch.empty((M, 1 << nbits), dtype=torch.float32, device=codes.device)
-    N.call("pqkv_accumulate_mass", N.ptr(_contig(codes)), N.ptr(_contig(p.float())), n, M, nbits,
-           N.ptr(h), N.stream_ptr(stream))
+    _call(codes.device, "pqkv_accumulate_mass", N.ptr(_contig(codes)), N.ptr(_contig(p.float())), n, M, nbits,
+           N.ptr(h), N.stream_ptr(stream, codes.device))
     return h
 
 

@@ -34,6 +34,12 @@ from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_devic
 __all__ = ["LayerKVCache", "CacheSnapshot"]
 
 
+def _host_codes(c: torch.Tensor) -> np.ndarray:
+    if c.dtype == torch.uint16:  # no numpy view of torch.uint16 on every build
+        return c.to(torch.int32).cpu().numpy().astype(np.uint16)
+    return c.cpu().numpy()
+
+
 @dataclass(frozen=True)
 class CacheSnapshot:
     """Immutable view: published codes + recent rows, tokens [0, n_total) once."""
@@ -84,6 +90,9 @@ class LayerKVCache:
         self._pending_rows = 0
         self._lock = threading.RLock()
         self.inline_flush_seconds = 0.0
+        # numpy in -> numpy snapshots, like the reference (kv_cache.py:269-290);
+        # decided by the first write (None until then)
+        self._numpy_io: bool | None = None
         self._side = (torch.cuda.Stream(device=self.device, priority=0)
                       if worker == "thread" else None)
         if self._side is not None:
@@ -137,7 +146,8 @@ class LayerKVCache:
         self._rk, self._rv, self._r0 = nk, nv, 0
 
     def _rows(self, x, name: str) -> torch.Tensor:
-        d = self.config.d
+        if self._numpy_io is None:
+            self._numpy_io = not _is_tensor(x)
         t = to_device(x if _is_tensor(x) else np.asarray(x, dtype=np.float32), torch.float32,
                       self.device)
         return t
@@ -351,6 +361,9 @@ class LayerKVCache:
         ck, cv, rk, rv, n_q, n_total = self.raw_snapshot()
         if self._layout == "decode" and n_q:
             ck, cv = K.relayout(ck, False), K.relayout(cv, False)
+        if self._numpy_io:  # fed numpy: host copies, as the reference returns
+            ck, cv = _host_codes(ck), _host_codes(cv)
+            rk, rv = rk.cpu().numpy(), rv.cpu().numpy()
         return CacheSnapshot(codes_K=CodesMatrix(codes=ck, nbits=self.config.nbits),
                              codes_V=CodesMatrix(codes=cv, nbits=self.config.nbits),
                              recent_K=rk, recent_V=rv, n_q=n_q, n_total=n_total)

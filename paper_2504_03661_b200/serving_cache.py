@@ -172,6 +172,12 @@ class ServingCache:
         self.recent_v[:, :, :, r] = v
         self._nr += 1
         self.n_recent.fill_(self._nr)
+        if self._side is None:
+            # the reference's sync worker flushes whole batches until the
+            # window is below the threshold (append_decode, kv_cache.py:183-206)
+            while self._nr >= self.R_f:
+                self._flush()
+            return
         inflight = self._pending[1] if self._pending else 0
         if self._nr - inflight >= self.R_f and self._pending is None:
             self._flush()

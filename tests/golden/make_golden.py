@@ -269,6 +269,14 @@ def make_baselines(pq_core, attention):
             out[f"iq_{mode}_{nb}_sz"] = np.array([prm.s, prm.z], np.float64)
             out[f"iq_{mode}_{nb}_Xh"] = pq_core.integer_dequantize(Q, prm)
     out["iq_X"] = X
+    # grid-valued data: many exact .5 boundaries after X / s + z
+    Xg = (np.arange(-15, 16) / 10).reshape(1, -1)
+    out["iqg_X"] = Xg
+    for nb in (2, 3, 4):
+        for mode in ("symmetric", "asymmetric"):
+            Q, prm = pq_core.integer_quantize(Xg, nb, mode)
+            out[f"iqg_{mode}_{nb}_Q"] = Q
+            out[f"iqg_{mode}_{nb}_sz"] = np.array([prm.s, prm.z], np.float64)
     Qp, Kp, Vp = (rng.standard_normal((n, 64)) for n in (7, 19, 19))
     out["pf_Q"], out["pf_K"], out["pf_V"] = Qp, Kp, Vp
     out["pf_causal"] = attention.prefill_attention(Qp, Kp, Vp)
@@ -300,13 +308,101 @@ def make_analysis(pq_core, harness):
     np.savez_compressed(os.path.join(OUT, "analysis.npz"), **out)
 
 
+def make_attention_wide(pq_core, attention, kv_cache):
+    """decode_step streams with codes wider than a byte (uint16 cells: nbits
+    12 and 10, the m32b12-style presets pq_core.py:80-83) at sizes that keep
+    the codebooks small; same record layout as make_attention."""
+    out = {}
+    rng = np.random.default_rng(57)
+    cases = [
+        # d, M, nbits, R, R_f, n_prefill, steps, block_size
+        (8, 2, 12, 16, 16, 500, 3, 1024),
+        (16, 4, 10, 8, 8, 300, 4, 128),
+    ]
+    for ci, (d, M, nbits, R, R_f, npre, steps, bs) in enumerate(cases):
+        cfg = pq_core.PQConfig(d=d, M=M, nbits=nbits)
+        ck, cv = codebook_pair(pq_core, cfg, np.random.default_rng(200 + ci))
+        n = npre + steps
+        K = rng.standard_normal((n, d)).astype(np.float32)
+        V = rng.standard_normal((n, d)).astype(np.float32)
+        cache = kv_cache.LayerKVCache(ck, cv, recent_capacity=R, flush_threshold=R_f,
+                                      worker="sync")
+        cache.prefill_ingest(K[:npre], V[:npre])
+        snap = cache.snapshot()
+        out[f"c{ci}_snap0_codes_k"], out[f"c{ci}_snap0_codes_v"] = (snap.codes_K.codes.copy(),
+                                                                    snap.codes_V.codes.copy())
+        out[f"c{ci}_snap0_recent_k"] = snap.recent_K.copy()
+        out[f"c{ci}_snap0_recent_v"] = snap.recent_V.copy()
+        qs, outs, nqs = [], [], []
+        for s in range(steps):
+            q = rng.standard_normal(d)
+            nqs.append(cache.snapshot().n_q)
+            outs.append(attention.decode_step(q, K[npre + s], V[npre + s], cache, ck, cv,
+                                              block_size=bs))
+            qs.append(q)
+        fin = cache.snapshot()
+        out[f"c{ci}_params"] = np.array([d, M, nbits, R, R_f, npre, steps, bs])
+        out[f"c{ci}_cents_k"], out[f"c{ci}_cents_v"] = ck.centroids, cv.centroids
+        out[f"c{ci}_steps_k"], out[f"c{ci}_steps_v"] = K[npre:], V[npre:]
+        out[f"c{ci}_q"], out[f"c{ci}_out"] = np.stack(qs), np.stack(outs)
+        out[f"c{ci}_nq"] = np.array(nqs)
+        out[f"c{ci}_final_codes_k"] = fin.codes_K.codes
+        out[f"c{ci}_final_codes_v"] = fin.codes_V.codes
+    out["ncases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(OUT, "attention_wide.npz"), **out)
+
+
+def make_seam(pq_core, attention):
+    """The lower seam (_kernels.score_codes / accumulate_mass, _kernels.py:46-65,
+    numba loops :27-43) and the Counters accounting (attention.py:56-63,
+    test_attention.py:99-107)."""
+    from pqkv import _kernels
+    out = {}
+    rng = np.random.default_rng(61)
+    for ci, (M, nbits, n) in enumerate([(64, 8, 3000), (4, 12, 5000), (8, 3, 777)]):
+        ksub = 1 << nbits
+        dt = np.uint8 if nbits <= 8 else np.uint16
+        codes = rng.integers(0, ksub, (n, M)).astype(dt)
+        codes[:7] = codes[7:14]  # repeated rows: same-bin collisions
+        lut = rng.standard_normal((M, ksub))
+        p = np.exp(rng.standard_normal(n) * 3)
+        out[f"s{ci}_codes"], out[f"s{ci}_lut"], out[f"s{ci}_p"] = codes, lut, p
+        out[f"s{ci}_scores"] = _kernels.score_codes(lut, codes)
+        out[f"s{ci}_mass"] = _kernels.accumulate_mass(codes, p, ksub)
+    # Counters through the public API (d=8, M=4, nbits=2 as test_attention.py)
+    cfg = pq_core.PQConfig(d=8, M=4, nbits=2)
+    ck, cv = codebook_pair(pq_core, cfg, np.random.default_rng(62))
+    X = rng.standard_normal((37, 8))
+    codes_k, codes_v = pq_core.assign_codes(X, ck), pq_core.assign_codes(X, cv)
+    q = rng.standard_normal(8)
+    lut = attention.build_key_lut(q, ck)
+    c1 = attention.Counters()
+    attention.score_tokens(lut, codes_k, c1)
+    c2 = attention.Counters()
+    attention.quantized_partial(lut, codes_k, codes_v, cv, counters=c2)
+    c3 = attention.Counters()
+    attention.dense_partial(q, X[:5], X[5:10], counters=c3)
+    out["ctr_X"], out["ctr_q"] = X, q
+    out["ctr_cents_k"], out["ctr_cents_v"] = ck.centroids, cv.centroids
+    out["ctr"] = np.array([[c.lut_lookups, c.adds, c.code_bytes_read, c.dense_bytes_read]
+                           for c in (c1, c2, c3)])
+    np.savez_compressed(os.path.join(OUT, "seam.npz"), **out)
+
+
 def main():
     pq_core, attention, kv_cache, fileio, harness = _ref()
+    if "--wide-only" in sys.argv:
+        make_attention_wide(pq_core, attention, kv_cache)
+        make_seam(pq_core, attention)
+        return
     if "--synth-only" in sys.argv:
         make_synth(harness)
         return
     if "--kmeans-only" in sys.argv:
         make_kmeans(pq_core, harness)
+        return
+    if "--baselines-only" in sys.argv:
+        make_baselines(pq_core, attention)
         return
     if "--baselines-only" in sys.argv:
         make_baselines(pq_core, attention)
@@ -322,6 +418,8 @@ def main():
     make_kmeans(pq_core, harness)
     make_baselines(pq_core, attention)
     make_analysis(pq_core, harness)
+    make_attention_wide(pq_core, attention, kv_cache)
+    make_seam(pq_core, attention)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -24,6 +24,11 @@ def _check(g, device):
             assert (prm.s, prm.z) == tuple(g[f"iq_{mode}_{nb}_sz"]) and prm.mode == mode
             np.testing.assert_array_equal(integer_dequantize(Q, prm, device=device),
                                           g[f"iq_{mode}_{nb}_Xh"])
+    for nb in (2, 3, 4):  # grid-valued inputs: exact .5 boundaries (true division)
+        for mode in ("symmetric", "asymmetric"):
+            Q, prm = integer_quantize(g["iqg_X"], nb, mode, device=device)
+            np.testing.assert_array_equal(Q, g[f"iqg_{mode}_{nb}_Q"])
+            assert (prm.s, prm.z) == tuple(g[f"iqg_{mode}_{nb}_sz"])
     np.testing.assert_allclose(prefill_attention(g["pf_Q"], g["pf_K"], g["pf_V"], device=device),
                                g["pf_causal"], rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(prefill_attention(g["pf_Q"], g["pf_K"], g["pf_V"], causal=False,

@@ -25,6 +25,12 @@ def _cuda():
     N.load()  # fails loudly if the library is missing
 
 
+def _np(x):
+    """snapshot fields: numpy when the cache was fed numpy (as the reference),
+    CUDA tensors when it was fed tensors"""
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
 def _cb(cents, kind, nbits):
     import paper_2504_03661_b200 as P
     M, ksub, dsub = cents.shape
@@ -209,8 +215,8 @@ def test_decode_step_replay_matches_reference(golden, ci):
                                   g[f"c{ci}_steps_v"][s], cache, ck, cv, block_size=bs))
     np.testing.assert_allclose(np.stack(outs), g[f"c{ci}_out"], rtol=RTOL, atol=ATOL)
     fin = cache.snapshot()
-    np.testing.assert_array_equal(fin.codes_K.codes.cpu().numpy(), g[f"c{ci}_final_codes_k"])
-    np.testing.assert_array_equal(fin.codes_V.codes.cpu().numpy(), g[f"c{ci}_final_codes_v"])
+    np.testing.assert_array_equal(_np(fin.codes_K.codes), g[f"c{ci}_final_codes_k"])
+    np.testing.assert_array_equal(_np(fin.codes_V.codes), g[f"c{ci}_final_codes_v"])
 
 
 def test_dense_merge_finalize_golden(golden):
@@ -657,9 +663,9 @@ def test_cache_sequences_match_reference(golden):
         for t_ in range(npre, npre + n):
             c.append_decode(K_[t_], V_[t_])
         s = c.snapshot()
-        np.testing.assert_array_equal(s.codes_K.codes.cpu().numpy(), g[f"t{tr}_codes_k"])
-        np.testing.assert_array_equal(s.codes_V.codes.cpu().numpy(), g[f"t{tr}_codes_v"])
-        np.testing.assert_array_equal(s.recent_K.cpu().numpy(), g[f"t{tr}_recent_k"])
+        np.testing.assert_array_equal(_np(s.codes_K.codes), g[f"t{tr}_codes_k"])
+        np.testing.assert_array_equal(_np(s.codes_V.codes), g[f"t{tr}_codes_v"])
+        np.testing.assert_array_equal(_np(s.recent_K), g[f"t{tr}_recent_k"])
         assert (s.n_q, s.n_total) == tuple(int(v) for v in g[f"t{tr}_nq"])
 
 
@@ -688,9 +694,9 @@ def test_async_worker_bit_identical_to_sync(worker):
     other.drain()
     a, b = sync.snapshot(), other.snapshot()
     assert (a.n_q, a.n_total) == (b.n_q, b.n_total)
-    np.testing.assert_array_equal(a.codes_K.codes.cpu().numpy(), b.codes_K.codes.cpu().numpy())
-    np.testing.assert_array_equal(a.codes_V.codes.cpu().numpy(), b.codes_V.codes.cpu().numpy())
-    np.testing.assert_array_equal(a.recent_K.cpu().numpy(), b.recent_K.cpu().numpy())
+    np.testing.assert_array_equal(_np(a.codes_K.codes), _np(b.codes_K.codes))
+    np.testing.assert_array_equal(_np(a.codes_V.codes), _np(b.codes_V.codes))
+    np.testing.assert_array_equal(_np(a.recent_K), _np(b.recent_K))
 
 
 def test_codebook_file_to_device(golden, tmp_path):

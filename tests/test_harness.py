@@ -127,3 +127,28 @@ def test_cli_train_matches_reference_training(tmp_path):
     cb = fileio.read_codebook(tmp_path / "cb_key.pqkv")
     np.testing.assert_array_equal(cb.centroids, g["train_C"])
     assert fileio.read_codebook(tmp_path / "cb_value.pqkv").kind == "value"
+
+
+@pytest.mark.gpu
+def test_cli_sensitivity_and_stats(tmp_path):
+    """`sensitivity` / `stats` (cli.py:307-366): the reference's options, JSON
+    files and echo lines, backed by analysis.py (pinned by analysis.npz)."""
+    import json
+    import os
+    from click.testing import CliRunner
+    from paper_2504_03661_b200 import analysis, cli, fileio
+    from paper_2504_03661_b200.pq_core import PQConfig
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "analysis.npz"))
+    fileio.write_tensor(tmp_path / "k.f32", g["X"])
+    run = CliRunner().invoke
+    r = run(cli.main, ["stats", "--keys", str(tmp_path / "k.f32"), "--out", str(tmp_path)])
+    assert r.exit_code == 0 and "global absmax" in r.output, r.output
+    st = json.loads((tmp_path / "stats.json").read_text())
+    np.testing.assert_allclose(st["absmax"], g["cs_absmax"], rtol=1e-12)
+    r = run(cli.main, ["sensitivity", "--keys", str(tmp_path / "k.f32"), "--m", "16",
+                       "--nbits", "4", "--seed", "2", "--out", str(tmp_path)])
+    assert r.exit_code == 0 and "pq sensitivity" in r.output, r.output
+    rep = json.loads((tmp_path / "sensitivity.json").read_text())
+    assert set(rep) == {"fraction", "bits_per_value", "pq", "int"}
+    want = analysis.sensitivity_study(g["X"], PQConfig(32, 16, 4, seed=2), fraction=0.01)
+    assert rep["pq"]["sensitivity"] == pytest.approx(want.sensitivity, rel=1e-12)

@@ -153,3 +153,55 @@ def test_naive_quantized_matches_decode(golden):
             g[f"c{ci}_steps_k"][0], g[f"c{ci}_steps_v"][0])
     a = O.naive_quantized_attention(g[f"c{ci}_q"][0], *args)
     np.testing.assert_allclose(a, g[f"c{ci}_out"][0], rtol=1e-9)
+
+
+# ------------------------------------------------ wide codes, seam, batched --
+
+@pytest.mark.parametrize("ci", range(2))
+def test_oracle_replays_wide_code_streams(golden, ci):
+    """uint16 cells (nbits 12 / 10): the oracle replays the reference's
+    decode_step streams (attention_wide.npz)."""
+    g = golden("attention_wide")
+    outs, cache = _replay(g, ci)
+    np.testing.assert_allclose(outs, g[f"c{ci}_out"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_array_equal(cache.codes_k, g[f"c{ci}_final_codes_k"])
+    np.testing.assert_array_equal(cache.codes_v, g[f"c{ci}_final_codes_v"])
+
+
+def test_oracle_seam_bit_exact(golden):
+    """The oracle's score / mass loops equal the reference's numba seam bit for bit."""
+    g = golden("seam")
+    for ci in range(3):
+        codes, lut, p = g[f"s{ci}_codes"], g[f"s{ci}_lut"], g[f"s{ci}_p"]
+        np.testing.assert_array_equal(O.score_codes(lut, codes), g[f"s{ci}_scores"])
+        np.testing.assert_array_equal(O.accumulate_mass(codes, p, lut.shape[1]),
+                                      g[f"s{ci}_mass"])
+
+
+def test_c_batched_gqa_oracle_matches_numpy_oracle():
+    """oracle_decode_gqa_mt (the full-shape GPU tests' checker) == the numpy
+    oracle per query head, ragged lengths and recent windows."""
+    if O.c_library() is None:
+        pytest.skip("oracle C library not built (make -C oracle)")
+    rng = np.random.default_rng(0)
+    B, Hq, Hkv, n, R = 3, 6, 2, 400, 5
+    ck = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    cv = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    q = rng.standard_normal((B, Hq, 128))
+    kc = rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8)
+    vc = rng.integers(0, 256, (B, Hkv, n, 64), dtype=np.uint8)
+    rk = rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)
+    rv = rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)
+    kn = rng.standard_normal((B, Hkv, 128)).astype(np.float32)
+    vn = rng.standard_normal((B, Hkv, 128)).astype(np.float32)
+    nq = np.array([400, 0, 17], np.int32)
+    nr = np.array([5, 2, 0], np.int32)
+    got = O.c_decode_batched(q, kn, vn, kc, vc, nq, rk, rv, nr, ck, cv, 8, threads=2)
+    G = Hq // Hkv
+    for b in range(B):
+        for h in range(Hq):
+            kv = h // G
+            want = O.decode_from_snapshot(q[b, h], kn[b, kv], vn[b, kv], kc[b, kv, :nq[b]],
+                                          vc[b, kv, :nq[b]], rk[b, kv, :nr[b]],
+                                          rv[b, kv, :nr[b]], ck, cv, block_size=8192)
+            np.testing.assert_allclose(got[b, h], want, rtol=1e-12, atol=1e-13)
