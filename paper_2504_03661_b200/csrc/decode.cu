@@ -615,6 +615,10 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int part = lane % TL, slot = lane / TL;  // SPL-subspace share, token slot
+    // unit order of the warps, reversed: a segment's partial last round of
+    // units goes to the high warps, which the issue arbiter favours (they end
+    // their units ~0.5 us before warps 0-3, profiles/r02_step_timeline.txt)
+    const int wu = WARPS - 1 - warp;
 
     // value codebook: one TMA bulk copy per CTA, overlapped with the first
     // segment's code prefetch and LUT build -- and, when the codebook is static
@@ -662,13 +666,18 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // early_codes needs the shared-memory copy of n_q to re-validate it
     const bool early = A.early_codes && nq_cached;
     auto first_ring = [&]() {
-        cm = cost_map(A.n_q, A.B, Hqp, A.num_ctas / P);
+        // one snapshot of the lengths: every later walk reads nq_s
+        const int32_t *src = A.n_q;
+        if (nq_cached) {
+            for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = __ldcg(A.n_q + bb);
+            __syncthreads();
+            src = nq_s;
+        }
+        cm = cost_map(src, A.B, Hqp, A.num_ctas / P);
         pos = cta_begin(cm, pc);
         end = min(cta_begin(cm, pc + 1), cm.total);
         int64_t p0 = pos;
-        have_s0 = next_segment(A.n_q, A.B, Hqp, &p0, end, &s0);
-        if (nq_cached)
-            for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = A.n_q[bb];
+        have_s0 = next_segment(src, A.B, Hqp, &p0, end, &s0);
         if (have_s0) {
             const int vh0 = vhead(s0.bh);
             const int b = vh0 / Hqv, hkv = (vh0 - b * Hqv) * HG / group;
@@ -677,7 +686,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 #pragma unroll
             for (int rr = 0; rr < RING; ++rr)
                 load_unit(Ur[rr], A.codes_k + head_off + part * SPL,
-                          A.codes_v + head_off + part * SPL, u0 + warp + rr * WARPS, slot, s0.lo,
+                          A.codes_v + head_off + part * SPL, u0 + wu + rr * WARPS, slot, s0.lo,
                           s0.hi);
         }
     };
@@ -696,8 +705,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     // now -- the load overlaps the first table build -- and, if any changed,
     // redo the work split and the first ring from the fresh values (below).
     int nq_fresh = 0;
-    if (early && tid < A.B)
-        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(nq_fresh) : "l"(A.n_q + tid));
+    if (early && tid < A.B) nq_fresh = __ldcg(A.n_q + tid);
     if (!early) first_ring();
 #ifdef PQKV_TRACE
     PQKV_TR(10, gtime());  // cost map read, first ring issued
@@ -735,9 +743,23 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 
     const int32_t *nq = nq_cached ? nq_s : A.n_q;
     bool ring_loaded = have_s0;  // the first segment's ring is in flight
-    if (nq_cached) __syncthreads();  // nq_s is written
     Segment sg;
-    bool validate = early;  // first segment of an early launch: check n_q
+    // early launches: the first segment's barrier (or, for a CTA without
+    // segments, the check after the loop) compares the pre-wait lengths with
+    // nq_fresh; on a mismatch the CTA restarts from the fresh lengths
+    bool validate = early;
+    auto restart = [&]() {
+        __syncthreads();  // every thread has read the flag
+        if (tid < A.B) nq_s[tid] = nq_fresh;
+        if (tid == 0) *stale_s = 0;
+        __syncthreads();
+        cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
+        ring_loaded = false;
+    };
+    bool stale_now = false;
+  segments:
     while (next_segment(nq, A.B, Hqp, &pos, end, &sg)) {
         const int vh = vhead(sg.bh);  // virtual head: query heads hq0 .. hq0 + HG - 1
         const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
@@ -752,7 +774,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         if (!ring_loaded) {
 #pragma unroll
             for (int rr = 0; rr < RING; ++rr)
-                load_unit(Ur[rr], kbase, vbase, u0 + warp + rr * WARPS, slot, lo, hi);
+                load_unit(Ur[rr], kbase, vbase, u0 + wu + rr * WARPS, slot, lo, hi);
         }
         ring_loaded = false;
 #ifdef PQKV_TRACE
@@ -781,22 +803,8 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                          reinterpret_cast<const char *>(A.lut + (int64_t)bh0 * KSUB * M) + c * 16384,
                          16384, bar_lut);
         }
-        if (validate) {
-            validate = false;
-            if (tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
-            __syncthreads();
-            if (*stale_s) {  // rare: restart the CTA's work from the fresh lengths
-                __syncthreads();  // every thread has read the flag
-                if (tid < A.B) nq_s[tid] = nq_fresh;
-                if (tid == 0) *stale_s = 0;
-                __syncthreads();
-                cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P);
-                pos = cta_begin(cm, pc);
-                end = min(cta_begin(cm, pc + 1), cm.total);
-                ring_loaded = false;
-                continue;
-            }
-        }
+        if (validate && tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;  // read after the
+                                                                            // barrier below
         // dense partial by the CTA holding the head's last tokens (for most CTAs
         // their first segment, so it overlaps the prologue)
 #ifndef PQKV_NO_DENSE
@@ -832,6 +840,11 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 #ifdef PQKV_TRACE
             if (nseg_ == 0) PQKV_TR(2, gtime());
 #endif
+            if (h == 0 && validate) {
+                validate = false;
+                stale_now = *stale_s != 0;
+                if (stale_now) break;  // rare: restart from the fresh lengths (below)
+            }
             if (do_dense && tid < D) {
                 // merge the warps' dense states into record dense_base + bh0 + h
                 float Mx = -INFINITY;
@@ -860,6 +873,11 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
             }
         }
 
+        if (stale_now) {
+            stale_now = false;
+            restart();
+            continue;
+        }
         SlotState<HG> S;
 #pragma unroll
         for (int h = 0; h < HG; ++h) {
@@ -875,14 +893,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         // every unit processed masked (units past the segment load nothing and
         // contribute p = 0) -- a branch in the body would make the compiler
         // drain the ring's pending loads.
-        int u = u0 + warp;
-        const int nunits = max(0, (u1 - u0 - warp + WARPS - 1) / WARPS);
+        int u = u0 + wu;
+        const int nunits = max(0, (u1 - u0 - wu + WARPS - 1) / WARPS);
         // running load position: the next unit to load is u + RING * WARPS
         constexpr int64_t kStep = (int64_t)WARPS * UT * M;  // bytes per unit step of a warp
         const int64_t dv = vbase - kbase;
         int tn = (u + RING * WARPS) * UT + slot;
         const uint8_t *kp = kbase + (int64_t)tn * M;
-        for (int trip = 0; trip < (nunits + RING - 1) / RING; ++trip) {
+        static_assert(RING == 2, "the remainder below handles one leftover unit");
+        for (int trip = 0; trip < nunits / RING; ++trip) {
             // pin the lane-constant address words in registers (no remat)
 #pragma unroll
             for (int k = 0; k < NPK; ++k) asm volatile("" : "+r"(packK[k]), "+r"(packV[k]));
@@ -924,6 +943,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 kp += GROUP * kStep;
                 tn += GROUP * WARPS * UT;
             }
+        }
+
+        if (nunits % RING) {
+            // an odd unit count: the last unit alone (ring slot 0), outside the
+            // straight-line body, instead of a masked full group
+            bool okA[1], okB[1];
+            const int ta = u * UT + slot;
+            okA[0] = ta >= lo && ta < hi;
+            okB[0] = ta + TS >= lo && ta + TS < hi;
+            process_units<kHalfCV, 1, HG>(Ur, S, packK, packV, okA, okB, []() {});
         }
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
@@ -1001,6 +1030,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 #ifdef PQKV_TRACE
     PQKV_TR(6, gtime());
 #endif
+    if (validate) {  // a CTA without segments in the pre-wait split checks here
+        validate = false;
+        if (tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+        __syncthreads();
+        if (*stale_s) {
+            restart();
+            goto segments;
+        }
+    }
     // ---- arrivals, after all of this CTA's segments (kept out of the segment
     // loop, whose code generation it would otherwise disturb).  Thread group
     // g = tid / 128 handles segments g, g + 4, ... in parallel: its leader
