@@ -32,6 +32,8 @@ extern "C" {
 #define PQKV_OK 0
 #define PQKV_EINVAL 1
 #define PQKV_ECUDA 2
+#define PQKV_EFORMAT 3 /* malformed file: the reference's FormatError */
+#define PQKV_EIO 4     /* file cannot be opened / read / written: OSError */
 
 #define PQKV_DTYPE_F32 0
 #define PQKV_DTYPE_BF16 1
@@ -256,6 +258,53 @@ int pqkv_score_codes_f64(const double *lut, const void *codes, int64_t n, int M,
                          int nbits, double *scores, void *stream);
 int pqkv_accumulate_mass_f64(const void *codes, const double *p, int64_t n, int M,
                              int nbits, double *h, void *stream);
+
+/* ---- Binary formats at the boundary (fileio.py:71-160) ----------------
+ * Unlike the entry points above these do file IO, allocate a pinned staging
+ * buffer (and a device temporary for layout conversion) and synchronise
+ * `stream` before returning.  Errors: PQKV_EFORMAT with the reference's
+ * FormatError texts, PQKV_EIO for the file system.
+ *
+ * .pqkv codebook (read_codebook fileio.py:80-96, write_codebook :71-77):
+ * "PQKV" + <IBIII (version 1, kind 0 key / 1 value, d, M, nbits), a 21-byte
+ * header, then M * 2^nbits * dsub float32, subspace-major (unaligned body).
+ *   pqkv_codebook_file_info  header + size check, no body read
+ *   pqkv_read_codebook       body -> centroids [M][ksub][dsub] (device, or
+ *                            host with PQKV_FILE_HOST) and/or, m64b8 only,
+ *                            straight into the decode kernel's layout
+ *                            (pqkv_prepare_key/value_codebook by the kind)
+ *   pqkv_write_codebook      centroids (device, or host) -> file */
+#define PQKV_FILE_HOST 1 /* the centroid pointer is host memory */
+int pqkv_codebook_file_info(const char *path, int *kind, int *d, int *M, int *nbits);
+int pqkv_read_codebook(const char *path, int flags, float *centroids, float *layout,
+                       void *stream);
+int pqkv_write_codebook(const char *path, int kind, int d, int M, int nbits,
+                        const float *centroids, int flags, void *stream);
+
+/* .pqkc cache dump (write_cache_dump fileio.py:99-114, read_cache_dump
+ * :117-156): "PQKC" + <IIIIQI (version 1, d, M, nbits, n_q u64, recent_len),
+ * K codes, V codes (reference row layout), recent K, recent V (float32).  A
+ * file of `heads` caches (every layer x sequence x KV head of a serving
+ * cache) is `heads` such records back to back.  Device buffers: head h's codes
+ * at codes + h * code_stride cells (layout PQKV_CODES_ROWS, or
+ * PQKV_CODES_DECODE for m64b8, converted on the device), its recent rows at
+ * recent + h * recent_stride floats.  Reading checks every record's header
+ * against the destination and, when a cell can hold one, out-of-range codes
+ * ("corrupted dump").
+ *   pqkv_cache_dump_info     header of the record at byte `offset` */
+#define PQKV_CODES_ROWS 0
+#define PQKV_CODES_DECODE 1
+int pqkv_cache_dump_info(const char *path, int64_t offset, int *d, int *M, int *nbits,
+                         int64_t *n_q, int *recent_len, int64_t *record_bytes);
+int pqkv_write_cache_dumps(const char *path, int heads, int d, int M, int nbits,
+                           int64_t n_q, int recent_len, const void *codes_k,
+                           const void *codes_v, int64_t code_stride, int layout,
+                           const float *recent_k, const float *recent_v,
+                           int64_t recent_stride, void *stream);
+int pqkv_read_cache_dumps(const char *path, int heads, int d, int M, int nbits,
+                          int64_t n_q, int recent_len, void *codes_k, void *codes_v,
+                          int64_t code_stride, int layout, float *recent_k,
+                          float *recent_v, int64_t recent_stride, void *stream);
 
 /* Test-only: one kernel that releases a following PDL launch immediately
  * (griddepcontrol.launch_dependents), waits ns nanoseconds, then writes v to

@@ -18,6 +18,7 @@ from .attention import (Lut, SoftmaxPartial, Counters, empty_partial, build_key_
                         decode_step)
 from .fileio import (FormatError, read_codebook, write_codebook, read_cache_dump,
                      write_cache_dump, dump_cache, read_tensor, write_tensor)
+from . import fileio, _kernels
 from .training import kmeans_train, train_codebooks
 from .baselines import IntQuantParams, integer_quantize, integer_dequantize, prefill_attention
 from .analysis import (ChannelStats, SensitivityReport, channel_stats, isolate_outliers,

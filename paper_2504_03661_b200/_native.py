@@ -15,7 +15,8 @@ import torch
 
 from .build import LIB
 
-PQKV_OK, PQKV_EINVAL, PQKV_ECUDA = 0, 1, 2
+PQKV_OK, PQKV_EINVAL, PQKV_ECUDA, PQKV_EFORMAT, PQKV_EIO = 0, 1, 2, 3, 4
+FILE_HOST, CODES_ROWS, CODES_DECODE = 1, 0, 1
 DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 PARTIAL_HEADER = 4
 DECODE_PDL, DECODE_STATIC_CODEBOOKS, DECODE_F16_VALUE_CODEBOOK, DECODE_EARLY_CODES = 1, 2, 4, 8
@@ -25,6 +26,8 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _I64 = ctypes.c_int64
 _F = ctypes.c_float
+_PI = ctypes.POINTER(ctypes.c_int)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
 
 # name -> (restype, argtypes); mirrors include/pqkv_sm100.h
 SIGNATURES = {
@@ -55,6 +58,14 @@ SIGNATURES = {
     "pqkv_accumulate_mass": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_score_codes_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_accumulate_mass_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "pqkv_codebook_file_info": (_I, [ctypes.c_char_p, _PI, _PI, _PI, _PI]),
+    "pqkv_read_codebook": (_I, [ctypes.c_char_p, _I, _P, _P, _P]),
+    "pqkv_write_codebook": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _P, _I, _P]),
+    "pqkv_cache_dump_info": (_I, [ctypes.c_char_p, _I64, _PI, _PI, _PI, _PI64, _PI, _PI64]),
+    "pqkv_write_cache_dumps": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _I64, _I, _P, _P, _I64, _I,
+                                    _P, _P, _I64, _P]),
+    "pqkv_read_cache_dumps": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _I64, _I, _P, _P, _I64, _I,
+                                   _P, _P, _I64, _P]),
     "pqkv_debug_delayed_fill": (_I, [_P, _I, _I, ctypes.c_longlong, _P]),
 }
 
@@ -94,6 +105,11 @@ def check(rc: int, what: str) -> None:
     msg = load(require_cuda=False).pqkv_last_error().decode(errors="replace")
     if rc == PQKV_EINVAL:
         raise ValueError(msg or what)
+    if rc == PQKV_EFORMAT:
+        from .fileio import FormatError
+        raise FormatError(msg or what)
+    if rc == PQKV_EIO:
+        raise OSError(msg or what)
     raise RuntimeError(msg or what)
 
 

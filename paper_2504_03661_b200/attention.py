@@ -422,3 +422,12 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         timings["flush_wait"] = timings.get("flush_wait", 0.0) + flush
         timings["append"] = timings.get("append", 0.0) + (t1 - t0 - flush)
     return out[0].double().cpu().numpy() if host else out[0]
+
+
+def __getattr__(name):
+    # the reference's attention.py also defines prefill_attention (:290-311);
+    # here it is in baselines.py (it imports this package's modules)
+    if name == "prefill_attention":
+        from .baselines import prefill_attention
+        return prefill_attention
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -326,6 +326,21 @@ class LayerKVCache:
             self._r0, self._rlen = 0, r
             self._n_total = snap.n_total
 
+    def _load_device(self, n_q: int, r: int, fill) -> None:
+        """Restore into an empty cache: fill(codes_k, codes_v, recent_k,
+        recent_v) writes n_q code rows (this cache's layout) and r recent rows
+        into the given device buffers (fileio.restore_cache, C reader)."""
+        if self._n_total != 0:
+            raise RuntimeError("load_snapshot requires an empty cache")
+        with self._lock:
+            self._ensure_store(max(n_q, 1))
+            if r:
+                self._ensure_recent(r)
+            with torch.cuda.device(self.device):
+                fill(self._store_k, self._store_v, self._rk, self._rv)
+            self._n_q, self._r0, self._rlen = n_q, 0, r
+            self._n_total = n_q + r
+
     # -- reads -------------------------------------------------------------------
     def raw_snapshot(self):
         """(codes_k, codes_v, recent_K, recent_V, n_q, n_total) with the code

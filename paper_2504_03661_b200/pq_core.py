@@ -248,3 +248,18 @@ def reconstruct(codes: CodesMatrix, cb: Codebook):
 
 def bits_per_value(config: PQConfig) -> float:
     return config.M * config.nbits / config.d
+
+
+# The reference's pq_core also defines k-means training (:171-266) and the
+# integer-quantization baseline (:149-156, :312-354); here they live in
+# training.py / baselines.py and are re-exported lazily (they import this module).
+_LAZY = {"kmeans_train": "training", "train_codebooks": "training",
+         "IntQuantParams": "baselines", "integer_quantize": "baselines",
+         "integer_dequantize": "baselines"}
+
+
+def __getattr__(name):
+    if name in _LAZY:
+        import importlib
+        return getattr(importlib.import_module(f".{_LAZY[name]}", __package__), name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

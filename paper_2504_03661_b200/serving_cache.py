@@ -242,6 +242,12 @@ class ServingCache:
         self.n_recent.fill_(self._nr)
         self._pending = None
 
+    def _set_lengths(self, n_q: int, n_recent: int) -> None:
+        """After a restore (fileio.load_serving_cache): publish the lengths."""
+        self._nq, self._nr = n_q, n_recent
+        self.n_q.fill_(n_q)
+        self.n_recent.fill_(n_recent)
+
     def snapshot(self, l: int, b: int, h: int):
         """Host copy of (codes_k, codes_v) in the reference row layout and the
         recent rows of (layer, sequence, KV head), as the decodes enqueued so

@@ -11,6 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+# the vendored reference suite runs only through tests/ref_suite/run_ref_suite.py
+collect_ignore = ["ref_suite"]
 
 
 def pytest_configure(config):
