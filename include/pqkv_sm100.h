@@ -259,6 +259,19 @@ int pqkv_score_codes_f64(const double *lut, const void *codes, int64_t n, int M,
 int pqkv_accumulate_mass_f64(const void *codes, const double *p, int64_t n, int M,
                              int nbits, double *h, void *stream);
 
+/* The reference API's float64 small ops on the GPU (the decode kernels keep
+ * their float32 tables in shared memory):
+ *   pqkv_build_lut_f64      build_key_lut (attention.py:70-83): out
+ *                           [n_heads][M][ksub] f64 (the Lut.table layout),
+ *                           (sum_j C[i][c][j] q[i dsub + j]) * scale
+ *   pqkv_dense_partial_f64  dense_partial (:169-190) over r rows K, V
+ *                           [r][d] f64 (d <= 1024): rec = (m, l, 0, 0,
+ *                           acc[d]) f64 */
+int pqkv_build_lut_f64(const double *q, int64_t n_heads, int d, const float *cb_k, int M,
+                       int nbits, double scale, double *out, void *stream);
+int pqkv_dense_partial_f64(const double *q, const double *K, const double *V, int64_t r,
+                           int d, double scale, double *rec, void *stream);
+
 /* ---- Binary formats at the boundary (fileio.py:71-160) ----------------
  * Unlike the entry points above these do file IO, allocate a pinned staging
  * buffer (and a device temporary for layout conversion) and synchronise

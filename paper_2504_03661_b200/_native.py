@@ -58,6 +58,8 @@ SIGNATURES = {
     "pqkv_accumulate_mass": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_score_codes_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
     "pqkv_accumulate_mass_f64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "pqkv_build_lut_f64": (_I, [_P, _I64, _I, _P, _I, _I, ctypes.c_double, _P, _P]),
+    "pqkv_dense_partial_f64": (_I, [_P, _P, _P, _I64, _I, ctypes.c_double, _P, _P]),
     "pqkv_codebook_file_info": (_I, [ctypes.c_char_p, _PI, _PI, _PI, _PI]),
     "pqkv_read_codebook": (_I, [ctypes.c_char_p, _I, _P, _P, _P]),
     "pqkv_write_codebook": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _P, _I, _P]),

@@ -84,16 +84,23 @@ def _scale(d: int, scale):
 
 
 def build_key_lut(q_n, cb_K: Codebook, scale: float | None = None) -> Lut:
-    """table[i][c] = scale * dot(q_n subvector i, key centroid c of subspace i)."""
+    """table[i][c] = scale * dot(q_n subvector i, key centroid c of subspace i).
+
+    ``table`` is float64 like the reference (pqkv_build_lut_f64); the kernels'
+    float32 centroid-major table (pqkv_build_lut) rides along as
+    ``device_table``."""
     cfg = cb_K.config
     host = not _is_tensor(q_n)
-    q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
-                  torch.float32)
-    if q.shape[0] != cfg.d:
-        raise ValueError(f"query width {q.shape[0]} != codebook d {cfg.d}")
-    cm = K.build_lut(q.view(1, -1), cb_K.device_centroids(q.device), cfg.nbits,
-                     _scale(cfg.d, scale))[0]
-    table = cm.t().double().cpu().numpy().copy() if host else cm.t()
+    q64 = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
+                    torch.float64)
+    if q64.shape[0] != cfg.d:
+        raise ValueError(f"query width {q64.shape[0]} != codebook d {cfg.d}")
+    dev = q64.device
+    sc = _scale(cfg.d, scale)
+    cents = cb_K.device_centroids(dev)
+    cm = K.build_lut(q64.float().view(1, -1), cents, cfg.nbits, sc)[0]
+    t64 = K.build_lut_f64(q64.view(1, -1), cents, cfg.nbits, sc)[0]
+    table = t64.cpu().numpy() if host else t64
     return Lut(table=table, nbits=cfg.nbits, device_table=cm)
 
 
@@ -129,8 +136,12 @@ def score_tokens(lut: Lut, codes_K: CodesMatrix, counters: Counters | None = Non
     host = not _is_tensor(c)
     if n == 0:
         return np.empty(0, dtype=np.float64) if host else torch.empty(0, device=tab.device)
-    s = K.score_codes(tab, codes_K.device_codes(tab.device), lut.nbits)
-    return s.double().cpu().numpy() if host else s
+    # the float64 seam with the reference's summation order (_kernels.py:27-34)
+    from . import _kernels
+    t64 = lut.table if _is_tensor(lut.table) else to_device(
+        np.asarray(lut.table, dtype=np.float64), torch.float64, tab.device)
+    s = _kernels.score_codes(t64, codes_K.device_codes(tab.device))
+    return s.cpu().numpy() if host else s
 
 
 def _decode_codes(codes: torch.Tensor, cfg) -> torch.Tensor:
@@ -184,7 +195,7 @@ def _n_tensor(n: int, device) -> torch.Tensor:
 def _partial_from_record(rec: torch.Tensor, host: bool) -> SoftmaxPartial:
     vals = rec.double().cpu().numpy()
     m, l = float(vals[0]), float(vals[1])
-    acc = vals[4:].copy() if host else rec[4:].clone()
+    acc = vals[4:].copy() if host else rec[4:].double().clone()
     if l == 0.0:
         m = -np.inf
     return SoftmaxPartial(m=m, l=l, acc=acc)
@@ -229,15 +240,16 @@ def quantized_partial(lut: Lut, codes_K: CodesMatrix, codes_V: CodesMatrix, cb_V
 
 def dense_partial(q_n, K_dense, V_dense, scale: float | None = None,
                   counters: Counters | None = None) -> SoftmaxPartial:
-    """Standard softmax partial over full-precision rows."""
+    """Standard softmax partial over full-precision rows, in float64 like the
+    reference (pqkv_dense_partial_f64)."""
     host = not _is_tensor(q_n)
     q = to_device(np.asarray(q_n, dtype=np.float64).ravel() if host else q_n.reshape(-1),
-                  torch.float32)
+                  torch.float64)
     d = q.shape[0]
-    Kd = to_device(K_dense if _is_tensor(K_dense) else np.asarray(K_dense, dtype=np.float32),
-                   torch.float32, q.device).reshape(-1, d)
-    Vd = to_device(V_dense if _is_tensor(V_dense) else np.asarray(V_dense, dtype=np.float32),
-                   torch.float32, q.device)
+    Kd = to_device(K_dense if _is_tensor(K_dense) else np.asarray(K_dense, dtype=np.float64),
+                   torch.float64, q.device).reshape(-1, d)
+    Vd = to_device(V_dense if _is_tensor(V_dense) else np.asarray(V_dense, dtype=np.float64),
+                   torch.float64, q.device)
     if Vd.dim() == 1:
         Vd = Vd.view(1, -1)
     if Kd.shape[0] != Vd.shape[0]:
@@ -247,12 +259,8 @@ def dense_partial(q_n, K_dense, V_dense, scale: float | None = None,
     r = Kd.shape[0]
     if counters is not None:
         counters.dense_bytes_read += 2 * r * d * 4
-    merged = torch.empty((1, d + 4), dtype=torch.float32, device=q.device)
-    K.decode_finish(None, 1, None, q.view(1, d), _scale(d, scale),
-                    recent_k=Kd.contiguous().view(1, 1, r, d),
-                    recent_v=Vd.contiguous().view(1, 1, r, d),
-                    n_recent=_n_tensor(r, q.device), merged=merged, B=1, Hq=1, d=d)
-    return _partial_from_record(merged[0], host)
+    rec = K.dense_partial_f64(q, Kd, Vd, _scale(d, scale))
+    return _partial_from_record(rec, host)
 
 
 def merge_partials(a: SoftmaxPartial, b: SoftmaxPartial) -> SoftmaxPartial:
@@ -406,10 +414,23 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
                     dev).contiguous().view(1, 1, r, cfg.d) if r else None
     if counters is not None:
         counters.dense_bytes_read += 2 * (r + 1) * cfg.d * 4
-    out = torch.empty((1, cfg.d), dtype=torch.float32, device=dev)
-    K.decode_finish(ws, 1, nq_t, q.view(1, -1), sc, recent_k=rkd, recent_v=rvd,
-                    n_recent=_n_tensor(r, dev) if r else None, k_cur=kc.view(1, 1, -1),
-                    v_cur=vc.view(1, 1, -1), out=out)
+    # quantized span: the split records merged (fixed order) into one record;
+    # dense rows (recent + current token) in float64 as the reference
+    # (dense_partial :169-190), merged and finalized in float64 (:193-211)
+    dense = K.dense_partial_f64(
+        q.double(), torch.cat([rkd.view(r, cfg.d).double() if r else kc.new_empty((0, cfg.d),
+                                                                                   dtype=torch.float64),
+                               _row64(k_n, dev)]),
+        torch.cat([rvd.view(r, cfg.d).double() if r else vc.new_empty((0, cfg.d),
+                                                                       dtype=torch.float64),
+                   _row64(v_n, dev)]), sc)
+    if n_q:
+        qrec = torch.empty((1, cfg.d + 4), dtype=torch.float32, device=dev)
+        K.decode_finish(ws, 1, nq_t, q.view(1, -1), sc, merged=qrec)
+        out = _merge_finalize64(qrec[0].double(), dense)
+    else:
+        out = dense[4:] / dense[1]
+    out = out.view(1, -1)
     if timings is not None:
         t1 = time.perf_counter()
         timings["dense"] = timings.get("dense", 0.0) + (t1 - t0)
@@ -422,6 +443,22 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
         timings["flush_wait"] = timings.get("flush_wait", 0.0) + flush
         timings["append"] = timings.get("append", 0.0) + (t1 - t0 - flush)
     return out[0].double().cpu().numpy() if host else out[0]
+
+
+def _row64(x, dev) -> torch.Tensor:
+    """The current token's row in float64, as the reference stacks it (:266-267)."""
+    return to_device(x if _is_tensor(x) else np.asarray(x, dtype=np.float64), torch.float64,
+                     dev).reshape(1, -1)
+
+
+def _merge_finalize64(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """merge_partials + finalize (:193-211) of two (m, l, 0, 0, acc) float64
+    records on the device."""
+    if float(a[1]) == 0.0:
+        return b[4:] / b[1]
+    m = torch.maximum(a[0], b[0])
+    wa, wb = torch.exp(a[0] - m), torch.exp(b[0] - m)
+    return (a[4:] * wa + b[4:] * wb) / (a[1] * wa + b[1] * wb)
 
 
 def __getattr__(name):

@@ -116,33 +116,41 @@ constexpr int kSwitchCost = PQKV_SWITCH_COST;  // tokens-equivalent of a head sw
 #endif
 constexpr int kDenseCost = PQKV_DENSE_COST;
 
-// The last kTailCtas CTAs of a launch get kTailPenalty fewer cost units: in a
-// PDL-chained sequence of launches they land on the SMs freed last by the
-// previous launch (its last-arriver finishers) and start late.
-#ifndef PQKV_TAIL_CTAS
-#define PQKV_TAIL_CTAS 0
+// Launch-order ramp: in a PDL-chained sequence of launches the highest CTA
+// indices are dispatched last, onto the SMs the previous launch frees last
+// (its last arrivers), and reach their main loop up to ~3 us late
+// (profiles/r02_step_timeline.txt).  The last kRampCtas CTAs therefore get
+// kRampSlope, 2 kRampSlope, ... fewer cost units (CTA n-1 the fewest).  The
+// split stays a pure function of (n_q, grid): results are deterministic.
+#ifndef PQKV_RAMP_CTAS
+#define PQKV_RAMP_CTAS 0  // measured: every ramp tried lost 3-5%
 #endif
-#ifndef PQKV_TAIL_PENALTY
-#define PQKV_TAIL_PENALTY 0
+#ifndef PQKV_RAMP_SLOPE
+#define PQKV_RAMP_SLOPE 16
 #endif
-constexpr int kTailCtas = PQKV_TAIL_CTAS, kTailPenalty = PQKV_TAIL_PENALTY;
+constexpr int kRampCtas = PQKV_RAMP_CTAS, kRampSlope = PQKV_RAMP_SLOPE;
+static_assert(kRampSlope % kChunkAlign == 0, "ramp steps keep chunks aligned");
 
 struct CostMap {
     int64_t total;
-    int64_t chunk;   // cost units of CTAs [0, nfirst)
-    int64_t chunk2;  // cost units of CTAs [nfirst, num_ctas)
-    int nfirst;
+    int64_t chunk;  // cost units of an unramped CTA
+    int n;          // CTAs (or CTA groups)
+    int ramp;       // the last `ramp` CTAs are ramped ...
+    int64_t slope;  // ... by `slope`, 2 `slope`, ... units
 };
 
-// first cost position of CTA c (c == num_ctas: past the end)
+// first cost position of CTA c (c == n: past the end)
 __device__ __forceinline__ int64_t cta_begin(const CostMap &cm, int c) {
-    return c < cm.nfirst ? (int64_t)c * cm.chunk
-                         : (int64_t)cm.nfirst * cm.chunk + (int64_t)(c - cm.nfirst) * cm.chunk2;
+    const int64_t j = max(0, c - (cm.n - cm.ramp));
+    return (int64_t)c * cm.chunk - cm.slope * (j * (j + 1) / 2);
 }
 // CTA holding cost position pos
 __device__ __forceinline__ int cta_of(const CostMap &cm, int64_t pos) {
-    const int64_t split = (int64_t)cm.nfirst * cm.chunk;
-    return pos < split ? (int)(pos / cm.chunk) : cm.nfirst + (int)((pos - split) / cm.chunk2);
+    const int first = cm.n - cm.ramp;
+    if (pos < (int64_t)first * cm.chunk) return (int)(pos / cm.chunk);
+    int c = first;
+    while (c + 1 < cm.n && cta_begin(cm, c + 1) <= pos) ++c;
+    return c;
 }
 
 __device__ __forceinline__ int64_t head_span(int n) {
@@ -150,16 +158,24 @@ __device__ __forceinline__ int64_t head_span(int n) {
 }
 
 __device__ __forceinline__ CostMap cost_map(const int32_t *__restrict__ n_q, int B, int Hq,
-                                            int num_ctas) {
+                                            int num_ctas, int P = 1) {
     int64_t tot = 0;
     for (int b = 0; b < B; ++b) tot += (int64_t)Hq * head_span(n_q[b]);
-    const int tail = (num_ctas > 2 * kTailCtas) ? kTailCtas : 0;
-    int64_t chunk = (tot + (int64_t)tail * kTailPenalty + num_ctas - 1) / num_ctas;
-    chunk = (chunk + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
-    if (chunk < kChunkAlign) chunk = kChunkAlign;
-    int64_t chunk2 = chunk - (tail ? kTailPenalty : 0);
-    chunk2 = max(chunk2 / kChunkAlign * kChunkAlign, (int64_t)kChunkAlign);
-    return {tot, chunk, chunk2, num_ctas - tail};
+    // groups of P CTAs: P times fewer groups, each P times steeper
+    int ramp = kRampCtas / P;
+    int64_t slope = (int64_t)kRampSlope * P;
+    if (num_ctas < 4 * ramp) ramp = 0;
+    auto chunk_for = [&](int r) {
+        int64_t c = (tot + slope * ((int64_t)r * (r + 1) / 2) + num_ctas - 1) / num_ctas;
+        c = (c + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
+        return c < kChunkAlign ? (int64_t)kChunkAlign : c;
+    };
+    int64_t chunk = chunk_for(ramp);
+    if (ramp && chunk - slope * ramp < 4 * slope) {  // small problems: no ramp
+        ramp = 0;
+        chunk = chunk_for(0);
+    }
+    return {tot, chunk, num_ctas, ramp, ramp ? slope : 0};
 }
 
 // Cost-axis position of token 0 of head bh; *len = n_q[b] (>= 0).

@@ -111,7 +111,8 @@ constexpr int SMEM_BYTES = OFF_NQ + 4 * kNqCache;
 // debug-only timeline: per (launch mod 64, CTA) [smid, t_entry, t_ready,
 // t_loop0_end, t_exit, nseg, t_segs_done, t_post_wait, t_lut_pre, t_cv_ready]
 constexpr int kTraceLaunches = 64, kTraceCtas = 256;
-__device__ unsigned long long g_trace[kTraceLaunches * kTraceCtas * 16];
+constexpr int kTraceSlots = 32;
+__device__ unsigned long long g_trace[kTraceLaunches * kTraceCtas * kTraceSlots];
 __device__ unsigned long long g_wtrace[kTraceLaunches * kTraceCtas * 32];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -120,7 +121,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define PQKV_TR(slot, val)                                                          \
     if (threadIdx.x == 0 && blockIdx.x < kTraceCtas)                                \
-    g_trace[((A.trace_id % kTraceLaunches) * kTraceCtas + blockIdx.x) * 16 + (slot)] = (val)
+    g_trace[((A.trace_id % kTraceLaunches) * kTraceCtas + blockIdx.x) * kTraceSlots + (slot)] = (val)
+// intra-CTA phase: SM cycles since the grid-dependency wait returned
+#define PQKV_TRC(slot) PQKV_TR(slot, clock64() - clk_pw_)
 #else
 #define PQKV_TR(slot, val)
 #endif
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
             __syncthreads();
             src = nq_s;
         }
-        cm = cost_map(src, A.B, Hqp, A.num_ctas / P);
+        cm = cost_map(src, A.B, Hqp, A.num_ctas / P, P);
         pos = cta_begin(cm, pc);
         end = min(cta_begin(cm, pc + 1), cm.total);
         int64_t p0 = pos;
@@ -699,6 +702,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     pdl_wait();  // q, n_q, recent rows, counters and partials belong to the stream order
 #ifdef PQKV_TRACE
     PQKV_TR(7, gtime());
+    const long long clk_pw_ = clock64();
 #endif
     // early: the lengths read before the wait may predate the previous kernel
     // (e.g. a publication's n_q.fill_ right before this launch).  Re-read them
@@ -708,7 +712,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     if (early && tid < A.B) nq_fresh = __ldcg(A.n_q + tid);
     if (!early) first_ring();
 #ifdef PQKV_TRACE
-    PQKV_TR(10, gtime());  // cost map read, first ring issued
+    PQKV_TRC(10);  // cost map read, first ring issued
 #endif
     if (tid == 0 && !A.early_cv) {
         mbar_expect_tx(bar_cv, kCvBytes);
@@ -753,7 +757,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         if (tid < A.B) nq_s[tid] = nq_fresh;
         if (tid == 0) *stale_s = 0;
         __syncthreads();
-        cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P);
+        cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P, P);
         pos = cta_begin(cm, pc);
         end = min(cta_begin(cm, pc + 1), cm.total);
         ring_loaded = false;
@@ -778,12 +782,12 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         }
         ring_loaded = false;
 #ifdef PQKV_TRACE
-        if (nseg_ == 0) PQKV_TR(11, gtime());  // ring loads issued
+        if (nseg_ == 0) PQKV_TRC(11);  // ring loads issued
 #endif
 
         __syncthreads();  // previous segment's epilogue is done with lut_s
 #ifdef PQKV_TRACE
-        if (nseg_ == 0) PQKV_TR(12, gtime());
+        if (nseg_ == 0) PQKV_TRC(12);
 #endif
         if (kLutFromQ) {
             float4 cc[lut_iters<NT>()];
@@ -793,7 +797,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 lut_build<NT>(lut_s + h * (LUT_BYTES / 4), cc, A.q + (int64_t)(bh0 + h) * D,
                               A.scale, tid);
 #ifdef PQKV_TRACE
-            if (nseg_ == 0) PQKV_TR(8, gtime());  // first table built
+            if (nseg_ == 0) PQKV_TRC(8);  // first table built
 #endif
         } else if (tid == 0) {
             mbar_expect_tx(bar_lut, LUT_BYTES);
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                                  A.k_cur, A.v_cur, A.Hkv, bh0 + h, b, hkv, warp, WARPS, lane, dn_m,
                                  dn_l, dn_acc);
 #ifdef PQKV_TRACE
-            if (nseg_ == 0) PQKV_TR(13, gtime());
+            if (nseg_ == 0) PQKV_TRC(13);
 #endif
             if (h == 0) {
                 if (!kLutFromQ) {
@@ -832,13 +836,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                     mbar_wait(bar_cv, 0);
                     cv_ready = true;
 #ifdef PQKV_TRACE
-                    PQKV_TR(9, gtime());  // value codebook arrived
+                    PQKV_TRC(9);  // value codebook arrived
 #endif
                 }
             }
             __syncthreads();
 #ifdef PQKV_TRACE
-            if (nseg_ == 0) PQKV_TR(2, gtime());
+            if (nseg_ == 0) {
+                PQKV_TR(2, gtime());
+                PQKV_TRC(16);  // main loop starts
+            }
 #endif
             if (h == 0 && validate) {
                 validate = false;
@@ -1029,6 +1036,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     }
 #ifdef PQKV_TRACE
     PQKV_TR(6, gtime());
+    const long long clk_segs = clock64();
 #endif
     if (validate) {  // a CTA without segments in the pre-wait split checks here
         validate = false;
@@ -1067,6 +1075,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 const bool last = (old == c_last - c_first);
                 if (last) A.counters[vh2] = 0;  // ready for the next launch
                 flag_s[grp] = last ? 1 : 0;
+#ifdef PQKV_TRACE
+                if (k == 0) PQKV_TR(14, clock64() - clk_segs);  // cycles to the arrival
+#endif
             }
             named_bar_sync(1 + grp, D);  // this group's 128 threads
             const bool last = flag_s[grp] != 0;
@@ -1078,6 +1089,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                     finish_head(A.parts, (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq, HG,
                                 s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged,
                                 P, half);
+#ifdef PQKV_TRACE
+                if (k == 0) PQKV_TR(15, clock64() - clk_segs);  // cycles to the merge's end
+#endif
             }
         }
     }
@@ -1441,7 +1455,7 @@ extern "C" int pqkv_decode_grid(int d, int M, int nbits, int *num_ctas) {
 }
 
 #ifdef PQKV_TRACE
-extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {  // n <= 64 * 256 * 16
+extern "C" int pqkv_debug_trace(unsigned long long *host, int n) {  // n <= 64 * 256 * 32
     return cudaMemcpyFromSymbol(host, fast::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
                ? 0 : 2;
 }

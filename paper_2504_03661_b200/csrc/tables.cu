@@ -165,6 +165,87 @@ __global__ void accumulate_mass_f64_kernel(const CT *__restrict__ codes,
     if (c < ksub) h[(int64_t)i * ksub + c] = acc;
 }
 
+// The reference API's float64 small ops (build_key_lut attention.py:70-83,
+// dense_partial :169-190), for callers of the reference API on the GPU: the
+// table / partial in float64 like the reference (the decode kernels use their
+// own float32 tables in shared memory).
+__global__ void build_lut_f64_kernel(const double *__restrict__ q, int d,
+                                     const float *__restrict__ cb, int M, int ksub, double scale,
+                                     double *__restrict__ out) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)M * ksub) return;
+    const int h = blockIdx.y, dsub = d / M;
+    const int i = (int)(idx / ksub), c = (int)(idx - (int64_t)i * ksub);
+    const double *qh = q + (int64_t)h * d + i * dsub;
+    const float *cc = cb + ((int64_t)i * ksub + c) * dsub;
+    double s = 0.0;
+    for (int j = 0; j < dsub; ++j) s += (double)cc[j] * qh[j];
+    out[(int64_t)h * M * ksub + idx] = s * scale;
+}
+
+// One CTA: online softmax over r rows in chunks of kDenseChunk (scores in
+// shared memory), record (m, l, 0, 0, acc[d]) in float64.
+constexpr int kDenseChunk = 1024, kDenseThreads = 256;
+__global__ void __launch_bounds__(kDenseThreads)
+    dense_partial_f64_kernel(const double *__restrict__ q, const double *__restrict__ K,
+                             const double *__restrict__ V, int64_t r, int d, double scale,
+                             double *__restrict__ rec) {
+    __shared__ double sc[kDenseChunk];
+    __shared__ double red[kDenseThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double m = -INFINITY, l = 0.0;
+    constexpr int kAcc = 1024 / kDenseThreads;  // d <= 1024
+    double acc[kAcc];
+#pragma unroll
+    for (int k = 0; k < kAcc; ++k) acc[k] = 0.0;
+    for (int64_t t0 = 0; t0 < r; t0 += kDenseChunk) {
+        const int cnt = (int)min((int64_t)kDenseChunk, r - t0);
+        __syncthreads();
+        for (int t = warp; t < cnt; t += kDenseThreads / 32) {  // warp per row
+            double dot = 0.0;
+            for (int j = lane; j < d; j += 32) dot += K[(t0 + t) * d + j] * q[j];
+            for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+            if (lane == 0) sc[t] = scale * dot;
+        }
+        __syncthreads();
+        double mc = -INFINITY;
+        for (int t = tid; t < cnt; t += kDenseThreads) mc = fmax(mc, sc[t]);
+        for (int off = 16; off > 0; off >>= 1) mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+        if (lane == 0) red[warp] = mc;
+        __syncthreads();
+        mc = red[0];
+        for (int w = 1; w < kDenseThreads / 32; ++w) mc = fmax(mc, red[w]);
+        const double mn = fmax(m, mc);
+        const double f = (m == -INFINITY) ? 0.0 : exp(m - mn);
+        l *= f;
+#pragma unroll
+        for (int k = 0; k < kAcc; ++k) acc[k] *= f;
+        m = mn;
+        double ls = 0.0;
+        for (int t = 0; t < cnt; ++t) {
+            const double p = exp(sc[t] - m);
+            ls += p;
+#pragma unroll
+            for (int k = 0; k < kAcc; ++k) {
+                const int j = tid + k * kDenseThreads;
+                if (j < d) acc[k] += p * V[(t0 + t) * d + j];
+            }
+        }
+        l += ls;
+    }
+#pragma unroll
+    for (int k = 0; k < kAcc; ++k) {
+        const int j = tid + k * kDenseThreads;
+        if (j < d) rec[4 + j] = acc[k];
+    }
+    if (tid == 0) {
+        rec[0] = m;
+        rec[1] = l;
+        rec[2] = 0.0;
+        rec[3] = 0.0;
+    }
+}
+
 // Test-only: lets the next PDL launch start at once, waits ns, then writes v
 // to p[0..n) -- a length update the dependent kernel can only see after its
 // griddepcontrol.wait (exercises the early_codes re-validation).
@@ -354,4 +435,26 @@ extern "C" int pqkv_accumulate_mass_f64(const void *codes, const double *p, int6
         accumulate_mass_f64_kernel<uint16_t><<<grid, 256, 0, as_stream(stream)>>>(
             (const uint16_t *)codes, p, n, M, ksub, h);
     return launch_status("pqkv_accumulate_mass_f64");
+}
+
+extern "C" int pqkv_build_lut_f64(const double *q, int64_t n_heads, int d, const float *cb_k,
+                                  int M, int nbits, double scale, double *out, void *stream) {
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits) && n_heads >= 0 && n_heads < 65536,
+                   "pqkv_build_lut_f64: bad arguments");
+    if (n_heads == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(q && cb_k && out, "pqkv_build_lut_f64: null pointer");
+    const int64_t cells = (int64_t)M << nbits;
+    dim3 grid((unsigned)((cells + 255) / 256), (unsigned)n_heads);
+    build_lut_f64_kernel<<<grid, 256, 0, as_stream(stream)>>>(q, d, cb_k, M, 1 << nbits, scale,
+                                                              out);
+    return launch_status("pqkv_build_lut_f64");
+}
+
+extern "C" int pqkv_dense_partial_f64(const double *q, const double *K, const double *V,
+                                      int64_t r, int d, double scale, double *rec, void *stream) {
+    PQKV_CHECK_ARG(r >= 1 && d >= 1 && d <= 1024, "pqkv_dense_partial_f64: bad sizes");
+    PQKV_CHECK_ARG(q && K && V && rec, "pqkv_dense_partial_f64: null pointer");
+    dense_partial_f64_kernel<<<1, kDenseThreads, 0, as_stream(stream)>>>(q, K, V, r, d, scale,
+                                                                         rec);
+    return launch_status("pqkv_dense_partial_f64");
 }

@@ -132,6 +132,8 @@ def reconstruct(codes: torch.Tensor, centroids: torch.Tensor, nbits: int, stream
     M, ksub, dsub = centroids.shape
     n = codes.shape[0]
     out = torch.empty((n, M * dsub), dtype=torch.float32, device=codes.device)
+    if n == 0:
+        return out
     if codes.stride(1) != 1:
         codes = codes.contiguous()
     _call(codes.device, "pqkv_reconstruct", N.ptr(codes), n, codes.stride(0), N.ptr(_contig(centroids)),
@@ -151,6 +153,34 @@ def build_lut(q: torch.Tensor, cb_k: torch.Tensor, nbits: int, scale: float,
     _call(q.device, "pqkv_build_lut", N.ptr(q), H, M * dsub, N.ptr(_contig(cb_k)), M, nbits, float(scale),
            N.ptr(out), N.stream_ptr(stream, q.device))
     return out
+
+
+def build_lut_f64(q: torch.Tensor, cb_k: torch.Tensor, nbits: int, scale: float,
+                  out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """(H, d) float64 queries -> (H, M, ksub) float64 tables (the reference's
+    Lut.table layout, build_key_lut attention.py:70-83)."""
+    _dev_check(q, cb_k)
+    M, ksub, dsub = cb_k.shape
+    q = _contig(q.double().reshape(-1, M * dsub))
+    H = q.shape[0]
+    if out is None:
+        out = torch.empty((H, M, ksub), dtype=torch.float64, device=q.device)
+    _call(q.device, "pqkv_build_lut_f64", N.ptr(q), H, M * dsub, N.ptr(_contig(cb_k.float())), M,
+          nbits, float(scale), N.ptr(out), N.stream_ptr(stream, q.device))
+    return out
+
+
+def dense_partial_f64(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, scale: float,
+                      stream=None) -> torch.Tensor:
+    """float64 (m, l, 0, 0, acc[d]) record of softmax(scale q K^T) over the
+    rows of K, V (dense_partial, attention.py:169-190)."""
+    _dev_check(q, K, V)
+    d = q.shape[-1]
+    q, K, V = _contig(q.double().reshape(d)), _contig(K.double()), _contig(V.double())
+    rec = torch.empty(d + 4, dtype=torch.float64, device=q.device)
+    _call(q.device, "pqkv_dense_partial_f64", N.ptr(q), N.ptr(K), N.ptr(V), K.shape[0], d,
+          float(scale), N.ptr(rec), N.stream_ptr(stream, q.device))
+    return rec
 
 
 def is_fast_geometry(d: int, M: int, nbits: int) -> bool:

@@ -44,11 +44,11 @@ if os.environ.get("GRAPH") == "1":  # replay a captured step (trace ids are bake
         step()
     gr.replay(); gr.replay()
 torch.cuda.synchronize()
-T = np.zeros(64 * 256 * 16, dtype=np.uint64)
+T = np.zeros(64 * 256 * 32, dtype=np.uint64)
 N.load().pqkv_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert N.load().pqkv_debug_trace(T.ctypes.data, T.size) == 0
 sl = slice(0, 32) if os.environ.get("GRAPH") == "1" else slice(32, 64)
-T = T.reshape(64, 256, 16)[sl, :dec.ws.num_ctas].astype(np.int64)
+T = T.reshape(64, 256, 32)[sl, :dec.ws.num_ctas].astype(np.int64)
 t0 = T[0, :, 1].min()
 rel = lambda c: (c - t0) / 1e3
 print(f"{'layer':>5} {'first_in':>8} {'last_in':>8} {'post_wait':>9} {'ready_med':>9} {'ready_max':>9} "
@@ -65,11 +65,26 @@ print(f"32 layers: {span:.1f} us -> {span/32:.2f} us/layer")
 ready = (T[:, :, 2] - T[:, :, 1]) / 1e3
 loop = (T[:, :, 6] - T[:, :, 2]) / 1e3
 fin = (T[:, :, 4] - T[:, :, 6]) / 1e3
-for name, c in (("post_wait", 7), ("cost_map", 10), ("lut_pre", 8), ("ring_issued", 11), ("sync1", 12), ("dense", 13), ("cv_ready", 9), ("ready", 2)):
+for name, c in (("post_wait", 7),):
     v = np.median((T[4:, :, c] - T[4:, :, 7].min(axis=1, keepdims=True)) / 1e3)
-    print(f"  {name:10s} median {v:6.2f} us after the layer's first post-wait")
+    print(f"  {name:10s} median {v:6.2f} us after the layer's first post-wait (globaltimer)")
+for name, c in (("ring_issued", 10), ("seg_ring", 11), ("sync1", 12), ("lut_built", 8),
+                ("dense", 13), ("cv_ready", 9), ("loop_start", 16)):
+    v = T[4:, :, c] / 1965.0
+    print(f"  {name:10s} median {np.median(v):6.2f} us, p90 {np.percentile(v, 90):6.2f} us after the CTA's post-wait (clock64)")
 print(f"per CTA (median over layers/CTAs): entry->ready {np.median(ready):.2f} us, ready->segs_done {np.median(loop):.2f} us, segs_done->exit {np.median(fin):.2f} us")
 np.save(os.path.join(ROOT, "gpurun_out", "trace_graph.npy"), T)
+# arrival / merge (clock64 cycles after segs_done, 1965 MHz), group 0's first segment
+arr, fin = T[4:, :, 14] / 1965.0, T[4:, :, 15] / 1965.0
+last = fin > 0
+print(f"arrival after segs_done: median {np.median(arr):.2f} us, p90 {np.percentile(arr, 90):.2f}")
+if last.any():
+    print(f"last-arriver merge end after segs_done: median {np.median(fin[last]):.2f} us, "
+          f"p90 {np.percentile(fin[last], 90):.2f}")
+ex = T[4:, :, 4]
+lc = ex.argmax(axis=1)
+print("layer-last CTA: arrival %.2f us, merge end %.2f us (medians over layers)" % (
+    np.median(arr[np.arange(len(lc)), lc]), np.median(fin[np.arange(len(lc)), lc])))
 # per-warp main-loop end (first segment): spread within each CTA
 Wt = np.zeros(64 * 256 * 32, dtype=np.uint64)
 N.load().pqkv_debug_wtrace.argtypes = [ctypes.c_void_p, ctypes.c_int]
