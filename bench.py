@@ -443,6 +443,7 @@ class Workload:
         # are not written by the kernel a launch overlaps: PDL may read them
         # early (n_q itself is re-validated after the wait)
         self.dec = PQDecoder(B, Hq, Hkv, PQConfig(D, M, NBITS), device=dev,
+                             num_ctas=int(os.environ.get("PQKV_BENCH_CTAS", "0")) or None,
                              pdl=not args.no_pdl, static_codebooks=not args.no_pdl,
                              early_codes=not args.no_pdl)
         if not args.no_l2_persist:

@@ -56,7 +56,9 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB,
         return lib
     out_dir = os.path.dirname(os.path.abspath(lib))
     os.makedirs(out_dir, exist_ok=True)
-    tag = "_".join(defines)
+    # object names unique per output library, so parallel builds of variants
+    # into one directory do not collide
+    tag = "_" + os.path.basename(lib).replace(".", "_") + "_".join(defines)
     objs, procs = [], []
     try:
         # the translation units compile in parallel (decode.cu dominates)
