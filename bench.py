@@ -472,19 +472,20 @@ class Workload:
             self.dec(self.q[l], self.codes_k[l], self.codes_v[l], self.n_q, self.cbk[l], cbv[l],
                      self.rk[l], self.rv[l], self.n_r, self.kc[l], self.vc[l], out=self.out[l])
 
-    def step_fn(self, half=False):
+    def step_fn(self, half=False, keys16=False):
         cbv = self.cbv16 if half else self.cbv32
+        self.dec.f16_key_table = keys16  # baked into the captured launches
 
         def step():
             for l in range(self.L):
                 self.layer(l, cbv)
         return step
 
-    def capture(self, half=False):
+    def capture(self, half=False, keys16=False):
         """the step captured in a CUDA graph (replay); if capturing the NCCL
         all-gather of a sequence split fails, the step runs eagerly"""
         import torch
-        step = self.step_fn(half)
+        step = self.step_fn(half, keys16)
         with torch.cuda.stream(self.stream):
             step()
             step()
@@ -751,6 +752,18 @@ def run_ours(args):
                             "(tests/test_gpu_parity.py::test_f16_value_codebook_mode, "
                             "tests/test_gpu_full_shapes.py)"}
         del r16
+        if Hq // Hkv >= 2 and (Hq // Hkv) % 2 == 0:
+            # GQA: + the two heads' key tables as one half2 table
+            r16k = w.capture(True, keys16=True)
+            ms16k = w.time(r16k, args.steps, args.warmup, barrier, max_over_ranks)
+            f16["f16_key_table"] = {
+                "value": jobs * B * 1e3 / ms16k, "unit": "tokens/s", "ms_per_step": ms16k,
+                "roofline_frac": bytes_per_launch / ((ms16k - merge_ms) / L * 1e-3) / 1e9
+                / hbm_peak,
+                "tolerance": "rtol 2e-3, atol 2e-4 vs the fp64 reference "
+                             "(tests/test_gpu_gqa_tables.py)"}
+            del r16k
+            w.dec.f16_key_table = False
 
     enc = None if (args.no_encode or world > 1) else encode_rate(dev, L, Hkv, n, stream)
     if enc is not None:

@@ -199,6 +199,12 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              keep one query head per CTA (by default a CTA
                              serves two query heads of a KV head and shares
                              the value gathers) */
+#define PQKV_DECODE_F16_KEY_TABLE 32 /* with PQKV_DECODE_F16_VALUE_CODEBOOK
+                             and an even GQA group: the two query heads a
+                             CTA serves keep one half2 key table (entry
+                             (c, i) = both heads' scores in fp16), one 4-byte
+                             gather per key code for both heads; scores are
+                             summed in fp32.  Ignored otherwise. */
 #define PQKV_DECODE_EARLY_CODES 8 /* the codes below n_q were written before
                              the previous kernel on the stream started (the
                              codes of a decode step are appended by an

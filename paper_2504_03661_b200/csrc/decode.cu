@@ -326,20 +326,42 @@ struct SlotState {
     unsigned long long acc[HG][SPL];  // float2 per (rotated) subspace of this lane's share
 };
 
-template <int HG>
+// sp0 += lo half of h2, sp1 += hi half (mixed f32 + f16 adds: FHADD)
+__device__ __forceinline__ void fhadd2(float &sp0, float &sp1, uint32_t h2) {
+    asm("{\n.reg .f16 lo, hi;\nmov.b32 {lo, hi}, %2;\n"
+        "add.rn.f32.f16 %0, lo, %0;\nadd.rn.f32.f16 %1, hi, %1;\n}"
+        : "+f"(sp0), "+f"(sp1)
+        : "r"(h2));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(0x400));
+    return v;
+}
+
+// kHalfLut (HG = 2): the two heads' tables are one half2 table, entry (c, i) =
+// (head 0, head 1) in fp16 -- one 4-byte gather per code byte for both heads
+template <int HG, bool kHalfLut = false>
 __device__ __forceinline__ void lut_score(const CodeVec k, const uint32_t (&packK)[NPK],
                                           float (&out)[HG]) {
     float sp[HG][4];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
         const uint32_t a = __byte_perm(cword(k, j >> 2), packK[j >> 1], sel_for(j));
+        if constexpr (kHalfLut) {
+            static_assert(HG == 2, "the packed table holds two heads");
+            const uint32_t x = lds_u32(a);
+            if (j < 4) sp[0][j] = sp[1][j] = 0.f;
+            fhadd2(sp[0][j & 3], sp[1][j & 3], x);
+        } else {
 #pragma unroll
-        for (int h = 0; h < HG; ++h) {
-            const float x = h == 0 ? lds_f32<0x400>(a) : lds_f32<0x10400>(a);
-            if (j < 4)
-                sp[h][j] = x;
-            else
-                sp[h][j & 3] += x;
+            for (int h = 0; h < HG; ++h) {
+                const float x = h == 0 ? lds_f32<0x400>(a) : lds_f32<0x10400>(a);
+                if (j < 4)
+                    sp[h][j] = x;
+                else
+                    sp[h][j & 3] += x;
+            }
         }
     }
 #pragma unroll
@@ -354,7 +376,7 @@ __device__ __forceinline__ void lut_score(const CodeVec k, const uint32_t (&pack
 // increase branches.
 // after_keys() runs once the key codes are consumed (the ring refills the key
 // registers there, half a unit earlier than the value registers).
-template <bool kHalfCV, int NU, int HG, typename AfterKeys>
+template <bool kHalfCV, int NU, int HG, bool kHalfLut, typename AfterKeys>
 __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
                                               const uint32_t (&packK)[NPK],
                                               const uint32_t (&packV)[NPK], const bool *okA,
@@ -362,8 +384,8 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
     float sa[NU][HG], sb[NU][HG];
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
-        lut_score<HG>(U[n].ka, packK, sa[n]);
-        lut_score<HG>(U[n].kb, packK, sb[n]);
+        lut_score<HG, kHalfLut>(U[n].ka, packK, sa[n]);
+        lut_score<HG, kHalfLut>(U[n].kb, packK, sb[n]);
     }
 #pragma unroll
     for (int off = 1; off < TL; off <<= 1)  // the TL lanes of a token
@@ -576,6 +598,29 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[lut_i
     }
 }
 
+// the two heads' tables as one half2 table (kHalfLut): entry (c, i) = (head 0,
+// head 1) rounded to fp16, the same 4-byte slots as one fp32 table
+template <int NT>
+__device__ __forceinline__ void lut_build_packed(uint32_t *lut_s, const float4 (&cc)[lut_iters<NT>()],
+                                                 const float *q0, const float *q1, float scale,
+                                                 int tid) {
+    constexpr int kLutIters = lut_iters<NT>();
+    const float4 qa = __ldg(reinterpret_cast<const float4 *>(q0) + (tid & 31));
+    const float4 qb = __ldg(reinterpret_cast<const float4 *>(q1) + (tid & 31));
+#pragma unroll
+    for (int k = 0; k < kLutIters; ++k) {
+        if (kLutSlots % NT != 0 && tid + k * NT >= kLutSlots) break;
+        const float a0 = scale * fmaf(qa.y, cc[k].y, qa.x * cc[k].x);
+        const float a1 = scale * fmaf(qa.w, cc[k].w, qa.z * cc[k].z);
+        const float b0 = scale * fmaf(qb.y, cc[k].y, qb.x * cc[k].x);
+        const float b1 = scale * fmaf(qb.w, cc[k].w, qb.z * cc[k].z);
+        uint2 o;
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.x) : "f"(b0), "f"(a0));  // lo = head 0
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.y) : "f"(b1), "f"(a1));
+        reinterpret_cast<uint2 *>(lut_s)[tid + k * NT] = o;
+    }
+}
+
 // kLutFromQ: build each head's LUT in shared memory from q and the
 // centroid-major key codebook ([256][64] float2, pqkv_prepare_key_codebook);
 // otherwise copy a precomputed [B*Hq][256][64] LUT (the Lut-taking API).
@@ -583,9 +628,11 @@ __device__ __forceinline__ void lut_build(float *lut_s, const float4 (&cc)[lut_i
 // of one KV head -- a "virtual head" -- with two key tables (one PRMT per
 // code byte feeds both) and one value gather per code shared by both heads.
 // W warps per CTA.
-template <bool kLutFromQ, bool kHalfCV, int HG, int W, int GROUP>
+template <bool kLutFromQ, bool kHalfCV, int HG, int W, int GROUP, bool kHalfLut = false>
 __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A) {
     static_assert(RING % GROUP == 0, "the ring holds whole groups");
+    static_assert(!kHalfLut || (HG == 2 && kHalfCV && kLutFromQ),
+                  "packed fp16 key tables: two heads per CTA in the fp16 mode");
     static_assert(HG == 1 || (HG == 2 && kHalfCV && kLutFromQ), "two heads need the fp16 codebook");
     static_assert(W <= PQKV_WARPS_MAX, "the shared-memory map is sized for PQKV_WARPS_MAX warps");
     constexpr int WARPS = W, NT = W * 32, NG = NT / 128;
@@ -792,10 +839,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
         if (kLutFromQ) {
             float4 cc[lut_iters<NT>()];
             lut_load<NT>(cc, A.ck, tid);
+            if constexpr (kHalfLut) {
+                lut_build_packed<NT>(reinterpret_cast<uint32_t *>(lut_s), cc,
+                                     A.q + (int64_t)bh0 * D, A.q + (int64_t)(bh0 + 1) * D,
+                                     A.scale, tid);
+            } else {
 #pragma unroll
-            for (int h = 0; h < HG; ++h)
-                lut_build<NT>(lut_s + h * (LUT_BYTES / 4), cc, A.q + (int64_t)(bh0 + h) * D,
-                              A.scale, tid);
+                for (int h = 0; h < HG; ++h)
+                    lut_build<NT>(lut_s + h * (LUT_BYTES / 4), cc, A.q + (int64_t)(bh0 + h) * D,
+                                  A.scale, tid);
+            }
 #ifdef PQKV_TRACE
             if (nseg_ == 0) PQKV_TRC(8);  // first table built
 #endif
@@ -924,7 +977,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                 if constexpr (!kHalfCV && PQKV_EARLY_KEYS) {
                     // exact path: refill the key registers as soon as the key
                     // phase consumed them (measured +1%; the fp16 variants spill)
-                    process_units<kHalfCV, GROUP, HG>(
+                    process_units<kHalfCV, GROUP, HG, kHalfLut>(
                         Ur + g * GROUP, S, packK, packV, okA, okB, [&]() {
 #pragma unroll
                             for (int n = 0; n < GROUP; ++n)
@@ -936,7 +989,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                         load_values_at(Ur[g * GROUP + n], kp + n * kStep + dv,
                                        tn + n * WARPS * UT, lo, hi);
                 } else {
-                    process_units<kHalfCV, GROUP, HG>(Ur + g * GROUP, S, packK, packV, okA, okB,
+                    process_units<kHalfCV, GROUP, HG, kHalfLut>(Ur + g * GROUP, S, packK, packV, okA, okB,
                                                       []() {});
 #pragma unroll
                     for (int n = 0; n < GROUP; ++n) {
@@ -959,7 +1012,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
             const int ta = u * UT + slot;
             okA[0] = ta >= lo && ta < hi;
             okB[0] = ta + TS >= lo && ta + TS < hi;
-            process_units<kHalfCV, 1, HG>(Ur, S, packK, packV, okA, okB, []() {});
+            process_units<kHalfCV, 1, HG, kHalfLut>(Ur, S, packK, packV, okA, okB, []() {});
         }
 
         // ---- epilogue: one (m, l, acc) record for this (CTA, head) segment
@@ -1499,12 +1552,12 @@ static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int 
 #define PQKV_GQA2_GROUP 2
 #endif
 template <bool kLutFromQ, bool kHalfCV = false, int HG = 1, int W = fast::WARPS,
-          int GROUP = fast::GROUP>
+          int GROUP = fast::GROUP, bool kHalfLut = false>
 static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
     static int attr_set[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV, HG, W, GROUP>;
+    auto kern = fast::decode_partials_m64b8<kLutFromQ, kHalfCV, HG, W, GROUP, kHalfLut>;
     if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              fast::SMEM_BYTES);
@@ -1651,7 +1704,7 @@ extern "C" int pqkv_decode_attention(
                    "pqkv_decode_attention: recent_k and recent_v go together");
     PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
                               PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES |
-                              PQKV_DECODE_ONE_HEAD_PER_CTA)) == 0,
+                              PQKV_DECODE_ONE_HEAD_PER_CTA | PQKV_DECODE_F16_KEY_TABLE)) == 0,
                    "pqkv_decode_attention: unknown flags");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
@@ -1695,9 +1748,13 @@ extern "C" int pqkv_decode_attention(
     }
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
         // even GQA groups: one CTA serves two query heads of a KV head
-        if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA))
+        if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA)) {
+            if (flags & PQKV_DECODE_F16_KEY_TABLE)
+                return launch_fast<true, true, 2, PQKV_GQA2_WARPS, PQKV_GQA2_GROUP, true>(
+                    a, pdl, st, "pqkv_decode_attention");
             return launch_fast<true, true, 2, PQKV_GQA2_WARPS, PQKV_GQA2_GROUP>(
                 a, pdl, st, "pqkv_decode_attention");
+        }
         return launch_fast<true, true, 1, PQKV_F16_WARPS, PQKV_F16_GROUP>(a, pdl, st,
                                                                           "pqkv_decode_attention");
     }

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
         const float trunc = __uint_as_float(0x3f800000u | cmask) - 1.f;  // ksub * 2^-23
         const float tol = (2e-6f + 2.f * trunc) * d1 + 1e-13f * (xx + ccmax) + 1e-30f;
         int a = (int)(b1[k] & cmask);
-        if (!(d2k > d1 + tol)) {  // near tie: the exact scan        if (!(b2[k] > b1[k] + tol)) {  // near tie: the exact scan
+        if (!(d2k > d1 + tol)) {  // near tie: the exact scan
             const double x0 = (double)xf0[k], x1 = (double)xf1[k];
             const double xxd = __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1));
             double best = INFINITY;

@@ -40,7 +40,7 @@ class PQDecoder:
 
     def __init__(self, B: int, Hq: int, Hkv: int, config: PQConfig, device=None,
                  num_ctas: int | None = None, pdl: bool = False, static_codebooks: bool = False,
-                 early_codes: bool = False):
+                 early_codes: bool = False, f16_key_table: bool = False):
         if Hq % Hkv:
             raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
         self.B, self.Hq, self.Hkv, self.config = B, Hq, Hkv, config
@@ -48,6 +48,8 @@ class PQDecoder:
                                     num_ctas=num_ctas)
         self.device = self.ws.device
         self.pdl, self.static_codebooks, self.early_codes = pdl, static_codebooks, early_codes
+        # stated-tolerance GQA mode (with an fp16 value codebook layout)
+        self.f16_key_table = f16_key_table
 
     @property
     def num_ctas(self) -> int:
@@ -73,7 +75,7 @@ class PQDecoder:
                            codes_v, n_q, cb_v_layout, recent_k=recent_k, recent_v=recent_v,
                            n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
                            merged=merged, pdl=self.pdl, static_codebooks=self.static_codebooks,
-                           early_codes=self.early_codes,
+                           early_codes=self.early_codes, f16_key_table=self.f16_key_table,
                            stream=stream)
         return out
 

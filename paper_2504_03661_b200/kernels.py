@@ -312,7 +312,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
                      codes_v, n_q, cb_v_layout, recent_k=None, recent_v=None, n_recent=None,
                      k_cur=None, v_cur=None, out=None, lse=None, merged=None, pdl: bool = False,
                      static_codebooks: bool = False, early_codes: bool = False,
-                     one_head_per_cta: bool = False, stream=None) -> None:
+                     one_head_per_cta: bool = False, f16_key_table: bool = False,
+                     stream=None) -> None:
     """One fused launch per layer (m64b8): quantized span + dense window +
     fixed-order merge + finalize for every (b, hq); other geometries fall back
     to decode_partials + decode_finish inside the library.
@@ -323,7 +324,10 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
     the value codebook before waiting for it (the codebooks must then have
     been written before the previous kernel started, e.g. at load time);
     early_codes likewise for n_q and the codes below it (appended by earlier
-    steps): the work split and the first code loads then precede the wait."""
+    steps): the work split and the first code loads then precede the wait.
+    f16_key_table (with the fp16 value codebook and an even GQA group): the
+    two query heads of a CTA share one half2 key table (stated tolerance,
+    tests/test_gpu_gqa_tables.py)."""
     _check_codes(ws, Hkv, codes_k, codes_v)
     ld_recent = 0
     if recent_k is not None:
@@ -335,6 +339,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
         flags |= N.DECODE_EARLY_CODES
     if one_head_per_cta:
         flags |= N.DECODE_ONE_HEAD_PER_CTA
+    if f16_key_table:
+        flags |= N.DECODE_F16_KEY_TABLE
     if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
         flags |= N.DECODE_F16_VALUE_CODEBOOK
     _call(codes_k.device, "pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),

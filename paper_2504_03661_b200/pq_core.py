@@ -6,8 +6,10 @@ reconstruct :290-304, bits_per_value :307-309) with the same names, argument
 meaning and errors.  Arrays may be numpy arrays (results come back as numpy,
 like the reference) or CUDA tensors (results stay on the device, nothing
 synchronises).  The arithmetic always runs in libpqkv_sm100.so; there is no
-CPU path.  Offline k-means training and the integer-quantization baseline are
-out of scope.
+CPU path.  The reference's training names (``kmeans_train``,
+``train_codebooks``) are re-exported from ``training.py`` (k-means++ / Lloyd,
+offline) and its integer-quantization baseline from
+``baselines.py``.
 """
 
 from __future__ import annotations

@@ -1,7 +1,8 @@
 """Parity at BASELINE's full GQA shapes and on the serving loop's launch flags.
 
 * config 3 (Llama-3-8B GQA 32:8, B=16, 32K) and config 4 (B=4, 128K): one
-  whole layer through the fused launch, exact and fp16 value-codebook modes,
+  whole layer through the fused launch, exact and fp16 value-codebook modes
+  (the latter also with the packed fp16 key tables),
   against the fp64 C restatement of the reference run per query head
   (snapshot -> build_key_lut -> quantized / dense partials -> merge ->
   finalize; reference attention.py:114-166, :214-287);
@@ -98,6 +99,9 @@ def test_full_gqa_layer_vs_c_oracle(cfg):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
     got16 = _decode(x, 32, 8, half=True)
     np.testing.assert_allclose(got16, want, rtol=RTOL16, atol=ATOL16)
+    # + the two query heads' key tables of a CTA as one half2 table
+    got16k = _decode(x, 32, 8, half=True, f16_key_table=True)
+    np.testing.assert_allclose(got16k, want, rtol=RTOL16, atol=ATOL16)
 
 
 def test_config4_eight_way_split_equals_unsplit():
