@@ -332,6 +332,25 @@ int pqkv_read_cache_dumps(const char *path, int heads, int d, int M, int nbits,
 int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns,
                             void *stream);
 
+/* ---- paged code store (growth without copies) ---------------------------
+ * Replaces the reference's grow-by-copy code store (kv_cache.py:74-76,
+ * 217-228).  A store reserves n_regions * region_bytes of virtual address
+ * space (region_bytes rounded up to the allocation granularity); region r
+ * starts at base + r * region_bytes.  pqkv_vstore_ensure(bytes) maps physical
+ * pages (CUDA VMM: cuMemCreate / cuMemMap, geometric growth) so that every
+ * region has at least `bytes` mapped; mapped pages never move, so a head's
+ * codes stay one contiguous run for the decode kernel (ld_tok = region_bytes
+ * / row bytes) and the store grows without copying.  Pages are not zeroed.
+ * pqkv_vstore_destroy synchronises the device, unmaps and frees. */
+typedef struct pqkv_vstore pqkv_vstore;
+int64_t pqkv_vstore_granularity(int device);
+int pqkv_vstore_create(int device, int64_t n_regions, int64_t region_bytes,
+                       pqkv_vstore **out, void **base);
+int pqkv_vstore_ensure(pqkv_vstore *vs, int64_t bytes);
+int64_t pqkv_vstore_mapped(const pqkv_vstore *vs);
+int64_t pqkv_vstore_region_bytes(const pqkv_vstore *vs);
+int pqkv_vstore_destroy(pqkv_vstore *vs);
+
 #ifdef __cplusplus
 }
 #endif

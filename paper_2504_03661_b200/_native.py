@@ -69,6 +69,12 @@ SIGNATURES = {
     "pqkv_read_cache_dumps": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _I64, _I, _P, _P, _I64, _I,
                                    _P, _P, _I64, _P]),
     "pqkv_debug_delayed_fill": (_I, [_P, _I, _I, ctypes.c_longlong, _P]),
+    "pqkv_vstore_granularity": (_I64, [_I]),
+    "pqkv_vstore_create": (_I, [_I, _I64, _I64, _P, _P]),
+    "pqkv_vstore_ensure": (_I, [_P, _I64]),
+    "pqkv_vstore_mapped": (_I64, [_P]),
+    "pqkv_vstore_region_bytes": (_I64, [_P]),
+    "pqkv_vstore_destroy": (_I, [_P]),
 }
 
 _lib = None

@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libpqkv_sm100.so")
-SOURCES = ["tables.cu", "encode.cu", "decode.cu", "fileio.cu"]
+SOURCES = ["tables.cu", "encode.cu", "decode.cu", "fileio.cu", "vstore.cu"]
 HEADERS = ["common.cuh"]
 
 NVCC_FLAGS = [

@@ -76,9 +76,9 @@ class LayerKVCache:
                                                       cb_K.config.nbits) else "rows"
         self.device = torch.device(device) if device is not None else default_device()
         cfg = self.config
-        cap = 1024
-        self._store_k = torch.zeros((cap, cfg.M), dtype=cfg.torch_code_dtype, device=self.device)
-        self._store_v = torch.zeros_like(self._store_k)
+        # paged code store (vstore.py): K and V rows in two regions of one
+        # virtual reservation, pages mapped as the rows grow -- no copies
+        self._new_store(self.DEFAULT_MAX_ROWS)
         self._n_q = 0
         rcap = max(64, 2 * (recent_capacity + flush_threshold))
         self._rk = torch.zeros((rcap, cfg.d), dtype=torch.float32, device=self.device)
@@ -119,17 +119,27 @@ class LayerKVCache:
         return self._rlen - self._pending_rows >= self.flush_threshold
 
     # -- storage helpers ---------------------------------------------------
+    DEFAULT_MAX_ROWS = 1 << 24  # virtual row capacity per kind (address space only)
+
+    def _new_store(self, max_rows: int) -> None:
+        from .vstore import PagedCodeStore
+        self._store = PagedCodeStore(2, max_rows, (self.config.M,),
+                                     self.config.torch_code_dtype, self.device)
+        self._store_k, self._store_v = self._store.tensor[0], self._store.tensor[1]
+
     def _ensure_store(self, n_new: int) -> None:
-        cap = self._store_k.shape[0]
-        if n_new <= cap:
+        """Map pages for n_new rows (the reference doubles and copies,
+        kv_cache.py:217-228; here rows never move).  Past the reservation
+        (16 Mi rows) the store moves once into a larger one."""
+        if n_new <= self._store.max_rows:
+            self._store.ensure(n_new)
             return
         self._wait_pending()
-        cap = max(n_new, 2 * cap)
-        gk = torch.zeros((cap, self.config.M), dtype=self._store_k.dtype, device=self.device)
-        gv = torch.zeros_like(gk)
-        gk[: self._n_q] = self._store_k[: self._n_q]
-        gv[: self._n_q] = self._store_v[: self._n_q]
-        self._store_k, self._store_v = gk, gv
+        old_k, old_v, n = self._store_k, self._store_v, self._n_q
+        self._new_store(max(n_new, 2 * self._store.max_rows))
+        self._store.ensure(n_new)
+        self._store_k[:n] = old_k[:n]
+        self._store_v[:n] = old_v[:n]
 
     def _ensure_recent(self, extra: int) -> None:
         cap = self._rk.shape[0]

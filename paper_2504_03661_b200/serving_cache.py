@@ -6,7 +6,8 @@ and KV head of a model in a few HBM tensors laid out for the fused decode
 launch, with the reference's semantics per (layer, sequence, head):
 
 * quantized span: ``[L][B][Hkv][cap][M]`` uint8 in the decode layout
-  (common.cuh), written by the bit-exact encoder (``pqkv_encode``);
+  (common.cuh), written by the bit-exact encoder (``pqkv_encode``), in paged
+  stores (vstore.py: virtual reservation, pages mapped on growth, no copies);
 * full-precision recent rows ``[L][B][Hkv][R_cap][d]`` float32, rows
   ``[0, n_recent[b])`` live;
 * device lengths ``n_q[B]`` and ``n_recent[B]`` (one per sequence; every layer
@@ -49,7 +50,8 @@ class ServingCache:
                  centroids_v, capacity: int, recent_capacity: int = 32,
                  flush_threshold: int = 32, async_flush: bool = True, device=None):
         """centroids_k / centroids_v: per layer (M, ksub, dsub) float32 tensors
-        (or Codebooks).  capacity: quantized tokens per sequence."""
+        (or Codebooks).  capacity: maximum quantized tokens per sequence --
+        reserved address space; memory is mapped as the cache fills."""
         if not K.is_fast_geometry(config.d, config.M, config.nbits):
             raise ValueError("ServingCache stores the m64b8 decode layout (d=128, M=64, nbits=8)")
         if len(centroids_k) != layers or len(centroids_v) != layers:
@@ -57,7 +59,7 @@ class ServingCache:
         if recent_capacity < 0 or flush_threshold < 1:
             raise ValueError("recent_capacity >= 0 and flush_threshold >= 1 required")
         self.L, self.B, self.Hkv, self.config = layers, B, Hkv, config
-        self.capacity, self.R, self.R_f = capacity, recent_capacity, flush_threshold
+        self.R, self.R_f = recent_capacity, flush_threshold
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         dev, M, d = self.device, config.M, config.d
 
@@ -72,8 +74,19 @@ class ServingCache:
         # decode-kernel codebook layouts (static: prepared once, at load time)
         self.cb_k = [K.key_codebook_layout(c, config.nbits) for c in self.cents_k]
         self.cb_v = [K.value_codebook_layout(c, config.nbits) for c in self.cents_v]
-        self.codes_k = torch.zeros((layers, B, Hkv, capacity, M), dtype=torch.uint8, device=dev)
-        self.codes_v = torch.zeros_like(self.codes_k)
+        # paged code stores (vstore.py): one region of virtual address space
+        # per (layer, sequence, KV head) and kind, `capacity` rows each; pages
+        # are mapped as the cache fills, so capacity costs address space only
+        # and growth never copies (the decode kernel reads each head's rows
+        # as one contiguous run, ld_tok = the region's row capacity)
+        from .vstore import PagedCodeStore
+        self._stores = [PagedCodeStore(layers * B * Hkv, capacity, (M,), torch.uint8, dev)
+                        for _ in range(2)]
+        self.capacity = capacity
+        self.ld_tok = self._stores[0].max_rows  # row stride of a head: the reservation,
+                                                # rounded up to whole pages
+        self.codes_k = self._stores[0].tensor.view(layers, B, Hkv, self.ld_tok, M)
+        self.codes_v = self._stores[1].tensor.view(layers, B, Hkv, self.ld_tok, M)
         # recent rows: the live window plus one in-flight batch and one step
         self.R_cap = max(1, recent_capacity + 2 * flush_threshold + 1)
         self.recent_k = torch.zeros((layers, B, Hkv, self.R_cap, d), device=dev)
@@ -86,6 +99,15 @@ class ServingCache:
         self.async_flush = async_flush
         lo, _ = torch.cuda.Stream.priority_range()
         self._side = torch.cuda.Stream(device=dev, priority=lo) if async_flush else None
+
+    def ensure_rows(self, rows: int) -> None:
+        """Back `rows` code rows of every (layer, sequence, head) with pages."""
+        for st in self._stores:
+            st.ensure(max(rows, 1))
+
+    @property
+    def mapped_rows(self) -> int:
+        return self._stores[0].mapped_rows
 
     # -- views for PQDecoder --------------------------------------------------
     def layer(self, l: int) -> dict:
@@ -152,6 +174,7 @@ class ServingCache:
         n_enc = n - keep
         if n_enc > self.capacity:
             raise ValueError("prefill exceeds the code capacity")
+        self.ensure_rows(n_enc)
         if n_enc:
             self._encode_layers(K_rows[:, :, :, :n_enc].float().contiguous(),
                                 V_rows[:, :, :, :n_enc].float().contiguous(), 0)
@@ -203,6 +226,7 @@ class ServingCache:
         batch = self.R_f
         if self._nq + batch > self.capacity:
             raise RuntimeError("code capacity exhausted")
+        self.ensure_rows(self._nq + batch)
         main = torch.cuda.current_stream(self.device)
         rows_k = self.recent_k[:, :, :, :batch].clone()  # snapshot on the main stream
         rows_v = self.recent_v[:, :, :, :batch].clone()
