@@ -472,20 +472,21 @@ class Workload:
             self.dec(self.q[l], self.codes_k[l], self.codes_v[l], self.n_q, self.cbk[l], cbv[l],
                      self.rk[l], self.rv[l], self.n_r, self.kc[l], self.vc[l], out=self.out[l])
 
-    def step_fn(self, half=False, keys16=False):
+    def step_fn(self, half=False, keys16=False, pairs=False):
         cbv = self.cbv16 if half else self.cbv32
         self.dec.f16_key_table = keys16  # baked into the captured launches
+        self.dec.key_table_pairs = pairs
 
         def step():
             for l in range(self.L):
                 self.layer(l, cbv)
         return step
 
-    def capture(self, half=False, keys16=False):
+    def capture(self, half=False, keys16=False, pairs=False):
         """the step captured in a CUDA graph (replay); if capturing the NCCL
         all-gather of a sequence split fails, the step runs eagerly"""
         import torch
-        step = self.step_fn(half, keys16)
+        step = self.step_fn(half, keys16, pairs)
         with torch.cuda.stream(self.stream):
             step()
             step()
@@ -753,7 +754,7 @@ def run_ours(args):
                             "tests/test_gpu_full_shapes.py)"}
         del r16
         if Hq // Hkv >= 2 and (Hq // Hkv) % 2 == 0:
-            # GQA: + the two heads' key tables as one half2 table
+            # GQA: + the query heads of a CTA (four for groups of 4) share one packed fp16 key table
             r16k = w.capture(True, keys16=True)
             ms16k = w.time(r16k, args.steps, args.warmup, barrier, max_over_ranks)
             f16["f16_key_table"] = {
@@ -763,7 +764,15 @@ def run_ours(args):
                 "tolerance": "rtol 2e-3, atol 2e-4 vs the fp64 reference "
                              "(tests/test_gpu_gqa_tables.py)"}
             del r16k
+            if (Hq // Hkv) % 4 == 0:
+                # the same with two query heads per CTA (one half2 table per pair)
+                r16p = w.capture(True, keys16=True, pairs=True)
+                ms16p = w.time(r16p, args.steps, args.warmup, barrier, max_over_ranks)
+                f16["f16_key_table"]["two_heads_per_cta"] = {
+                    "value": jobs * B * 1e3 / ms16p, "unit": "tokens/s", "ms_per_step": ms16p}
+                del r16p
             w.dec.f16_key_table = False
+            w.dec.key_table_pairs = False
 
     enc = None if (args.no_encode or world > 1) else encode_rate(dev, L, Hkv, n, stream)
     if enc is not None:

@@ -200,11 +200,18 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              serves two query heads of a KV head and shares
                              the value gathers) */
 #define PQKV_DECODE_F16_KEY_TABLE 32 /* with PQKV_DECODE_F16_VALUE_CODEBOOK
-                             and an even GQA group: the two query heads a
-                             CTA serves keep one half2 key table (entry
-                             (c, i) = both heads' scores in fp16), one 4-byte
-                             gather per key code for both heads; scores are
-                             summed in fp32.  Ignored otherwise. */
+                             and an even GQA group: the query heads a CTA
+                             serves keep one packed fp16 key table (entry
+                             (c, i) = their scores in fp16), one gather per
+                             key code for all of them; scores are summed in
+                             fp32.  A group that is a multiple of 4: four
+                             query heads per CTA (8-byte entries, the value
+                             gathers shared by the four, fp32 weights);
+                             otherwise two (4-byte entries).  Ignored for
+                             odd groups. */
+#define PQKV_DECODE_KEY_TABLE_PAIRS 64 /* with PQKV_DECODE_F16_KEY_TABLE: two
+                             query heads per CTA even when the group is a
+                             multiple of 4 */
 #define PQKV_DECODE_EARLY_CODES 8 /* the codes below n_q were written before
                              the previous kernel on the stream started (the
                              codes of a decode step are appended by an

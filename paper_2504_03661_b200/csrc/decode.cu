@@ -1155,6 +1155,600 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
     PQKV_TR(5, nseg_);
 #endif
 }
+
+// ================================================ GQA: four heads per CTA ==
+// decode_gqa4_f16 -- PQKV_DECODE_F16_KEY_TABLE with a GQA group that is a
+// multiple of 4 (stated tolerance, as the fp16 value-codebook mode).  One CTA
+// serves four query heads of a KV head (a "virtual head"), so every key-code
+// gather feeds all four heads' scores and every value-code gather all four
+// heads' accumulators -- the per-query-head shared-memory work of the pair
+// kernel above (HG = 2, two CTAs per group of four) is shared once more.
+//   * shared memory: the four heads' key tables (build_key_lut,
+//     attention.py:70-83) as ONE fp16 table of 8-byte entries (h0, h1, h2,
+//     h3), laid out [half][256][32] (address half << 16 | code << 8 |
+//     (i & 31) << 3, 128 KiB), and the fp16 value codebook [256][2][32] half2
+//     (64 KiB, pqkv_prepare_value_codebook_f16);
+//   * lane = (slot s, eighth w), 8 lanes per token: the lane's 8 code bytes
+//     are bytes [8w, 8w + 8) of token A = 8u + {0,1,4,5}[s] and bytes
+//     [8(w^1), 8(w^1) + 8) of token B = A + 2.  On the stored decode layout
+//     (common.cuh) B's rotation is A's + 8 and its bytes sit 8 further into the
+//     quarter, so both tokens touch the same 8 subspaces at every step (one set
+//     of accumulators per lane), and a warp instruction touches 16 distinct
+//     subspaces mod 16 per half-warp (8-byte table gathers) and 32 distinct
+//     mod 32 (4-byte value gathers): bank-conflict free for ANY code values,
+//     with the MHA kernel's stored layout unchanged (scripts/check_gqa4_lanes.py);
+//   * the 8 lanes of a token reduce their four partial scores with a
+//     transposing butterfly (4 shuffles: each lane ends with one head's sum)
+//     and broadcast them back (3 shuffles);
+//   * scores in log2 units (the table entries carry log2(e)), so a weight is
+//     one FADD + EX2; the records' maxima are converted back to natural units;
+//   * value path: the half2 codebook entry is widened to float2 and feeds one
+//     FFMA2 per head with the fp32 weight (the pair kernel rounds the weights
+//     to fp16; here only the codebook and the table entries are rounded).
+namespace g4 {
+constexpr int HG = 4;
+constexpr int UT = 8;                          // tokens per warp per unit
+constexpr int TAB_BYTES = 2 * KSUB * 32 * 8;   // 131072: [half][256][32] x 8 B
+constexpr int CV16_BYTES = KSUB * 2 * 32 * 4;  // 65536: [256][2][32] half2
+constexpr int CV_IMM = 0x400 + TAB_BYTES;      // LDS immediate of the value codebook
+
+__device__ __forceinline__ int tau_a(int s) { return (s & 1) | ((s & 2) << 1); }  // 0 1 4 5
+
+// subspace of byte j of lane (s, w) -- for token A and, identically, token B
+__device__ __forceinline__ int lane_subspace(int s, int w, int j) {
+    const int q = w >> 1;
+    const int r = decode_lane_rot(4 * tau_a(s) + q);
+    return 16 * q + ((8 * (w & 1) + j + r) & 15);
+}
+
+struct Unit4 {
+    uint2 ka, kb, va, vb;
+};
+struct State4 {
+    float m[HG], l[HG];
+    unsigned long long acc[HG][8];  // float2 per subspace of this lane
+};
+
+__device__ __forceinline__ uint2 ld8(const uint8_t *p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint2 lds_tab(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(a), "n"(0x400));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_cv16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(CV_IMM));
+    return v;
+}
+// half2 -> float2 (packed in a 64-bit register pair for FFMA2)
+__device__ __forceinline__ unsigned long long widen(uint32_t h) {
+    unsigned long long r;
+    asm("{\n.reg .f16 lo, hi;\n.reg .f32 a, b;\nmov.b32 {lo, hi}, %1;\n"
+        "cvt.f32.f16 a, lo;\ncvt.f32.f16 b, hi;\nmov.b64 %0, {a, b};\n}"
+        : "=l"(r)
+        : "r"(h));
+    return r;
+}
+
+// unit u: tokens [8u, 8u + 8); lane takes A = 8u + tA (bytes 8w..) and B = A + 2
+// (bytes 8(w^1)..): B's code row pointer is A's + dB
+__device__ __forceinline__ void load_unit4(Unit4 &U, const uint8_t *kbase, const uint8_t *vbase,
+                                           int u, int tA, int dB, int lo, int hi) {
+    const int ta = u * UT + tA, tb = ta + 2;
+    const int64_t o = (int64_t)ta * M;
+    if (ta >= lo && ta < hi) {
+        U.ka = ld8(kbase + o);
+        U.va = ld8(vbase + o);
+    }
+    if (tb >= lo && tb < hi) {
+        U.kb = ld8(kbase + o + dB);
+        U.vb = ld8(vbase + o + dB);
+    }
+}
+
+// four heads' partial scores of one token from this lane's 8 key codes
+__device__ __forceinline__ void key_scores(const uint2 k, const uint32_t (&pk)[4],
+                                           float (&out)[HG]) {
+    float sp[HG][2] = {};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint2 e = lds_tab(__byte_perm(j < 4 ? k.x : k.y, pk[j >> 1], sel_for(j)));
+        fhadd2(sp[0][j & 1], sp[1][j & 1], e.x);
+        fhadd2(sp[2][j & 1], sp[3][j & 1], e.y);
+    }
+#pragma unroll
+    for (int h = 0; h < HG; ++h) out[h] = sp[h][0] + sp[h][1];
+}
+
+// sum v[0..3] over the 8 lanes of a token (lanes w = lane & 7), full scores of
+// all four heads back in every lane: transposing butterfly, then broadcast.
+// Head h is summed on lanes w = 2h, 2h + 1 (commutative adds: the same bits),
+// so every lane of the token ends with identical values.
+__device__ __forceinline__ void token_reduce(float (&v)[HG], int w) {
+    const bool b4 = (w & 4) != 0, b2 = (w & 2) != 0;
+    const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
+    float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 4);  // heads 2 b4, 2 b4 + 1 over w, w ^ 4
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+    const float s = b2 ? k0 : k1;
+    float k = b2 ? k1 : k0;
+    k += __shfl_xor_sync(0xffffffffu, s, 2);  // head 2 b4 + b2 over 4 lanes
+    k += __shfl_xor_sync(0xffffffffu, k, 1);  // ... over all 8
+    const float o = __shfl_xor_sync(0xffffffffu, k, 2);
+    const float p0 = b2 ? o : k, p1 = b2 ? k : o;  // heads 2 b4, 2 b4 + 1
+    const float q0 = __shfl_xor_sync(0xffffffffu, p0, 4), q1 = __shfl_xor_sync(0xffffffffu, p1, 4);
+    v[0] = b4 ? q0 : p0;
+    v[1] = b4 ? q1 : p1;
+    v[2] = b4 ? p0 : q0;
+    v[3] = b4 ? p1 : q1;
+}
+
+// NU units: key phase, one running-max update per head, value phase (see
+// process_units; masked tokens take p = 0 without a branch)
+template <int NU, typename AfterKeys>
+__device__ __forceinline__ void process4(const Unit4 *U, State4 &S, const uint32_t (&pk)[4],
+                                         const uint32_t (&pv)[4], const bool *okA,
+                                         const bool *okB, int w, AfterKeys after_keys) {
+    float sa[NU][HG], sb[NU][HG];
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        key_scores(U[n].ka, pk, sa[n]);
+        key_scores(U[n].kb, pk, sb[n]);
+    }
+    after_keys();
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        token_reduce(sa[n], w);
+        token_reduce(sb[n], w);
+    }
+    float pa[NU][HG], pb[NU][HG];
+#pragma unroll
+    for (int h = 0; h < HG; ++h) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int n = 0; n < NU; ++n)
+            mx = fmaxf(mx, fmaxf(okA[n] ? sa[n][h] : -INFINITY, okB[n] ? sb[n][h] : -INFINITY));
+        if (mx > S.m[h]) {
+            const float f = fast_exp2(S.m[h] - mx);
+            S.l[h] *= f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) fmul2(S.acc[h][k], f);
+            S.m[h] = mx;
+        }
+#pragma unroll
+        for (int n = 0; n < NU; ++n) {
+            pa[n][h] = okA[n] ? fast_exp2(sa[n][h] - S.m[h]) : 0.f;
+            pb[n][h] = okB[n] ? fast_exp2(sb[n][h] - S.m[h]) : 0.f;
+            S.l[h] += pa[n][h] + pb[n][h];
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t wa = j < 4 ? U[n].va.x : U[n].va.y;
+            const uint32_t wb = j < 4 ? U[n].vb.x : U[n].vb.y;
+            const unsigned long long ca = widen(lds_cv16(__byte_perm(wa, pv[j >> 1], sel_for(j))));
+            const unsigned long long cb = widen(lds_cv16(__byte_perm(wb, pv[j >> 1], sel_for(j))));
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                ffma2(S.acc[h][j], pa[n][h], ca);
+                ffma2(S.acc[h][j], pb[n][h], cb);
+            }
+        }
+    }
+}
+
+// the four heads' tables as one fp16 table: entry (c, i) = (h0, h1, h2, h3);
+// slot f = tid + k NT of the [256][32] float4 key codebook layout holds
+// subspaces 2(f & 31), +1 of centroid f / 32 -> one 16-byte store
+template <int NT>
+__device__ __forceinline__ void tab_build4(unsigned char *tab, const float4 (&cc)[lut_iters<NT>()],
+                                           const float *q0, float scale, int tid) {
+    constexpr int kLutIters = lut_iters<NT>();
+    float4 qh[HG];
+#pragma unroll
+    for (int h = 0; h < HG; ++h) qh[h] = __ldg(reinterpret_cast<const float4 *>(q0 + h * D) + (tid & 31));
+#pragma unroll
+    for (int k = 0; k < kLutIters; ++k) {
+        const int f = tid + k * NT;
+        if (kLutSlots % NT != 0 && f >= kLutSlots) break;
+        float e0[HG], e1[HG];
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            e0[h] = scale * fmaf(qh[h].y, cc[k].y, qh[h].x * cc[k].x);
+            e1[h] = scale * fmaf(qh[h].w, cc[k].w, qh[h].z * cc[k].z);
+        }
+        uint4 o;
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.x) : "f"(e0[1]), "f"(e0[0]));  // lo = head 0
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.y) : "f"(e0[3]), "f"(e0[2]));
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.z) : "f"(e1[1]), "f"(e1[0]));
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.w) : "f"(e1[3]), "f"(e1[2]));
+        const int c = f >> 5, i0 = 2 * (f & 31);
+        *reinterpret_cast<uint4 *>(tab + ((i0 >> 5) << 16) + (c << 8) + ((i0 & 31) << 3)) = o;
+    }
+}
+}  // namespace g4
+
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
+    constexpr int HG = g4::HG, UT = g4::UT, TAB_BYTES = g4::TAB_BYTES,
+                  CV16_BYTES = g4::CV16_BYTES;
+    using g4::tau_a, g4::lane_subspace, g4::Unit4, g4::State4, g4::load_unit4, g4::ld8,
+        g4::process4, g4::tab_build4;
+    constexpr int NT = W * 32, NG = NT / 128;
+    static_assert(NT % 128 == 0, "W must be a multiple of 4");
+    static_assert(HG * NG <= 2 * (WMAX / 4), "column sums fit the colsum region");
+    static_assert(HG * W * 4 * D * 4 <= TAB_BYTES, "slot rows fit the key table");
+    static_assert(2 * HG * W <= 4 * WMAX, "max / sum reductions fit the red region");
+    static_assert(TAB_BYTES + CV16_BYTES <= OFF_RED, "tables before the reduction area");
+    const int Hqv = A.Hq / HG;  // virtual heads per sequence
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *rows_s = reinterpret_cast<float *>(smem);  // epilogue: slot rows in the key table
+    float *red_m = reinterpret_cast<float *>(smem + OFF_RED);
+    float *red_l = red_m + HG * W;
+    float(*colsum)[D] = reinterpret_cast<float(*)[D]>(smem + OFF_COL);
+    float *dn_m = reinterpret_cast<float *>(smem + OFF_DNS);
+    float *dn_l = dn_m + W;
+    float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + W);
+    int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
+    int *nq_s = reinterpret_cast<int *>(smem + OFF_NQ);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();
+    const uint32_t cta_byte = sbase & 0xFF000000u;
+    const uint32_t bar_cv = sbase + OFF_BAR;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = lane & 7, slot = lane >> 3;
+    const int tA = tau_a(slot);
+    const int dB = 2 * M + 8 * ((w ^ 1) - w);  // token B's code bytes relative to A's
+    const int wu = W - 1 - warp;               // unit order (see decode_partials_m64b8)
+
+    if (tid == 0) {
+        mbar_init(bar_cv, 1);
+        if (A.early_cv) {
+            mbar_expect_tx(bar_cv, CV16_BYTES);
+#pragma unroll
+            for (int c = 0; c < CV16_BYTES / 16384; ++c)
+                bulk_g2s(sbase + TAB_BYTES + c * 16384,
+                         reinterpret_cast<const char *>(A.cv) + c * 16384, 16384, bar_cv);
+        }
+    }
+    const int cta = blockIdx.x;
+    const int group = A.Hq / A.Hkv;
+    const int P = A.share > 1 ? A.share : 1;
+    const int pc = cta / P, half = cta - pc * P, Hqp = Hqv / P;
+    auto vhead = [&](int ph) {
+        const int bb = ph / Hqp;
+        return bb * Hqv + (ph - bb * Hqp) * P + half;
+    };
+    Unit4 Ur[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) Ur[rr].ka = Ur[rr].kb = Ur[rr].va = Ur[rr].vb = uint2{0u, 0u};
+    CostMap cm;
+    Segment s0;
+    bool have_s0 = false;
+    int64_t pos = 0, end = 0;
+    const bool nq_cached = A.B <= kNqCache;
+    const bool early = A.early_codes && nq_cached;
+    auto first_ring = [&]() {
+        const int32_t *src = A.n_q;
+        if (nq_cached) {
+            for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = __ldcg(A.n_q + bb);
+            __syncthreads();
+            src = nq_s;
+        }
+        cm = cost_map(src, A.B, Hqp, A.num_ctas / P, P);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
+        int64_t p0 = pos;
+        have_s0 = next_segment(src, A.B, Hqp, &p0, end, &s0);
+        if (have_s0) {
+            const int vh0 = vhead(s0.bh);
+            const int b = vh0 / Hqv, hkv = (vh0 - b * Hqv) * HG / group;
+            const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
+            const int u0 = s0.lo / UT;
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr)
+                load_unit4(Ur[rr], A.codes_k + head_off + 8 * w, A.codes_v + head_off + 8 * w,
+                           u0 + wu + rr * W, tA, dB, s0.lo, s0.hi);
+        }
+    };
+    int *stale_s = flag_s + (WMAX / 4);
+    if (early) {
+        if (tid == 0) *stale_s = 0;
+        first_ring();
+    }
+    pdl_launch_dependents();
+    pdl_wait();
+    int nq_fresh = 0;
+    if (early && tid < A.B) nq_fresh = __ldcg(A.n_q + tid);
+    if (!early) first_ring();
+    if (tid == 0 && !A.early_cv) {
+        mbar_expect_tx(bar_cv, CV16_BYTES);
+#pragma unroll
+        for (int c = 0; c < CV16_BYTES / 16384; ++c)
+            bulk_g2s(sbase + TAB_BYTES + c * 16384, reinterpret_cast<const char *>(A.cv) + c * 16384,
+                     16384, bar_cv);
+    }
+
+    // lane-constant address bytes: table [half][code][32] x 8 B, value
+    // codebook [code][half][32] x 4 B (subspace half = w >> 2 for this lane)
+    uint32_t pk[4], pv[4];
+    const uint32_t khalf = (uint32_t)(w >> 2);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = lane_subspace(slot, w, 2 * jp + e);
+            a |= (uint32_t)((i & 31) << 3) << (8 * e);
+            b |= (uint32_t)(((i >> 5) << 7) | ((i & 31) << 2)) << (8 * e);
+        }
+        pk[jp] = a | (khalf << 16) | cta_byte;
+        pv[jp] = b | cta_byte;
+    }
+
+    bool cv_ready = false;
+    const int32_t *nq = nq_cached ? nq_s : A.n_q;
+    bool ring_loaded = have_s0;
+    Segment sg;
+    bool validate = early;
+    auto restart = [&]() {
+        __syncthreads();
+        if (tid < A.B) nq_s[tid] = nq_fresh;
+        if (tid == 0) *stale_s = 0;
+        __syncthreads();
+        cm = cost_map(nq_s, A.B, Hqp, A.num_ctas / P, P);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
+        ring_loaded = false;
+    };
+    bool stale_now = false;
+  segments:
+    while (next_segment(nq, A.B, Hqp, &pos, end, &sg)) {
+        const int vh = vhead(sg.bh);
+        const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
+        const int bh0 = b * A.Hq + hq0;
+        const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M;
+        const uint8_t *kbase = A.codes_k + head_off + 8 * w;
+        const uint8_t *vbase = A.codes_v + head_off + 8 * w;
+        const int lo = sg.lo, hi = sg.hi;
+        const int u0 = lo / UT, u1 = (hi + UT - 1) / UT;
+        if (!ring_loaded) {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr)
+                load_unit4(Ur[rr], kbase, vbase, u0 + wu + rr * W, tA, dB, lo, hi);
+        }
+        ring_loaded = false;
+
+        __syncthreads();  // the previous segment's epilogue is done with the table
+        {
+            float4 cc[lut_iters<NT>()];
+            lut_load<NT>(cc, A.ck, tid);
+            // scores in log2 units: the table holds scale * log2(e) * (q . c)
+            tab_build4<NT>(smem, cc, A.q + (int64_t)bh0 * D, A.scale * kLog2e, tid);
+        }
+        if (validate && tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+        const bool do_dense = A.counters != nullptr && sg.last;
+        const int64_t dense_base = (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq;
+#pragma unroll 1
+        for (int h = 0; h < HG; ++h) {
+            if (h > 0) __syncthreads();  // the previous head's merge has read dn_*
+            if (do_dense)
+                dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent,
+                                 A.k_cur, A.v_cur, A.Hkv, bh0 + h, b, hkv, warp, W, lane, dn_m,
+                                 dn_l, dn_acc);
+            if (h == 0 && !cv_ready) {
+                mbar_wait(bar_cv, 0);
+                cv_ready = true;
+            }
+            __syncthreads();
+            if (h == 0 && validate) {
+                validate = false;
+                stale_now = *stale_s != 0;
+                if (stale_now) break;
+            }
+            if (do_dense && tid < D) {
+                float Mx = -INFINITY;
+#pragma unroll
+                for (int ww = 0; ww < W; ++ww)
+                    if (dn_l[ww] > 0.f) Mx = fmaxf(Mx, dn_m[ww]);
+                float L = 0.f, acc = 0.f;
+                if (Mx != -INFINITY) {
+#pragma unroll
+                    for (int ww = 0; ww < W; ++ww) {
+                        if (dn_l[ww] > 0.f) {
+                            const float f = expf(dn_m[ww] - Mx);
+                            L += dn_l[ww] * f;
+                            acc += dn_acc[ww][tid] * f;
+                        }
+                    }
+                }
+                float *rec = A.parts + (dense_base + bh0 + h) * (D + kPS);
+                rec[kPS + tid] = acc;
+                if (tid == 0) {
+                    rec[0] = Mx;
+                    rec[1] = L;
+                    rec[2] = 0.f;
+                    rec[3] = 0.f;
+                }
+            }
+        }
+        if (stale_now) {
+            stale_now = false;
+            restart();
+            continue;
+        }
+        State4 S;
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            S.m[h] = -INFINITY;
+            S.l[h] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) S.acc[h][k] = 0ull;
+        }
+        int u = u0 + wu;
+        const int nunits = max(0, (u1 - u0 - wu + W - 1) / W);
+        constexpr int64_t kStep = (int64_t)W * UT * M;  // bytes per unit step of a warp
+        const int64_t dv = vbase - kbase;
+        int tn = (u + 2 * W) * UT + tA;  // token A of the next unit to load
+        const uint8_t *kp = kbase + (int64_t)tn * M;
+        for (int trip = 0; trip < nunits / 2; ++trip) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) asm volatile("" : "+r"(pk[k]), "+r"(pv[k]));
+            bool okA[2], okB[2];
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                const int ta = (u + n * W) * UT + tA;
+                okA[n] = ta >= lo && ta < hi;
+                okB[n] = ta + 2 >= lo && ta + 2 < hi;
+            }
+            process4<2>(Ur, S, pk, pv, okA, okB, w, [&]() {
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    const int ta = tn + n * W * UT;
+                    const uint8_t *p = kp + n * kStep;
+                    if (ta >= lo && ta < hi) Ur[n].ka = ld8(p);
+                    if (ta + 2 >= lo && ta + 2 < hi) Ur[n].kb = ld8(p + dB);
+                }
+            });
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                const int ta = tn + n * W * UT;
+                const uint8_t *p = kp + n * kStep + dv;
+                if (ta >= lo && ta < hi) Ur[n].va = ld8(p);
+                if (ta + 2 >= lo && ta + 2 < hi) Ur[n].vb = ld8(p + dB);
+            }
+            u += 2 * W;
+            kp += 2 * kStep;
+            tn += 2 * W * UT;
+        }
+        if (nunits % 2) {
+            bool okA[1], okB[1];
+            const int ta = u * UT + tA;
+            okA[0] = ta >= lo && ta < hi;
+            okB[0] = ta + 2 >= lo && ta + 2 < hi;
+            process4<1>(Ur, S, pk, pv, okA, okB, w, []() {});
+        }
+
+        // ---- epilogue: one (m, l, acc) record per head for this segment
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            float mw = S.m[h];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+            if (lane == 0) red_m[h * W + warp] = mw;
+        }
+        __syncthreads();  // all warps are past the main loop: the table is free
+        float Mx[HG];
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            Mx[h] = red_m[h * W];
+#pragma unroll
+            for (int ww = 1; ww < W; ++ww) Mx[h] = fmaxf(Mx[h], red_m[h * W + ww]);
+            const float f = (S.m[h] == -INFINITY) ? 0.f : fast_exp2(S.m[h] - Mx[h]);
+            float lw = (w == 0) ? S.l[h] * f : 0.f;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
+            if (lane == 0) red_l[h * W + warp] = lw;
+            float *rows = rows_s + ((h * W + warp) * 4 + slot) * D;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = lane_subspace(slot, w, j);
+                const float2 a = unpack2(S.acc[h][j]);
+                rows[2 * i] = a.x * f;
+                rows[2 * i + 1] = a.y * f;
+            }
+        }
+        __syncthreads();
+        {
+            constexpr int RPP = W * 4 / NG;  // slot rows per 128-thread part
+            const int col = tid & (D - 1), prt = tid >> 7;
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                float cs = 0.f;
+                const float *rows = rows_s + h * W * 4 * D;
+#pragma unroll 8
+                for (int rr = prt * RPP; rr < prt * RPP + RPP; ++rr) cs += rows[rr * D + col];
+                colsum[h * NG + prt][col] = cs;
+            }
+        }
+        __syncthreads();
+        if (tid < D) {
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                float *rec =
+                    A.parts + ((int64_t)HG * ((int64_t)(pc + sg.bh) * P + half) + h) * (D + kPS);
+                float a = colsum[h * NG][tid];
+#pragma unroll
+                for (int pp = 1; pp < NG; ++pp) a += colsum[h * NG + pp][tid];
+                rec[kPS + tid] = a;
+                if (tid == 0) {
+                    float L = 0.f;
+#pragma unroll
+                    for (int ww = 0; ww < W; ++ww) L += red_l[h * W + ww];
+                    rec[0] = Mx[h] * kLn2;  // log2 units -> natural
+                    rec[1] = L;
+                    rec[2] = 0.f;
+                    rec[3] = 0.f;
+                }
+            }
+        }
+    }
+    if (validate) {
+        validate = false;
+        if (tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+        __syncthreads();
+        if (*stale_s) {
+            restart();
+            goto segments;
+        }
+    }
+    // ---- arrivals and the last arriver's merge (as decode_partials_m64b8)
+    if (A.counters != nullptr) {
+        __syncthreads();
+        const int grp = tid >> 7, gt = tid & (D - 1);
+        int64_t p2 = cta_begin(cm, pc);
+        Segment s2;
+        for (int k = 0; next_segment(nq, A.B, Hqp, &p2, end, &s2); ++k) {
+            if (k % NG != grp) continue;
+            int c_first, c_last, len;
+            head_ctas(nq, Hqp, s2.bh, cm, &c_first, &c_last, &len);
+            const int vh2 = vhead(s2.bh);
+            if (gt == 0) {
+                int old;
+                asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "l"(A.counters + vh2)
+                             : "memory");
+                const bool last = (old == c_last - c_first);
+                if (last) A.counters[vh2] = 0;
+                flag_s[grp] = last ? 1 : 0;
+            }
+            named_bar_sync(1 + grp, D);
+            const bool last = flag_s[grp] != 0;
+            named_bar_sync(1 + grp, D);
+            if (last) {
+                const int b2 = vh2 / Hqv, bq0 = b2 * A.Hq + (vh2 - b2 * Hqv) * HG;
+#pragma unroll 1
+                for (int h = 0; h < HG; ++h)
+                    finish_head(A.parts, (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq, HG,
+                                s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged,
+                                P, half);
+            }
+        }
+    }
+    if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight
+}
 }  // namespace fast
 
 // ========================================================= generic path ====
@@ -1520,9 +2114,9 @@ extern "C" int pqkv_debug_wtrace(unsigned long long *host, int n) {  // n <= 64 
 #endif
 
 extern "C" int64_t pqkv_partials_floats(int num_ctas, int B, int Hq, int d) {
-    // split records (two per split and virtual head when a CTA serves two
-    // query heads) + one dense record per query head
-    return (2 * (int64_t)num_ctas + 2 * (int64_t)B * Hq) * (int64_t)(d + kPS);
+    // split records (up to four per split and virtual head when a CTA serves
+    // several query heads) + one dense record per query head
+    return (4 * (int64_t)num_ctas + 2 * (int64_t)B * Hq) * (int64_t)(d + kPS);
 }
 
 static int check_decode_args(const char *fn, int B, int Hq, int Hkv, int d, int M, int nbits,
@@ -1568,6 +2162,36 @@ static int launch_fast(const fast::Args &args, bool pdl, cudaStream_t st, const 
     static int trace_seq = 0;
     const_cast<fast::Args &>(args).trace_id = trace_seq++;
 #endif
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(args.num_ctas);
+    cfg.blockDim = dim3(W * 32);
+    cfg.dynamicSmemBytes = fast::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+    return launch_status(fn);
+}
+
+#ifndef PQKV_GQA4_WARPS
+#define PQKV_GQA4_WARPS 12
+#endif
+template <int W>
+static int launch_gqa4(const fast::Args &args, bool pdl, cudaStream_t st, const char *fn) {
+    static int attr_set[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = fast::decode_gqa4_f16<W>;
+    if (dev >= 64 || !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             fast::SMEM_BYTES);
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+        if (dev < 64) attr_set[dev] = 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(args.num_ctas);
     cfg.blockDim = dim3(W * 32);
@@ -1704,7 +2328,8 @@ extern "C" int pqkv_decode_attention(
                    "pqkv_decode_attention: recent_k and recent_v go together");
     PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
                               PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES |
-                              PQKV_DECODE_ONE_HEAD_PER_CTA | PQKV_DECODE_F16_KEY_TABLE)) == 0,
+                              PQKV_DECODE_ONE_HEAD_PER_CTA | PQKV_DECODE_F16_KEY_TABLE |
+                              PQKV_DECODE_KEY_TABLE_PAIRS)) == 0,
                    "pqkv_decode_attention: unknown flags");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
@@ -1738,14 +2363,21 @@ extern "C" int pqkv_decode_attention(
     // GQA: the CTAs serving the virtual heads of one KV head stream its codes
     // concurrently (one DRAM fetch, L2 hits for the others) -- P = virtual
     // heads per KV head, reduced until it divides the grid
+    const int group = Hq / Hkv;
+    // four query heads per CTA: the packed fp16 key table with a group that
+    // is a multiple of 4 (unless pairs are asked for)
+    const bool four = (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) &&
+                      (flags & PQKV_DECODE_F16_KEY_TABLE) && group % 4 == 0 &&
+                      !(flags & (PQKV_DECODE_ONE_HEAD_PER_CTA | PQKV_DECODE_KEY_TABLE_PAIRS));
     {
-        const int group = Hq / Hkv;
         const bool two = (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) && group % 2 == 0 &&
                          !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA);
-        int P = PQKV_SHARE ? group / (two ? 2 : 1) : 1;
+        int P = PQKV_SHARE ? group / (four ? 4 : two ? 2 : 1) : 1;
         while (P > 1 && (num_ctas % P != 0 || P > 16)) P = (P % 2 == 0) ? P / 2 : 1;
         a.share = P;
     }
+    if (four)
+        return launch_gqa4<PQKV_GQA4_WARPS>(a, pdl, st, "pqkv_decode_attention");
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
         // even GQA groups: one CTA serves two query heads of a KV head
         if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA)) {

@@ -40,7 +40,8 @@ class PQDecoder:
 
     def __init__(self, B: int, Hq: int, Hkv: int, config: PQConfig, device=None,
                  num_ctas: int | None = None, pdl: bool = False, static_codebooks: bool = False,
-                 early_codes: bool = False, f16_key_table: bool = False):
+                 early_codes: bool = False, f16_key_table: bool = False,
+                 key_table_pairs: bool = False):
         if Hq % Hkv:
             raise ValueError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
         self.B, self.Hq, self.Hkv, self.config = B, Hq, Hkv, config
@@ -50,6 +51,7 @@ class PQDecoder:
         self.pdl, self.static_codebooks, self.early_codes = pdl, static_codebooks, early_codes
         # stated-tolerance GQA mode (with an fp16 value codebook layout)
         self.f16_key_table = f16_key_table
+        self.key_table_pairs = key_table_pairs  # two query heads per CTA even for groups of 4
 
     @property
     def num_ctas(self) -> int:
@@ -76,6 +78,7 @@ class PQDecoder:
                            n_recent=n_recent, k_cur=k_cur, v_cur=v_cur, out=out, lse=lse,
                            merged=merged, pdl=self.pdl, static_codebooks=self.static_codebooks,
                            early_codes=self.early_codes, f16_key_table=self.f16_key_table,
+                           key_table_pairs=self.key_table_pairs,
                            stream=stream)
         return out
 

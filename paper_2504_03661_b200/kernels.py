@@ -313,7 +313,7 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
                      k_cur=None, v_cur=None, out=None, lse=None, merged=None, pdl: bool = False,
                      static_codebooks: bool = False, early_codes: bool = False,
                      one_head_per_cta: bool = False, f16_key_table: bool = False,
-                     stream=None) -> None:
+                     key_table_pairs: bool = False, stream=None) -> None:
     """One fused launch per layer (m64b8): quantized span + dense window +
     fixed-order merge + finalize for every (b, hq); other geometries fall back
     to decode_partials + decode_finish inside the library.
@@ -326,8 +326,9 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
     early_codes likewise for n_q and the codes below it (appended by earlier
     steps): the work split and the first code loads then precede the wait.
     f16_key_table (with the fp16 value codebook and an even GQA group): the
-    two query heads of a CTA share one half2 key table (stated tolerance,
-    tests/test_gpu_gqa_tables.py)."""
+    query heads of a CTA share one packed fp16 key table (stated tolerance,
+    tests/test_gpu_gqa_tables.py): four per CTA when the group is a multiple
+    of 4 (key_table_pairs=True keeps two), else two."""
     _check_codes(ws, Hkv, codes_k, codes_v)
     ld_recent = 0
     if recent_k is not None:
@@ -341,6 +342,8 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
         flags |= N.DECODE_ONE_HEAD_PER_CTA
     if f16_key_table:
         flags |= N.DECODE_F16_KEY_TABLE
+    if key_table_pairs:
+        flags |= N.DECODE_KEY_TABLE_PAIRS
     if cb_v_layout.dtype == torch.float16:  # value_codebook_layout(..., half=True)
         flags |= N.DECODE_F16_VALUE_CODEBOOK
     _call(codes_k.device, "pqkv_decode_attention", N.ptr(q), float(scale), N.ptr(cb_k_layout), N.ptr(ws.lut),

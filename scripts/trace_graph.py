@@ -21,14 +21,15 @@ ck = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
 cv = [random_codes((Bb, Hkv, n, 64), 8, g, dev) for _ in range(L)]
 cb_all = torch.empty((L, 2, 64 * 256 * 2), device=dev)
 cbk = [K.key_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8, out=cb_all[l, 0]) for l in range(L)]
-cbv = [K.value_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8, out=cb_all[l, 1]) for l in range(L)]
+F16 = os.environ.get("F16") == "1"  # the fp16 value-codebook mode
+cbv = [K.value_codebook_layout(torch.randn((64, 256, 2), generator=g, device=dev), 8, half=F16, out=None if F16 else cb_all[l, 1]) for l in range(L)]
 q = torch.randn((L, Bb, Hq, 128), generator=g, device=dev)
 rk = torch.randn((L, Bb, Hkv, R, 128), generator=g, device=dev); rv = torch.randn_like(rk)
 kc = torch.randn((L, Bb, Hkv, 128), generator=g, device=dev); vc = torch.randn_like(kc)
 nq = torch.full((Bb,), n, dtype=torch.int32, device=dev); nr = torch.full((Bb,), R, dtype=torch.int32, device=dev)
 out = torch.empty((L, Bb, Hq, 128), device=dev)
 torch.cuda.synchronize()
-dec = PQDecoder(Bb, Hq, Hkv, PQConfig(128, 64, 8), device=dev, pdl=True, static_codebooks=True, early_codes=os.environ.get("EARLY", "1") == "1")
+dec = PQDecoder(Bb, Hq, Hkv, PQConfig(128, 64, 8), device=dev, pdl=True, static_codebooks=os.environ.get("STATIC", "1") == "1", early_codes=os.environ.get("EARLY", "1") == "1")
 st = torch.cuda.Stream()
 if os.environ.get("L2_PERSIST") == "1":
     N.call("pqkv_l2_persist", N.ptr(cb_all), cb_all.numel() * 4, 1.0, N.stream_ptr(st))

@@ -65,7 +65,7 @@ def test_bad_arguments_fail_before_cuda(lib):
 def test_partials_size(lib):
     from paper_2504_03661_b200 import _native as N
     # split records + one dense-window record per head
-    assert N.partials_floats(148, 16, 32, 128) == (2 * 148 + 2 * 16 * 32) * 132
+    assert N.partials_floats(148, 16, 32, 128) == (4 * 148 + 2 * 16 * 32) * 132
 
 
 def test_reference_signatures_kept():

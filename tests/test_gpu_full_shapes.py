@@ -99,9 +99,12 @@ def test_full_gqa_layer_vs_c_oracle(cfg):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
     got16 = _decode(x, 32, 8, half=True)
     np.testing.assert_allclose(got16, want, rtol=RTOL16, atol=ATOL16)
-    # + the two query heads' key tables of a CTA as one half2 table
+    # + the four query heads' key tables of a CTA as one packed fp16 table
     got16k = _decode(x, 32, 8, half=True, f16_key_table=True)
     np.testing.assert_allclose(got16k, want, rtol=RTOL16, atol=ATOL16)
+    # ... and two query heads per CTA (one half2 table)
+    got16p = _decode(x, 32, 8, half=True, f16_key_table=True, key_table_pairs=True)
+    np.testing.assert_allclose(got16p, want, rtol=RTOL16, atol=ATOL16)
 
 
 def test_config4_eight_way_split_equals_unsplit():

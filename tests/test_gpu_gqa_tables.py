@@ -1,9 +1,11 @@
 """PQKV_DECODE_F16_KEY_TABLE (GQA, stated tolerance): with the fp16 value
-codebook and an even group, the CTA serving two query heads of a KV head keeps
-their key tables as ONE half2 table -- entry (c, i) holds both heads'
-build_key_lut values (attention.py:70-83) rounded to fp16 -- so one 4-byte
-gather per key code feeds both heads' scores, which are summed in fp32
-(mixed f32 + f16 adds).  Each table entry carries a relative rounding error
+codebook and an even group, the CTA serving the query heads of a KV head keeps
+their key tables as ONE packed fp16 table -- entry (c, i) holds the heads'
+build_key_lut values (attention.py:70-83) rounded to fp16 -- so one gather per
+key code feeds every head's score, summed in fp32 (mixed f32 + f16 adds).
+Groups that are a multiple of 4 run four query heads per CTA (8-byte entries,
+decode_gqa4_f16, fp32 softmax weights); key_table_pairs=True (and groups of 2)
+run two (4-byte entries, fp16 weights).  Each table entry carries a relative rounding error
 of at most 2^-11, so a score's absolute error is at most
 2^-11 * sum_i |lut[i][code_i]|; the softmax weights and the value path are
 those of the fp16 value-codebook mode.
@@ -26,14 +28,17 @@ pytestmark = pytest.mark.gpu
 RTOL16, ATOL16 = 2e-3, 2e-4
 
 
+@pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
-    (2, 8, 2, 5000, [4999, 1234], [5, 32]),          # G = 4: two heads per CTA
+    (2, 8, 2, 5000, [4999, 1234], [5, 32]),          # G = 4: four (or two) heads per CTA
     (3, 2, 1, 700, [0, 1, 7], [0, 3, 0]),            # G = 2, empty / tiny spans
     (1, 8, 1, 20000, [20000], [7]),                  # G = 8, many CTAs per virtual head
     (4, 32, 8, 9000, [9000, 8000, 2500, 4500], [31, 0, 3, 17]),  # Llama-3 grouping, ragged
+    (5, 16, 4, 300, [0, 64, 170, 299, 96], [1, 0, 32, 5, 9]),     # empty / short spans, G = 4
 ])
-def test_f16_key_table_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
-    got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True, f16_keys=True)
+def test_f16_key_table_vs_oracle(B, Hq, Hkv, cap, n_q, n_r, pairs):
+    got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True, f16_keys=True,
+                                      pairs=pairs)
     # vs the oracle on the fp16-rounded value codebook: the key-table and
     # weight roundings only
     np.testing.assert_allclose(got, want16, rtol=RTOL16, atol=ATOL16)

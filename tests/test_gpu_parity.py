@@ -270,7 +270,7 @@ def _oracle_heads(q, ck_codes, cv_codes, n_q, rk, rv, n_r, kcur, vcur, cents_k, 
 
 
 def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_cv=False,
-                  f16_keys=False):
+                  f16_keys=False, pairs=False):
     from paper_2504_03661_b200 import kernels as K
     from paper_2504_03661_b200.engine import PQDecoder
     import paper_2504_03661_b200 as P
@@ -287,7 +287,8 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_c
     vc = rng.standard_normal((B, Hkv, 128)).astype(np.float32)
     dev = torch.device("cuda")
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-    dec = PQDecoder(B, Hq, Hkv, cfg, num_ctas=num_ctas, f16_key_table=f16_keys)
+    dec = PQDecoder(B, Hq, Hkv, cfg, num_ctas=num_ctas, f16_key_table=f16_keys,
+                    key_table_pairs=pairs)
     cbk = K.key_codebook_layout(t(cents_k), 8)
     cbv = K.value_codebook_layout(t(cents_v), 8, half=half_cv)
     dk, dv = K.relayout(t(codes_k), True), K.relayout(t(codes_v), True)  # decode layout
