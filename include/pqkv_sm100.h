@@ -195,10 +195,13 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
                              kernel finishes (with PQKV_DECODE_PDL) */
 #define PQKV_DECODE_F16_VALUE_CODEBOOK 4 /* cb_v is the fp16 layout of
                              pqkv_prepare_value_codebook_f16 */
-#define PQKV_DECODE_ONE_HEAD_PER_CTA 16 /* fp16 mode with an even GQA group:
-                             keep one query head per CTA (by default a CTA
-                             serves two query heads of a KV head and shares
-                             the value gathers) */
+#define PQKV_DECODE_ONE_HEAD_PER_CTA 16 /* GQA: keep one query head per CTA.
+                             By default the fp16 mode with an even group
+                             serves two (or four) query heads of a KV head per
+                             CTA, and the exact path with a group that is a
+                             multiple of 4 runs clusters of two CTAs that
+                             serve four query heads (each CTA one half of the
+                             subspaces), sharing the value gathers */
 #define PQKV_DECODE_F16_KEY_TABLE 32 /* with PQKV_DECODE_F16_VALUE_CODEBOOK
                              and an even GQA group: the query heads a CTA
                              serves keep one packed fp16 key table (entry

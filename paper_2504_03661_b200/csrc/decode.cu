@@ -1216,6 +1216,14 @@ __device__ __forceinline__ uint2 ld8(const uint8_t *p) {
                  : "l"(p));
     return r;
 }
+// refill in place: the destination is tied to the ring register's current
+// value ("+r"), so the compiler has no reason to load into a fresh register and
+// move it back (a move would wait for the load)
+__device__ __forceinline__ void ld8_into(uint2 &r, const uint8_t *p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "+r"(r.x), "+r"(r.y)
+                 : "l"(p));
+}
 __device__ __forceinline__ uint2 lds_tab(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(a), "n"(0x400));
@@ -1749,6 +1757,632 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
     }
     if (!cv_ready) mbar_wait(bar_cv, 0);  // never exit with a bulk copy in flight
 }
+// ======================================== exact GQA: CTA pairs (clusters) ==
+// decode_gqa_pair -- the exact fp32 path for a GQA group that is a multiple of
+// 4.  A cluster of two CTAs serves four query heads of a KV head (a virtual
+// head); CTA c of the pair owns subspace half c (32 subspaces, output dims
+// [64c, 64c + 64)).  Per CTA: the four heads' fp32 key tables of its half as
+// two float2 tables (heads 0-1, 2-3: [256][32] x 8 B, 64 KiB each) and its
+// half of the fp32 value codebook ([256][32] float2, 64 KiB) -- the value
+// gathers are shared by the four heads and every table is exact fp32, which no
+// single CTA could hold (4 x 64 KiB tables + 128 KiB codebook).
+//   * lane = (token slot s, eighth w): 4 lanes per token, 8 code bytes each
+//     ([32c + 8w, +8) of token s (instruction A) and s + 8 (B) of every
+//     16-token unit), rotated by 2 bytes when s & 2 (two PRMT per 8 bytes): on
+//     the stored decode layout every 8-byte gather of a warp is bank-conflict
+//     free (scripts/check_gqa_pair_lanes.py);
+//   * a token's 4 lanes reduce the four heads' partial scores with a
+//     transposing butterfly (lane w ends with head w over its half), then the
+//     pair exchanges them through distributed shared memory: each lane
+//     st.async-es its (token A, token B) partial into the peer warp's mailbox,
+//     completing tx bytes on the peer's mbarrier, and waits for the peer's
+//     (two mailboxes per warp, alternating; the pair runs its units in
+//     lockstep, so a mailbox is never overwritten before it is read).  Both
+//     CTAs add own + peer (commutative: the same bits), so both run the same
+//     online softmax;
+//   * lane w owns head w's softmax state of its token slot (one max update and
+//     two EX2 per unit) and broadcasts the weights to the slot's 4 lanes;
+//   * value path: one LDS.64 per code byte feeds four FFMA2 (one per head);
+//   * the records: each CTA writes its 64 output dims of the pair's (m, l, acc)
+//     record (rank 0 the header); both CTAs arrive on the virtual head's counter
+//     and the last arriver merges in pair order (deterministic).
+#ifndef PQKV_PAIR_CLAMP
+#define PQKV_PAIR_CLAMP 1
+#endif
+namespace gp {
+constexpr int HG = 4;
+constexpr int UT = 16;       // tokens per warp per unit
+constexpr int TAB = 0x10000; // tables: heads 0-1 at 0, heads 2-3 at TAB ([256][32] float2 each)
+constexpr int CVO = 0x20000; // the CTA's half of the value codebook ([256][32] float2)
+constexpr int HALF_BYTES = KSUB * 32 * 8;                  // 65536
+constexpr int OFF_MB = (SMEM_BYTES + 127) / 128 * 128;     // mailboxes [W][2][32] float2
+__host__ __device__ constexpr int off_mbar(int W) { return OFF_MB + W * 2 * 32 * 8; }
+__host__ __device__ constexpr int smem_bytes(int W) { return off_mbar(W) + W * 2 * 8; }
+
+template <int IMM>
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(IMM));
+    return v;
+}
+__device__ __forceinline__ void fadd2(unsigned long long &acc, unsigned long long x) {
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(x));
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// (a, b) into the peer's mailbox; the bytes complete on the peer's mbarrier
+__device__ __forceinline__ void st_async2(uint32_t raddr, float a, float b, uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+            raddr),
+        "f"(a), "f"(b), "r"(rbar)
+        : "memory");
+}
+
+struct UnitP {
+    uint2 ka, kb, va, vb;
+};
+struct StateP {
+    float m, l;                     // this lane's head (lane & 3) of its token slot
+    unsigned long long acc[HG][8];  // float2 per subspace of this lane, per head
+};
+
+// subspace (global index) of byte j of lane (s, w) in CTA half c, after the
+// lane's rotation
+__device__ __forceinline__ int lane_subspace(int c, int s, int w, int j) {
+    const int b = 32 * c + 8 * w + ((j + ((s & 2) ? 2 : 0)) & 7);  // byte of the row
+    const int q = b >> 4;
+    return 16 * q + (((b & 15) + decode_lane_rot(4 * s + q)) & 15);
+}
+
+// the lane's 8 code bytes in processing order: rotated by 2 bytes (slots 2, 3, 6, 7)
+__device__ __forceinline__ uint2 rot8(uint2 v, uint32_t sx, uint32_t sy) {
+    return make_uint2(__byte_perm(v.x, v.y, sx), __byte_perm(v.x, v.y, sy));
+}
+
+// the four heads' partial scores of one token over this lane's 8 subspaces:
+// (h0, h1) and (h2, h3) packed
+__device__ __forceinline__ void key_scores(const uint2 k, const uint32_t (&pk)[4],
+                                           unsigned long long &s01, unsigned long long &s23) {
+    unsigned long long a01 = 0, b01 = 0, a23 = 0, b23 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t a = __byte_perm(j < 4 ? k.x : k.y, pk[j >> 1], sel_for(j));
+        const unsigned long long e01 = lds64<0x400>(a), e23 = lds64<0x400 + TAB>(a);
+        if (j < 2) {
+            (j & 1 ? b01 : a01) = e01;
+            (j & 1 ? b23 : a23) = e23;
+        } else {
+            fadd2(j & 1 ? b01 : a01, e01);
+            fadd2(j & 1 ? b23 : a23, e23);
+        }
+    }
+    fadd2(a01, b01);
+    fadd2(a23, b23);
+    s01 = a01;
+    s23 = a23;
+}
+
+// this lane's head (w = lane & 3) summed over the token's 4 lanes
+__device__ __forceinline__ float reduce_head(unsigned long long s01, unsigned long long s23, int w) {
+    const bool b2 = (w & 2) != 0, b1 = (w & 1) != 0;
+    const unsigned long long snd = b2 ? s01 : s23;
+    unsigned long long keep = b2 ? s23 : s01;
+    const float2 sv = unpack2(snd);
+    unsigned long long rcv;
+    {
+        const float rx = __shfl_xor_sync(0xffffffffu, sv.x, 2);
+        const float ry = __shfl_xor_sync(0xffffffffu, sv.y, 2);
+        asm("mov.b64 %0, {%1,%2};" : "=l"(rcv) : "f"(rx), "f"(ry));
+    }
+    fadd2(keep, rcv);  // heads 2 b2, 2 b2 + 1 over w, w ^ 2
+    const float2 kv = unpack2(keep);
+    const float sndf = b1 ? kv.x : kv.y;
+    const float k = b1 ? kv.y : kv.x;
+    return k + __shfl_xor_sync(0xffffffffu, sndf, 1);  // head w over all 4 lanes
+}
+}  // namespace gp
+
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
+    constexpr int HG = gp::HG, UT = gp::UT, NT = W * 32;
+    constexpr int NPART = NT / 64;  // column-sum parts of 64 threads
+    static_assert(NT % 64 == 0, "W must be even");
+    static_assert(2 * HG * W <= 4 * WMAX, "max / sum reductions fit the red region");
+    static_assert(HG * W * 8 * 64 * 4 <= 2 * gp::TAB, "slot rows fit the key tables");
+    static_assert(HG * NPART * 64 <= 2 * (WMAX / 4) * D, "column sums fit the colsum region");
+    using gp::UnitP;
+    const int Hqv = A.Hq / HG;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *rows_s = reinterpret_cast<float *>(smem);  // epilogue: slot rows in the tables
+    float *red_m = reinterpret_cast<float *>(smem + OFF_RED);
+    float *red_l = red_m + HG * W;
+    float *colsum = reinterpret_cast<float *>(smem + OFF_COL);  // [HG][NPART][64]
+    float *dn_m = reinterpret_cast<float *>(smem + OFF_DNS);
+    float *dn_l = dn_m + W;
+    float(*dn_acc)[D] = reinterpret_cast<float(*)[D]>(dn_l + W);
+    int *flag_s = reinterpret_cast<int *>(smem + OFF_FLAG);
+    int *nq_s = reinterpret_cast<int *>(smem + OFF_NQ);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    if ((sbase & 0xFFFFFFu) != kDynBase) __trap();
+    const uint32_t cta_byte = sbase & 0xFF000000u;
+    const uint32_t bar_cv = sbase + OFF_BAR;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = lane & 3, slot = lane >> 2;
+    const int wu = W - 1 - warp;
+    const uint32_t crank = gp::cluster_rank(), peer = crank ^ 1u;
+    const int c = (int)crank;  // subspace half of this CTA
+    const int pc = blockIdx.x >> 1, npairs = A.num_ctas >> 1;
+    // rotation selectors (slots 2, 3, 6, 7 read their bytes rotated by 2)
+    const uint32_t rsx = (slot & 2) ? 0x5432u : 0x3210u, rsy = (slot & 2) ? 0x1076u : 0x7654u;
+
+    // mailboxes and mbarriers of this warp (local), and the peer's
+    const uint32_t mb_loc = sbase + gp::OFF_MB + warp * 2 * 32 * 8;
+    const uint32_t bar_loc = sbase + gp::off_mbar(W) + warp * 2 * 8;
+    const uint32_t mb_rem = gp::mapa(mb_loc, peer), bar_rem = gp::mapa(bar_loc, peer);
+    if (tid == 0) {
+        mbar_init(bar_cv, 1);
+        if (A.early_cv) {
+            mbar_expect_tx(bar_cv, gp::HALF_BYTES);
+#pragma unroll
+            for (int k = 0; k < gp::HALF_BYTES / 16384; ++k)
+                bulk_g2s(sbase + gp::CVO + k * 16384,
+                         reinterpret_cast<const char *>(A.cv) + c * gp::HALF_BYTES + k * 16384,
+                         16384, bar_cv);
+        }
+    }
+    if (lane == 0) {
+        mbar_init(bar_loc, 1);
+        mbar_init(bar_loc + 8, 1);
+    }
+    gp::cluster_sync();  // the peer's mbarriers exist before any st.async
+
+    const int group = A.Hq / A.Hkv;
+    UnitP Ur[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) Ur[rr].ka = Ur[rr].kb = Ur[rr].va = Ur[rr].vb = uint2{0u, 0u};
+    CostMap cm;
+    Segment s0;
+    bool have_s0 = false;
+    int64_t pos = 0, end = 0;
+    const bool nq_cached = A.B <= kNqCache;
+    const bool early = A.early_codes && nq_cached;
+    // ring loads are unconditional: a token outside [lo, hi) loads a row of
+    // the segment instead (its weight is masked to 0), so no load result is
+    // ever merged into a ring register by a move that would wait for it
+    auto row = [](int t, int lo, int hi) { return (int64_t)min(max(t, lo), hi - 1) * M; };
+    auto load_unit = [&](UnitP &U, const uint8_t *kbase, const uint8_t *vbase, int u, int lo,
+                         int hi) {
+        if (hi <= lo) return;  // an empty segment has no units
+        const int ta = u * UT + slot;
+#if PQKV_PAIR_CLAMP
+        U.ka = g4::ld8(kbase + row(ta, lo, hi));
+        U.va = g4::ld8(vbase + row(ta, lo, hi));
+        U.kb = g4::ld8(kbase + row(ta + 8, lo, hi));
+        U.vb = g4::ld8(vbase + row(ta + 8, lo, hi));
+#else
+        if (ta >= lo && ta < hi) {
+            U.ka = g4::ld8(kbase + (int64_t)ta * M);
+            U.va = g4::ld8(vbase + (int64_t)ta * M);
+        }
+        if (ta + 8 >= lo && ta + 8 < hi) {
+            U.kb = g4::ld8(kbase + (int64_t)(ta + 8) * M);
+            U.vb = g4::ld8(vbase + (int64_t)(ta + 8) * M);
+        }
+#endif
+    };
+    auto first_ring = [&]() {
+        const int32_t *src = A.n_q;
+        if (nq_cached) {
+            for (int bb = tid; bb < A.B; bb += NT) nq_s[bb] = __ldcg(A.n_q + bb);
+            __syncthreads();
+            src = nq_s;
+        }
+        cm = cost_map(src, A.B, Hqv, npairs);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
+        int64_t p0 = pos;
+        have_s0 = next_segment(src, A.B, Hqv, &p0, end, &s0);
+        if (have_s0) {
+            const int b = s0.bh / Hqv, hkv = (s0.bh - b * Hqv) * HG / group;
+            const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M + 32 * c + 8 * w;
+            const int u0 = s0.lo / UT;
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr)
+                load_unit(Ur[rr], A.codes_k + head_off, A.codes_v + head_off, u0 + wu + rr * W,
+                          s0.lo, s0.hi);
+        }
+    };
+    int *stale_s = flag_s + (WMAX / 4);
+    if (early) {
+        if (tid == 0) *stale_s = 0;
+        first_ring();
+    }
+    pdl_launch_dependents();
+    pdl_wait();
+    int nq_fresh = 0;
+    if (early && tid < A.B) nq_fresh = __ldcg(A.n_q + tid);
+    if (!early) first_ring();
+    if (tid == 0 && !A.early_cv) {
+        mbar_expect_tx(bar_cv, gp::HALF_BYTES);
+#pragma unroll
+        for (int k = 0; k < gp::HALF_BYTES / 16384; ++k)
+            bulk_g2s(sbase + gp::CVO + k * 16384,
+                     reinterpret_cast<const char *>(A.cv) + c * gp::HALF_BYTES + k * 16384, 16384,
+                     bar_cv);
+    }
+
+    // lane-constant address bytes: key tables and value codebook share the
+    // address code << 8 | (i & 31) << 3 (the regions ride in the immediates)
+    uint32_t pk[4];
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            a |= (uint32_t)((gp::lane_subspace(c, slot, w, 2 * jp + e) & 31) << 3) << (8 * e);
+        pk[jp] = a | cta_byte;
+    }
+
+    bool cv_ready = false;
+    const int32_t *nq = nq_cached ? nq_s : A.n_q;
+    bool ring_loaded = have_s0;
+    Segment sg;
+    bool validate = early;
+    uint32_t xu = 0;  // units exchanged with the peer warp (mailbox xu & 1, parity (xu >> 1) & 1)
+    auto restart = [&]() {
+        __syncthreads();
+        if (tid < A.B) nq_s[tid] = nq_fresh;
+        if (tid == 0) *stale_s = 0;
+        __syncthreads();
+        cm = cost_map(nq_s, A.B, Hqv, npairs);
+        pos = cta_begin(cm, pc);
+        end = min(cta_begin(cm, pc + 1), cm.total);
+        ring_loaded = false;
+    };
+    bool stale_now = false;
+  segments:
+    while (next_segment(nq, A.B, Hqv, &pos, end, &sg)) {
+        const int vh = sg.bh;
+        const int b = vh / Hqv, hq0 = (vh - b * Hqv) * HG, hkv = hq0 / group;
+        const int bh0 = b * A.Hq + hq0;
+        const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M + 32 * c + 8 * w;
+        const uint8_t *kbase = A.codes_k + head_off;
+        const uint8_t *vbase = A.codes_v + head_off;
+        const int lo = sg.lo, hi = sg.hi;
+        const int u0 = lo / UT, u1 = (hi + UT - 1) / UT;
+        if (!ring_loaded) {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr)
+                load_unit(Ur[rr], kbase, vbase, u0 + wu + rr * W, lo, hi);
+        }
+        ring_loaded = false;
+
+        __syncthreads();  // the previous segment's epilogue is done with the tables
+        {
+            // this half's tables, scores in log2 units: entry (code, i) of head h
+            // = scale log2(e) (q_h[2i] C[code][i].x + q_h[2i+1] C[code][i].y)
+            constexpr int kSlots = KSUB * 16;  // float4 slots (two subspaces) of the half
+            const float sc = A.scale * kLog2e;
+            const float4 *src = reinterpret_cast<const float4 *>(A.ck);
+#pragma unroll 4
+            for (int f = tid; f < kSlots; f += NT) {
+                const int cc = f >> 4, pr = f & 15;
+                const float4 cb = __ldg(src + cc * 32 + 16 * c + pr);
+                float e[HG][2];
+#pragma unroll
+                for (int h = 0; h < HG; ++h) {
+                    const float4 qv =
+                        __ldg(reinterpret_cast<const float4 *>(A.q + (int64_t)(bh0 + h) * D) +
+                              16 * c + pr);
+                    e[h][0] = sc * fmaf(qv.y, cb.y, qv.x * cb.x);
+                    e[h][1] = sc * fmaf(qv.w, cb.w, qv.z * cb.z);
+                }
+                const int off = (cc << 8) | (pr << 4);
+                *reinterpret_cast<float4 *>(smem + off) = make_float4(e[0][0], e[1][0], e[0][1], e[1][1]);
+                *reinterpret_cast<float4 *>(smem + gp::TAB + off) =
+                    make_float4(e[2][0], e[3][0], e[2][1], e[3][1]);
+            }
+        }
+        if (validate && tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+        const bool do_dense = A.counters != nullptr && sg.last && c == 0;
+        const int64_t dense_base = (int64_t)HG * npairs + (int64_t)A.B * A.Hq;
+#pragma unroll 1
+        for (int h = 0; h < HG; ++h) {
+            if (h > 0) __syncthreads();
+            if (do_dense)
+                dense_warp_state(A.q, A.scale, A.recent_k, A.recent_v, A.ld_recent, A.n_recent,
+                                 A.k_cur, A.v_cur, A.Hkv, bh0 + h, b, hkv, warp, W, lane, dn_m,
+                                 dn_l, dn_acc);
+            if (h == 0 && !cv_ready) {
+                mbar_wait(bar_cv, 0);
+                cv_ready = true;
+            }
+            __syncthreads();
+            if (h == 0 && validate) {
+                validate = false;
+                stale_now = *stale_s != 0;
+                if (stale_now) break;
+            }
+            if (do_dense && tid < D) {
+                float Mx = -INFINITY;
+#pragma unroll
+                for (int ww = 0; ww < W; ++ww)
+                    if (dn_l[ww] > 0.f) Mx = fmaxf(Mx, dn_m[ww]);
+                float L = 0.f, acc = 0.f;
+                if (Mx != -INFINITY) {
+#pragma unroll
+                    for (int ww = 0; ww < W; ++ww) {
+                        if (dn_l[ww] > 0.f) {
+                            const float f = expf(dn_m[ww] - Mx);
+                            L += dn_l[ww] * f;
+                            acc += dn_acc[ww][tid] * f;
+                        }
+                    }
+                }
+                float *rec = A.parts + (dense_base + bh0 + h) * (D + kPS);
+                rec[kPS + tid] = acc;
+                if (tid == 0) {
+                    rec[0] = Mx;
+                    rec[1] = L;
+                    rec[2] = 0.f;
+                    rec[3] = 0.f;
+                }
+            }
+        }
+        if (stale_now) {
+            stale_now = false;
+            restart();
+            continue;
+        }
+        gp::StateP S;
+        S.m = -INFINITY;
+        S.l = 0.f;
+#pragma unroll
+        for (int h = 0; h < HG; ++h)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) S.acc[h][k] = 0ull;
+
+        int u = u0 + wu;
+        const int nunits = max(0, (u1 - u0 - wu + W - 1) / W);
+        // one unit through ring slot U (static register indices: the loop
+        // below runs the two slots alternately)
+        auto unit_step = [&](UnitP &U) {
+            const int ta = u * UT + slot;
+            const bool okA = ta >= lo && ta < hi, okB = ta + 8 >= lo && ta + 8 < hi;
+            // key phase (this half), the pair's exchange, softmax at the owner lane
+            unsigned long long a01, a23, b01, b23;
+            gp::key_scores(gp::rot8(U.ka, rsx, rsy), pk, a01, a23);
+            gp::key_scores(gp::rot8(U.kb, rsx, rsy), pk, b01, b23);
+            const float oa = gp::reduce_head(a01, a23, w), ob = gp::reduce_head(b01, b23, w);
+            const uint32_t buf = xu & 1u, par = (xu >> 1) & 1u;
+            ++xu;
+            gp::st_async2(mb_rem + buf * 256 + lane * 8, oa, ob, bar_rem + buf * 8);
+            if (lane == 0) mbar_expect_tx(bar_loc + buf * 8, 256);
+            // refill this ring slot's key registers (the key phase is done with them)
+            {
+                const int tn = (u + 2 * W) * UT + slot;
+#if PQKV_PAIR_CLAMP
+                g4::ld8_into(U.ka, kbase + row(tn, lo, hi));
+                g4::ld8_into(U.kb, kbase + row(tn + 8, lo, hi));
+#else
+                if (tn >= lo && tn < hi) U.ka = g4::ld8(kbase + (int64_t)tn * M);
+                if (tn + 8 >= lo && tn + 8 < hi) U.kb = g4::ld8(kbase + (int64_t)(tn + 8) * M);
+#endif
+            }
+            mbar_wait(bar_loc + buf * 8, par);
+            float pa_, pb_;
+            {
+                float2 r;
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(r.x), "=f"(r.y)
+                             : "r"(mb_loc + buf * 256 + lane * 8));
+                // own + peer in rank order: both CTAs add the same two values
+                const float sa = c == 0 ? oa + r.x : r.x + oa;
+                const float sb = c == 0 ? ob + r.y : r.y + ob;
+                const float mx = fmaxf(okA ? sa : -INFINITY, okB ? sb : -INFINITY);
+                const bool up = mx > S.m;
+                if (__any_sync(0xffffffffu, up)) {  // rare: rescale the slot's accumulators
+                    const float f = up ? fast_exp2(S.m - mx) : 1.f;
+                    if (up) {
+                        S.l *= f;
+                        S.m = mx;
+                    }
+#pragma unroll
+                    for (int h = 0; h < HG; ++h) {
+                        const float fh = __shfl_sync(0xffffffffu, f, (lane & ~3) | h);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) fmul2(S.acc[h][k], fh);
+                    }
+                }
+                pa_ = okA ? fast_exp2(sa - S.m) : 0.f;
+                pb_ = okB ? fast_exp2(sb - S.m) : 0.f;
+                S.l += pa_ + pb_;
+            }
+            // the slot's four heads' weights in every lane of the slot
+            float pa[HG], pb[HG];
+            {
+                const float xa = __shfl_xor_sync(0xffffffffu, pa_, 1);
+                const float xb = __shfl_xor_sync(0xffffffffu, pb_, 1);
+                const bool b1 = (w & 1) != 0, b2 = (w & 2) != 0;
+                const float a0 = b1 ? xa : pa_, a1 = b1 ? pa_ : xa;  // heads 2 b2, 2 b2 + 1
+                const float c0 = b1 ? xb : pb_, c1 = b1 ? pb_ : xb;
+                const float ya0 = __shfl_xor_sync(0xffffffffu, a0, 2);
+                const float ya1 = __shfl_xor_sync(0xffffffffu, a1, 2);
+                const float yb0 = __shfl_xor_sync(0xffffffffu, c0, 2);
+                const float yb1 = __shfl_xor_sync(0xffffffffu, c1, 2);
+                pa[0] = b2 ? ya0 : a0;
+                pa[1] = b2 ? ya1 : a1;
+                pa[2] = b2 ? a0 : ya0;
+                pa[3] = b2 ? a1 : ya1;
+                pb[0] = b2 ? yb0 : c0;
+                pb[1] = b2 ? yb1 : c1;
+                pb[2] = b2 ? c0 : yb0;
+                pb[3] = b2 ? c1 : yb1;
+            }
+            // value phase: one gather per code byte, four FFMA2
+            {
+                const uint2 va = gp::rot8(U.va, rsx, rsy), vb = gp::rot8(U.vb, rsx, rsy);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t wa = j < 4 ? va.x : va.y, wb = j < 4 ? vb.x : vb.y;
+                    const unsigned long long ca =
+                        gp::lds64<0x400 + gp::CVO>(__byte_perm(wa, pk[j >> 1], sel_for(j)));
+                    const unsigned long long cb =
+                        gp::lds64<0x400 + gp::CVO>(__byte_perm(wb, pk[j >> 1], sel_for(j)));
+#pragma unroll
+                    for (int h = 0; h < HG; ++h) {
+                        ffma2(S.acc[h][j], pa[h], ca);
+                        ffma2(S.acc[h][j], pb[h], cb);
+                    }
+                }
+            }
+            {
+                const int tn = (u + 2 * W) * UT + slot;
+#if PQKV_PAIR_CLAMP
+                g4::ld8_into(U.va, vbase + row(tn, lo, hi));
+                g4::ld8_into(U.vb, vbase + row(tn + 8, lo, hi));
+#else
+                if (tn >= lo && tn < hi) U.va = g4::ld8(vbase + (int64_t)tn * M);
+                if (tn + 8 >= lo && tn + 8 < hi) U.vb = g4::ld8(vbase + (int64_t)(tn + 8) * M);
+#endif
+            }
+            u += W;
+        };
+        for (int trip = 0; trip < nunits / 2; ++trip) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) asm volatile("" : "+r"(pk[k]));
+            unit_step(Ur[0]);
+            unit_step(Ur[1]);
+        }
+        if (nunits & 1) unit_step(Ur[0]);
+
+        // ---- epilogue: this CTA's 64 dims of the pair's record per head
+        {
+            float mw = S.m;  // head w: max over the warp's slots (lanes with the same w)
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1)
+                mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+            if (lane < HG) red_m[lane * W + warp] = mw;
+        }
+        __syncthreads();  // all warps are past the main loop: the tables are free
+        float Mx[HG];
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            Mx[h] = red_m[h * W];
+#pragma unroll
+            for (int ww = 1; ww < W; ++ww) Mx[h] = fmaxf(Mx[h], red_m[h * W + ww]);
+        }
+        {
+            const float f = (S.m == -INFINITY) ? 0.f : fast_exp2(S.m - Mx[w]);
+            float lw = S.l * f;
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
+            if (lane < HG) red_l[lane * W + warp] = lw;
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                const float fh = __shfl_sync(0xffffffffu, f, (lane & ~3) | h);
+                float *rows = rows_s + ((h * W + warp) * 8 + slot) * 64;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int i = gp::lane_subspace(c, slot, w, j) - 32 * c;
+                    const float2 a = unpack2(S.acc[h][j]);
+                    rows[2 * i] = a.x * fh;
+                    rows[2 * i + 1] = a.y * fh;
+                }
+            }
+        }
+        __syncthreads();
+        {
+            constexpr int RPP = W * 8 / NPART;  // slot rows per 64-thread part
+            const int col = tid & 63, prt = tid >> 6;
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+                float cs = 0.f;
+                const float *rows = rows_s + h * W * 8 * 64;
+#pragma unroll 8
+                for (int rr = prt * RPP; rr < prt * RPP + RPP; ++rr) cs += rows[rr * 64 + col];
+                colsum[(h * NPART + prt) * 64 + col] = cs;
+            }
+        }
+        __syncthreads();
+        if (tid < HG * 64) {
+            const int h = tid >> 6, col = tid & 63;
+            float *rec = A.parts + ((int64_t)HG * (pc + sg.bh) + h) * (D + kPS);
+            float a = colsum[(h * NPART) * 64 + col];
+#pragma unroll
+            for (int pp = 1; pp < NPART; ++pp) a += colsum[(h * NPART + pp) * 64 + col];
+            rec[kPS + 64 * c + col] = a;
+            if (c == 0 && col == 0) {
+                float L = 0.f;
+#pragma unroll
+                for (int ww = 0; ww < W; ++ww) L += red_l[h * W + ww];
+                rec[0] = Mx[h] * kLn2;  // log2 units -> natural
+                rec[1] = L;
+                rec[2] = 0.f;
+                rec[3] = 0.f;
+            }
+        }
+    }
+    if (validate) {
+        validate = false;
+        if (tid < A.B && nq_fresh != nq_s[tid]) *stale_s = 1;
+        __syncthreads();
+        if (*stale_s) {
+            restart();
+            goto segments;
+        }
+    }
+    gp::cluster_sync();  // every exchange with the peer is complete
+    // ---- arrivals (both CTAs of each pair) and the last arriver's merge
+    if (A.counters != nullptr) {
+        __syncthreads();
+        constexpr int NG = NT / 128;
+        const int grp = tid >> 7, gt = tid & (D - 1);
+        int64_t p2 = cta_begin(cm, pc);
+        Segment s2;
+        for (int k = 0; next_segment(nq, A.B, Hqv, &p2, end, &s2); ++k) {
+            if (k % NG != grp) continue;
+            int c_first, c_last, len;
+            head_ctas(nq, Hqv, s2.bh, cm, &c_first, &c_last, &len);
+            if (gt == 0) {
+                int old;
+                asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "l"(A.counters + s2.bh)
+                             : "memory");
+                const bool last = (old == 2 * (c_last - c_first) + 1);
+                if (last) A.counters[s2.bh] = 0;
+                flag_s[grp] = last ? 1 : 0;
+            }
+            named_bar_sync(1 + grp, D);
+            const bool last = flag_s[grp] != 0;
+            named_bar_sync(1 + grp, D);
+            if (last) {
+                const int b2 = s2.bh / Hqv, bq0 = b2 * A.Hq + (s2.bh - b2 * Hqv) * HG;
+#pragma unroll 1
+                for (int h = 0; h < HG; ++h)
+                    finish_head(A.parts, (int64_t)HG * npairs + (int64_t)A.B * A.Hq, HG, s2.bh, h,
+                                bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged, 1, 0);
+            }
+        }
+    }
+    if (!cv_ready) mbar_wait(bar_cv, 0);
+}
+
 }  // namespace fast
 
 // ========================================================= generic path ====
@@ -2207,6 +2841,54 @@ static int launch_gqa4(const fast::Args &args, bool pdl, cudaStream_t st, const 
     return launch_status(fn);
 }
 
+#ifndef PQKV_GQA_PAIR_WARPS
+#define PQKV_GQA_PAIR_WARPS 12
+#endif
+// exact GQA (group a multiple of 4): clusters of two CTAs; the grid is the
+// even number of CTAs that can be co-resident as pairs
+template <int W>
+static int launch_gqa_pair(fast::Args args, bool pdl, cudaStream_t st, const char *fn) {
+    static int attr_set[64] = {0}, max_pairs[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = fast::decode_gqa_pair<W>;
+    const int smem = fast::gp::smem_bytes(W);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(W * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    if (dev >= 64 || !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+        int n = 0;
+        cfg.gridDim = dim3(2 * 512);
+        cfg.numAttrs = 1;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess || n <= 0)
+            return fail(PQKV_ECUDA, "%s: no co-resident CTA pairs (%s)", fn, cudaGetErrorString(e));
+        if (dev < 64) {
+            attr_set[dev] = 1;
+            max_pairs[dev] = n;
+        }
+    }
+    const int pairs = std::min(args.num_ctas / 2, dev < 64 ? max_pairs[dev] : args.num_ctas / 2);
+    if (pairs < 1) return fail(PQKV_EINVAL, "%s: the exact GQA path needs num_ctas >= 2", fn);
+    args.num_ctas = 2 * pairs;
+    cfg.gridDim = dim3(args.num_ctas);
+    cfg.numAttrs = pdl ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+    if (e != cudaSuccess) return fail(PQKV_ECUDA, "%s: %s", fn, cudaGetErrorString(e));
+    return launch_status(fn);
+}
+
 static fast::Args fast_args(const float *q, float scale, const float *ck, const float *lut, int B,
                             int Hq, int Hkv, const void *codes_k, const void *codes_v,
                             int64_t ld_tok, const int32_t *n_q, const float *cb_v, int num_ctas,
@@ -2378,6 +3060,13 @@ extern "C" int pqkv_decode_attention(
     }
     if (four)
         return launch_gqa4<PQKV_GQA4_WARPS>(a, pdl, st, "pqkv_decode_attention");
+    // exact path, a group that is a multiple of 4: CTA pairs serve four query
+    // heads each (the subspace halves split across the pair)
+    if (!(flags & (PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_ONE_HEAD_PER_CTA)) &&
+        group % 4 == 0 && num_ctas >= 2) {
+        a.share = 1;
+        return launch_gqa_pair<PQKV_GQA_PAIR_WARPS>(a, pdl, st, "pqkv_decode_attention");
+    }
     if (flags & PQKV_DECODE_F16_VALUE_CODEBOOK) {
         // even GQA groups: one CTA serves two query heads of a KV head
         if ((Hq / Hkv) % 2 == 0 && !(flags & PQKV_DECODE_ONE_HEAD_PER_CTA)) {

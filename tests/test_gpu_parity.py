@@ -314,6 +314,44 @@ def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r,num_ctas", [
+    (2, 8, 2, 5000, [4999, 1234], [5, 32], None),           # G = 4
+    (1, 8, 1, 20000, [20000], [7], None),                   # G = 8: two virtual heads
+    (4, 32, 8, 3000, [3000, 17, 0, 2222], [31, 0, 3, 17], None),  # Llama-3 grouping, ragged
+    (3, 4, 1, 700, [0, 1, 9], [0, 3, 31], 2),               # one pair, tiny / empty spans
+    (2, 16, 4, 4000, [4000, 2500], [8, 8], 9),              # odd grid: 4 pairs
+])
+def test_gqa_exact_cta_pairs(B, Hq, Hkv, cap, n_q, n_r, num_ctas):
+    """Exact GQA with a group that is a multiple of 4: clusters of two CTAs
+    (decode_gqa_pair), each CTA one half of the subspaces for four query heads,
+    partial scores exchanged through distributed shared memory -- the exact
+    path's tolerance, and the one-head-per-CTA launch agrees."""
+    got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r, num_ctas=num_ctas)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_gqa_exact_pairs_match_one_head_per_cta():
+    from paper_2504_03661_b200 import kernels as K
+    B, Hq, Hkv, n, R = 2, 8, 2, 6000, 16
+    x = _fused_inputs(B, Hq, Hkv, n, R, 19)
+    cv = K.value_codebook_layout(
+        torch.from_numpy(np.random.default_rng(19).standard_normal((64, 256, 2)).astype(
+            np.float32)).cuda(), 8)
+    nq = torch.tensor([6000, 2500], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([16, 3], dtype=torch.int32, device="cuda")
+    outs = []
+    for one in (False, True):
+        ws = K.DecodeWorkspace(B, Hq, 128, 64, 8)
+        out = torch.empty((B * Hq, 128), device="cuda")
+        for _ in range(2):  # the self-resetting counters serve a second launch
+            K.decode_attention(ws, Hkv, x["q"], 0.09, x["cbk"], x["ck"], x["cv"], nq, cv,
+                               recent_k=x["rk"], recent_v=x["rv"], n_recent=nr, k_cur=x["kc"],
+                               v_cur=x["vc"], out=out, one_head_per_cta=one)
+        assert int(ws.counters.abs().sum()) == 0
+        outs.append(out.cpu().numpy())
+    np.testing.assert_allclose(outs[0], outs[1], rtol=2e-6, atol=1e-6)
+
+
 @pytest.mark.parametrize("num_ctas", [7, 148, 150, 1000])
 def test_gqa_shared_stream_grids(num_ctas):
     """GQA 8:1 exact: the 8 CTAs of a group split the same token ranges of one
