@@ -9,3 +9,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_gqa4_lane_mapping():
     runpy.run_path(os.path.join(ROOT, "scripts", "check_gqa4_lanes.py"))
+
+
+def test_gqa_pair_lane_mapping():
+    """The exact GQA cluster-pair kernel's rotated lanes (scripts/check_gqa_pair_lanes.py)."""
+    runpy.run_path(os.path.join(ROOT, "scripts", "check_gqa_pair_lanes.py"))
