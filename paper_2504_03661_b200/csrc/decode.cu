@@ -1178,8 +1178,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 //     mod 32 (4-byte value gathers): bank-conflict free for ANY code values,
 //     with the MHA kernel's stored layout unchanged (scripts/check_gqa4_lanes.py);
 //   * the 8 lanes of a token reduce their four partial scores with a
-//     transposing butterfly (4 shuffles: each lane ends with one head's sum)
-//     and broadcast them back (3 shuffles);
+//     transposing butterfly (4 shuffles: lanes 2h, 2h + 1 end with head h's
+//     sum), keep head h's online-softmax state there (one max update, 2 NU
+//     EX2 per unit group) and shuffle the weights to the token's 8 lanes;
 //   * scores in log2 units (the table entries carry log2(e)), so a weight is
 //     one FADD + EX2; the records' maxima are converted back to natural units;
 //   * value path: the half2 codebook entry is widened to float2 and feeds one
@@ -1205,8 +1206,8 @@ struct Unit4 {
     uint2 ka, kb, va, vb;
 };
 struct State4 {
-    float m[HG], l[HG];
-    unsigned long long acc[HG][8];  // float2 per subspace of this lane
+    float m, l;                     // head (w >> 1) & 3 of this lane's token slot (owner lanes)
+    unsigned long long acc[HG][8];  // float2 per subspace of this lane, per head
 };
 
 __device__ __forceinline__ uint2 ld8(const uint8_t *p) {
@@ -1274,31 +1275,24 @@ __device__ __forceinline__ void key_scores(const uint2 k, const uint32_t (&pk)[4
     for (int h = 0; h < HG; ++h) out[h] = sp[h][0] + sp[h][1];
 }
 
-// sum v[0..3] over the 8 lanes of a token (lanes w = lane & 7), full scores of
-// all four heads back in every lane: transposing butterfly, then broadcast.
-// Head h is summed on lanes w = 2h, 2h + 1 (commutative adds: the same bits),
-// so every lane of the token ends with identical values.
-__device__ __forceinline__ void token_reduce(float (&v)[HG], int w) {
+// sum v[0..3] over the 8 lanes of a token: the transposing butterfly only --
+// lane w returns head (w >> 1) & 3 (lanes w, w ^ 1 hold the same bits)
+__device__ __forceinline__ float token_reduce_own(const float (&v)[HG], int w) {
     const bool b4 = (w & 4) != 0, b2 = (w & 2) != 0;
     const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
     float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
-    k0 += __shfl_xor_sync(0xffffffffu, s0, 4);  // heads 2 b4, 2 b4 + 1 over w, w ^ 4
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 4);
     k1 += __shfl_xor_sync(0xffffffffu, s1, 4);
     const float s = b2 ? k0 : k1;
     float k = b2 ? k1 : k0;
-    k += __shfl_xor_sync(0xffffffffu, s, 2);  // head 2 b4 + b2 over 4 lanes
-    k += __shfl_xor_sync(0xffffffffu, k, 1);  // ... over all 8
-    const float o = __shfl_xor_sync(0xffffffffu, k, 2);
-    const float p0 = b2 ? o : k, p1 = b2 ? k : o;  // heads 2 b4, 2 b4 + 1
-    const float q0 = __shfl_xor_sync(0xffffffffu, p0, 4), q1 = __shfl_xor_sync(0xffffffffu, p1, 4);
-    v[0] = b4 ? q0 : p0;
-    v[1] = b4 ? q1 : p1;
-    v[2] = b4 ? p0 : q0;
-    v[3] = b4 ? p1 : q1;
+    k += __shfl_xor_sync(0xffffffffu, s, 2);
+    return k + __shfl_xor_sync(0xffffffffu, k, 1);
 }
 
-// NU units: key phase, one running-max update per head, value phase (see
-// process_units; masked tokens take p = 0 without a branch)
+// NU units: key phase, then the softmax at the owner lanes (lane w of a token
+// holds head (w >> 1) & 3: one running-max update, 2 NU EX2), the weights
+// shuffled to the token's 8 lanes, value phase.  Masked tokens take p = 0
+// without a branch; only a running-max increase (rare) branches.
 template <int NU, typename AfterKeys>
 __device__ __forceinline__ void process4(const Unit4 *U, State4 &S, const uint32_t (&pk)[4],
                                          const uint32_t (&pv)[4], const bool *okA,
@@ -1310,30 +1304,43 @@ __device__ __forceinline__ void process4(const Unit4 *U, State4 &S, const uint32
         key_scores(U[n].kb, pk, sb[n]);
     }
     after_keys();
+    float oa[NU], ob[NU];
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
-        token_reduce(sa[n], w);
-        token_reduce(sb[n], w);
+        oa[n] = token_reduce_own(sa[n], w);
+        ob[n] = token_reduce_own(sb[n], w);
     }
-    float pa[NU][HG], pb[NU][HG];
-#pragma unroll
-    for (int h = 0; h < HG; ++h) {
+    const int base = (threadIdx.x & 31) & ~7;  // lane 0 of this token slot
+    {
         float mx = -INFINITY;
 #pragma unroll
         for (int n = 0; n < NU; ++n)
-            mx = fmaxf(mx, fmaxf(okA[n] ? sa[n][h] : -INFINITY, okB[n] ? sb[n][h] : -INFINITY));
-        if (mx > S.m[h]) {
-            const float f = fast_exp2(S.m[h] - mx);
-            S.l[h] *= f;
+            mx = fmaxf(mx, fmaxf(okA[n] ? oa[n] : -INFINITY, okB[n] ? ob[n] : -INFINITY));
+        const bool up = mx > S.m;
+        if (__any_sync(0xffffffffu, up)) {  // rare: rescale the slot's accumulators
+            const float f = up ? fast_exp2(S.m - mx) : 1.f;
+            if (up) {
+                S.l *= f;
+                S.m = mx;
+            }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) fmul2(S.acc[h][k], f);
-            S.m[h] = mx;
+            for (int h = 0; h < HG; ++h) {
+                const float fh = __shfl_sync(0xffffffffu, f, base | (2 * h));
+#pragma unroll
+                for (int k = 0; k < 8; ++k) fmul2(S.acc[h][k], fh);
+            }
         }
+    }
+    float pa[NU][HG], pb[NU][HG];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) {
-            pa[n][h] = okA[n] ? fast_exp2(sa[n][h] - S.m[h]) : 0.f;
-            pb[n][h] = okB[n] ? fast_exp2(sb[n][h] - S.m[h]) : 0.f;
-            S.l[h] += pa[n][h] + pb[n][h];
+    for (int n = 0; n < NU; ++n) {
+        const float qa = okA[n] ? fast_exp2(oa[n] - S.m) : 0.f;
+        const float qb = okB[n] ? fast_exp2(ob[n] - S.m) : 0.f;
+        S.l += qa + qb;
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            pa[n][h] = __shfl_sync(0xffffffffu, qa, base | (2 * h));
+            pb[n][h] = __shfl_sync(0xffffffffu, qb, base | (2 * h));
         }
     }
 #pragma unroll
@@ -1596,13 +1603,12 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
             continue;
         }
         State4 S;
+        S.m = -INFINITY;
+        S.l = 0.f;
 #pragma unroll
-        for (int h = 0; h < HG; ++h) {
-            S.m[h] = -INFINITY;
-            S.l[h] = 0.f;
+        for (int h = 0; h < HG; ++h)
 #pragma unroll
             for (int k = 0; k < 8; ++k) S.acc[h][k] = 0ull;
-        }
         int u = u0 + wu;
         const int nunits = max(0, (u1 - u0 - wu + W - 1) / W);
         constexpr int64_t kStep = (int64_t)W * UT * M;  // bytes per unit step of a warp
@@ -1648,13 +1654,13 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
         }
 
         // ---- epilogue: one (m, l, acc) record per head for this segment
+        // (lane w = 2h of each slot holds head h's state)
+        {
+            float mw = S.m;
 #pragma unroll
-        for (int h = 0; h < HG; ++h) {
-            float mw = S.m[h];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
+            for (int off = 8; off < 32; off <<= 1)
                 mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
-            if (lane == 0) red_m[h * W + warp] = mw;
+            if (lane < 8 && (lane & 1) == 0) red_m[(lane >> 1) * W + warp] = mw;
         }
         __syncthreads();  // all warps are past the main loop: the table is free
         float Mx[HG];
@@ -1663,11 +1669,17 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
             Mx[h] = red_m[h * W];
 #pragma unroll
             for (int ww = 1; ww < W; ++ww) Mx[h] = fmaxf(Mx[h], red_m[h * W + ww]);
-            const float f = (S.m[h] == -INFINITY) ? 0.f : fast_exp2(S.m[h] - Mx[h]);
-            float lw = (w == 0) ? S.l[h] * f : 0.f;
+        }
+        const float f_own = (S.m == -INFINITY) ? 0.f : fast_exp2(S.m - Mx[(w >> 1) & 3]);
+        {
+            float lw = (w & 1) ? 0.f : S.l * f_own;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
-            if (lane == 0) red_l[h * W + warp] = lw;
+            for (int off = 8; off < 32; off <<= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
+            if (lane < 8 && (lane & 1) == 0) red_l[(lane >> 1) * W + warp] = lw;
+        }
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+            const float f = __shfl_sync(0xffffffffu, f_own, (lane & ~7) | (2 * h));
             float *rows = rows_s + ((h * W + warp) * 4 + slot) * D;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
