@@ -816,9 +816,9 @@ def run_ours(args):
     del replay, w
     torch.cuda.empty_cache()
 
-    # ---- N > 1: the head-sharded and sequence-split configs beside it -------
-    if world > 1 and args.config == "llama2-32k" and not args.no_extra_configs:
-        for extra in ("llama3-gqa-32k", "llama3-gqa-128k"):
+    # ---- the GQA configs beside it (N > 1: head-sharded and sequence-split) --
+    if args.config == "llama2-32k" and not args.no_extra_configs:
+        for extra in ("llama3-gqa-32k", "llama3-gqa-128k") if world > 1 else ("llama3-gqa-32k",):
             try:
                 pe = shard_plan(extra, rank, world)
                 we = Workload(args, pe, dev, stream, True)
@@ -833,7 +833,25 @@ def run_ours(args):
                 ent["roofline_frac"] = (we.bytes_per_launch * we.L /
                                         ((mse - ent.get("merge_ms_per_step", 0.0)) * 1e-3)
                                         / 1e9 / hbm_peak)
-                del re_, we
+                ent["kernel"] = ("decode_gqa_pair (exact fp32, clusters of two CTAs, four query "
+                                 "heads per pair)")
+                del re_
+                if not args.no_f16_mode:
+                    # stated tolerance: fp16 value codebook + one packed fp16 key table
+                    # for four query heads per CTA (decode_gqa4_f16)
+                    r16 = we.capture(True, keys16=True)
+                    ms16 = we.time(r16, args.steps, args.warmup, barrier, max_over_ranks)
+                    ent["f16_key_table"] = {
+                        "value": pe["jobs"] * we.B * 1e3 / ms16, "unit": "tokens/s",
+                        "ms_per_step": ms16,
+                        "roofline_frac": (we.bytes_per_launch * we.L /
+                                          ((ms16 - ent.get("merge_ms_per_step", 0.0)) * 1e-3)
+                                          / 1e9 / hbm_peak),
+                        "kernel": "decode_gqa4_f16",
+                        "tolerance": "rtol 2e-3, atol 2e-4 vs the fp64 reference "
+                                     "(tests/test_gpu_gqa_tables.py)"}
+                    del r16
+                del we
                 torch.cuda.empty_cache()
             except Exception as e:  # noqa: BLE001 -- the headline line still prints
                 ent = {"error": f"{type(e).__name__}: {e!s:.200}"}
