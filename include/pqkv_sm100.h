@@ -342,6 +342,19 @@ int pqkv_read_cache_dumps(const char *path, int heads, int d, int M, int nbits,
 int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns,
                             void *stream);
 
+/* ---- per-token appends with device-resident lengths --------------------
+ * A cache's (n_q, n_recent) as int32 lens[2] on the device, updated in stream
+ * order, so that a decode step needs no host->device length transfer.
+ * pqkv_append_recent replaces LayerKVCache.append_decode's row write
+ * (kv_cache.py:188-200): rows n = lens[1] of rk / rv (row stride d) take the d
+ * floats of k / v, then lens[1] = n + 1.  pqkv_publish_lengths is a flush's
+ * single publication point (kv_cache.py:228) on the device: lens[0] += batch,
+ * lens[1] -= batch (the recent base pointer the caller passes moves by batch
+ * rows). */
+int pqkv_append_recent(const float *k, const float *v, float *rk, float *rv,
+                       int32_t *lens, int d, void *stream);
+int pqkv_publish_lengths(int32_t *lens, int batch, void *stream);
+
 /* ---- paged code store (growth without copies) ---------------------------
  * Replaces the reference's grow-by-copy code store (kv_cache.py:74-76,
  * 217-228).  A store reserves n_regions * region_bytes of virtual address

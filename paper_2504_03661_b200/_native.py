@@ -69,6 +69,8 @@ SIGNATURES = {
     "pqkv_read_cache_dumps": (_I, [ctypes.c_char_p, _I, _I, _I, _I, _I64, _I, _P, _P, _I64, _I,
                                    _P, _P, _I64, _P]),
     "pqkv_debug_delayed_fill": (_I, [_P, _I, _I, ctypes.c_longlong, _P]),
+    "pqkv_append_recent": (_I, [_P, _P, _P, _P, _P, _I, _P]),
+    "pqkv_publish_lengths": (_I, [_P, _I, _P]),
     "pqkv_vstore_granularity": (_I64, [_I]),
     "pqkv_vstore_create": (_I, [_I, _I64, _I64, _P, _P]),
     "pqkv_vstore_ensure": (_I, [_P, _I64]),

@@ -259,10 +259,43 @@ __global__ void delayed_fill_kernel(int32_t *p, int n, int32_t v, long long ns) 
     for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
 }
 
+// append_decode's row write (kv_cache.py:188-200) with the recent length on
+// the device: rows n of rk / rv (n = *lens[1]) take k / v, then *lens[1] = n + 1
+__global__ void append_recent_kernel(const float *__restrict__ k, const float *__restrict__ v,
+                                     float *rk, float *rv, int32_t *lens, int d) {
+    const int n = lens[1];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        rk[(int64_t)n * d + i] = k[i];
+        rv[(int64_t)n * d + i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) lens[1] = n + 1;
+}
+
+// a flush's publication on the device: n_q += batch, n_recent -= batch
+__global__ void publish_lengths_kernel(int32_t *lens, int batch) {
+    lens[0] += batch;
+    lens[1] -= batch;
+}
+
 }  // namespace
 }  // namespace pqkv
 
 using namespace pqkv;
+
+extern "C" int pqkv_append_recent(const float *k, const float *v, float *rk, float *rv,
+                                  int32_t *lens, int d, void *stream) {
+    PQKV_CHECK_ARG(k && v && rk && rv && lens && d > 0 && d <= 4096,
+                   "pqkv_append_recent: bad arguments");
+    append_recent_kernel<<<1, 128, 0, as_stream(stream)>>>(k, v, rk, rv, lens, d);
+    return launch_status("pqkv_append_recent");
+}
+
+extern "C" int pqkv_publish_lengths(int32_t *lens, int batch, void *stream) {
+    PQKV_CHECK_ARG(lens && batch >= 0, "pqkv_publish_lengths: bad arguments");
+    publish_lengths_kernel<<<1, 1, 0, as_stream(stream)>>>(lens, batch);
+    return launch_status("pqkv_publish_lengths");
+}
 
 extern "C" int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns, void *stream) {
     PQKV_CHECK_ARG(p && n >= 0 && ns >= 0 && ns < 10000000000LL,

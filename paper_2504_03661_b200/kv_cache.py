@@ -28,6 +28,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _native as N
 from . import kernels as K
 from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_device
 
@@ -83,6 +84,11 @@ class LayerKVCache:
         rcap = max(64, 2 * (recent_capacity + flush_threshold))
         self._rk = torch.zeros((rcap, cfg.d), dtype=torch.float32, device=self.device)
         self._rv = torch.zeros_like(self._rk)
+        # (n_q, recent length) on the device, in the callers' stream order: the
+        # per-token append bumps it and a publication moves a batch from the
+        # second to the first (pqkv_append_recent / pqkv_publish_lengths), so a
+        # decode step reads its lengths without a host->device transfer
+        self._lens = torch.zeros(2, dtype=torch.int32, device=self.device)
         self._r0 = 0          # first live recent row in _rk/_rv
         self._rlen = 0        # live recent rows (published + in-flight flushes)
         self._n_total = 0
@@ -199,18 +205,31 @@ class LayerKVCache:
                 self._rlen += keep
             self._n_q += n_enc
             self._n_total += n
+            self._set_device_lengths()
+
+    def _set_device_lengths(self) -> None:
+        """lens <- (n_q, recent length) after a bulk state change (prefill,
+        restore), enqueued on the current stream."""
+        self._lens.copy_(torch.tensor([self._n_q, self._rlen], dtype=torch.int32),
+                         non_blocking=False)
+
+    def _publish_device(self, batch: int) -> None:
+        N.call("pqkv_publish_lengths", N.ptr(self._lens), batch,
+               N.stream_ptr(None, self.device))
 
     def append_decode(self, k_n, v_n) -> None:
         """Append the current token's full-precision KV pair; flush whole
         batches once the recent window reaches the threshold."""
-        k = self._check_row(k_n, "k_n")
-        v = self._check_row(v_n, "v_n")
+        k = self._check_row(k_n, "k_n").contiguous()
+        v = self._check_row(v_n, "v_n").contiguous()
         with self._lock:
             self._publish_completed()
             self._ensure_recent(1)
-            a = self._r0 + self._rlen
-            self._rk[a].copy_(k)
-            self._rv[a].copy_(v)
+            # row r0 + rlen of the ring, and the device recent length + 1
+            off = self._r0 * self.config.d * 4
+            N.call("pqkv_append_recent", N.ptr(k), N.ptr(v), self._rk.data_ptr() + off,
+                   self._rv.data_ptr() + off, N.ptr(self._lens), self.config.d,
+                   N.stream_ptr(None, self.device))
             self._rlen += 1
             self._n_total += 1
             needed = self._flush_needed_locked()
@@ -274,6 +293,7 @@ class LayerKVCache:
             self._n_q += batch          # single publication point
             self._r0 += batch
             self._rlen -= batch
+            self._publish_device(batch)
             return
         main = torch.cuda.current_stream(self.device)
         self._side.wait_stream(main)    # the rows were written on the main stream
@@ -303,6 +323,7 @@ class LayerKVCache:
             self._n_q += batch          # single publication point
             self._r0 += batch
             self._rlen -= batch
+            self._publish_device(batch)
 
     def _wait_pending(self) -> None:
         self._publish_completed(block=True)
@@ -335,6 +356,7 @@ class LayerKVCache:
                 self._rv[:r] = self._rows(snap.recent_V, "recent_V").reshape(r, -1)
             self._r0, self._rlen = 0, r
             self._n_total = snap.n_total
+            self._set_device_lengths()
 
     def _load_device(self, n_q: int, r: int, fill) -> None:
         """Restore into an empty cache: fill(codes_k, codes_v, recent_k,
@@ -350,6 +372,7 @@ class LayerKVCache:
                 fill(self._store_k, self._store_v, self._rk, self._rv)
             self._n_q, self._r0, self._rlen = n_q, 0, r
             self._n_total = n_q + r
+            self._set_device_lengths()
 
     # -- reads -------------------------------------------------------------------
     def raw_snapshot(self):
@@ -375,6 +398,18 @@ class LayerKVCache:
             rk = self._rk[self._r0: self._r0 + self._rlen]
             rv = self._rv[self._r0: self._r0 + self._rlen]
             return (self._store_k[:n_q], self._store_v[:n_q], rk, rv, n_q, self._n_total)
+
+    def step_view(self):
+        """decode_step's per-token view: (codes_k, codes_v, recent_K,
+        recent_V, lens, n_q, recent length) -- the code stores and the recent
+        ring from its first live row, and the device lengths lens = (n_q,
+        recent length) in stream order (the kernel reads its lengths there;
+        the host values are for accounting)."""
+        with self._lock:
+            self._publish_completed()
+            rk = self._rk[self._r0:]
+            rv = self._rv[self._r0:]
+            return (self._store_k, self._store_v, rk, rv, self._lens, self._n_q, self._rlen)
 
     @property
     def code_layout(self) -> str:
