@@ -76,6 +76,33 @@ int pqkv_encode_batched(const void *x, int x_dtype, int batches, int64_t n, int 
                         int64_t c_bstride, int M, int nbits, void *codes, int64_t ld_codes,
                         int64_t codes_bstride, int64_t rot_base, void *stream);
 
+/* ---- candidate grid of the dsub = 2 encoder (nbits <= 8) ----------------
+ * Per subspace a 64 x 64 grid over the centroids' bounding box (+25% each
+ * side); each cell lists the <= 24 centroids that can be the nearest -- or
+ * within 1/128 relative of it -- for a point of the cell.  pqkv_encode_grid
+ * runs pqkv_encode's fp32 filter over the cell's list instead of all ksub
+ * centroids (same keys, same near-tie test, same exact fp64 re-scan over all
+ * centroids on a near tie; points outside the grid and crowded cells scan all
+ * of them), so its codes are pqkv_encode's -- the reference's -- bit for bit.
+ * pqkv_encode_grid_bytes: bytes of a codebook's grid (0: no grid for this
+ * geometry); pqkv_build_encode_grid fills it from the centroids (once per
+ * codebook); grid == NULL makes pqkv_encode_grid a plain pqkv_encode.
+ * pqkv_encode_batched_grid: the fp32 batched form (grid at grid + z *
+ * g_bstride bytes). */
+int64_t pqkv_encode_grid_bytes(int d, int M, int nbits);
+int pqkv_build_encode_grid(const float *centroids, int d, int M, int nbits,
+                           void *grid, void *stream);
+int pqkv_encode_grid(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
+                     const float *centroids, const void *grid, int M, int nbits,
+                     void *codes, int64_t ld_codes, int64_t rot_base, void *stream);
+int pqkv_encode_batched_grid(const void *x, int batches, int64_t n, int d,
+                             int64_t ld_x, int64_t x_bstride,
+                             const float *centroids, int64_t c_bstride,
+                             const void *grid, int64_t g_bstride, int M, int nbits,
+                             void *codes, int64_t ld_codes,
+                             int64_t codes_bstride, int64_t rot_base,
+                             void *stream);
+
 /* Convert n rows between the row layout and the decode layout (to_decode = 1:
  * rows -> decode, 0: decode -> rows); row 0 is token index t_first. */
 int pqkv_relayout_codes(const void *src, int64_t ld_src, void *dst,

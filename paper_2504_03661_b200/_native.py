@@ -36,6 +36,11 @@ SIGNATURES = {
     "pqkv_encode": (_I, [_P, _I, _I64, _I, _I64, _P, _I, _I, _P, _I64, _I64, _P]),
     "pqkv_encode_batched": (_I, [_P, _I, _I, _I64, _I, _I64, _I64, _P, _I64, _I, _I, _P, _I64,
                                  _I64, _I64, _P]),
+    "pqkv_encode_grid_bytes": (_I64, [_I, _I, _I]),
+    "pqkv_build_encode_grid": (_I, [_P, _I, _I, _I, _P, _P]),
+    "pqkv_encode_grid": (_I, [_P, _I, _I64, _I, _I64, _P, _P, _I, _I, _P, _I64, _I64, _P]),
+    "pqkv_encode_batched_grid": (_I, [_P, _I, _I64, _I, _I64, _I64, _P, _I64, _P, _I64, _I, _I,
+                                      _P, _I64, _I64, _I64, _P]),
     "pqkv_relayout_codes": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P]),
     "pqkv_reconstruct": (_I, [_P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
     "pqkv_build_lut": (_I, [_P, _I64, _I, _P, _I, _I, _F, _P, _P]),

@@ -14,6 +14,8 @@
 // vectors, with that subspace's centroids and norms staged in shared memory
 // as float64 (warp-uniform broadcast reads).  FP64 bound: 256 * ~7 DFMA-class
 // ops per (vector, subspace) for m64b8.
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -325,6 +327,271 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
     }
 }
 
+// ---- dsub == 2 with a candidate grid (nbits <= 8) ------------------------
+// A 2-D subspace is a plane: per subspace a 64 x 64 grid over the centroids'
+// bounding box (+25% each side) lists, per cell, every centroid that can be
+// the nearest -- or within 1/128 relative (+ an absolute margin) of it -- for
+// a point of the cell (cells widened by 2% for the index rounding).  The
+// bound: for x in cell B, d(x, nearest)^2 <= U = min_c max_{y in B} |y - c|^2,
+// so a centroid with min_{y in B} |y - c|^2 > U (1 + 1/128) + abs is never
+// within the filter's tolerance of the best.  The encoder then runs the same
+// fp32 filter (the same keys, the same near-tie test, the same exact fp64
+// re-scan over ALL centroids on a near tie) over the cell's list instead of
+// all ksub centroids; points outside the grid and cells whose list did not
+// fit scan all of them.  Results are therefore the fp32 filter's, i.e. the
+// reference's, bit for bit.
+// Record per subspace: header (lo_x, lo_y, 1/h_x, 1/h_y, pool bytes used) |
+// offs[cells] uint16 | cnt[cells] uint8 (255: full scan) | pool of uint8
+// centroid indices (at most EG_POOL bytes, so a CTA stages ~45 KB).
+constexpr int EG = 64;                              // cells per axis
+constexpr int EG_CELLS = EG * EG;
+constexpr int EG_POOL = 28 * 1024;                  // candidate-index bytes per subspace
+constexpr int EG_LMAX = 24;                         // a longer list -> full scan
+constexpr int EG_HDR = 32;
+constexpr int EG_OFFS = EG_HDR, EG_CNT = EG_OFFS + 2 * EG_CELLS, EG_PL = EG_CNT + EG_CELLS;
+constexpr int EG_REC = EG_PL + EG_POOL;             // bytes per subspace
+static_assert(EG_REC % 16 == 0 && EG_PL % 16 == 0, "grid records stay 16-byte aligned");
+
+__global__ void __launch_bounds__(256) build_encode_grid_kernel(const float *__restrict__ cents,
+                                                                int ksub,
+                                                                unsigned char *__restrict__ grid) {
+    const int i = blockIdx.x;
+    __shared__ double2 c_s[256];
+    __shared__ float hdr_s[4];
+    __shared__ double absm_s;
+    __shared__ unsigned char n_s[EG_CELLS];
+    __shared__ uint16_t off_s[EG_CELLS];
+    __shared__ int used_s;
+    const float2 *ci = reinterpret_cast<const float2 *>(cents + (size_t)i * ksub * 2);
+    unsigned char *rec = grid + (size_t)i * EG_REC;
+    for (int c = threadIdx.x; c < ksub; c += blockDim.x) {
+        const float2 f = __ldg(ci + c);
+        c_s[c] = make_double2(f.x, f.y);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY, amax = 0.0;
+        for (int c = 0; c < ksub; ++c) {
+            x0 = fmin(x0, c_s[c].x);
+            x1 = fmax(x1, c_s[c].x);
+            y0 = fmin(y0, c_s[c].y);
+            y1 = fmax(y1, c_s[c].y);
+            amax = fmax(amax, fmax(fabs(c_s[c].x), fabs(c_s[c].y)));
+        }
+        const double floor_span = fmax(amax * 0x1p-10, 1e-20);
+        const double sx = fmax(x1 - x0, floor_span), sy = fmax(y1 - y0, floor_span);
+        const float lx = (float)(x0 - 0.25 * sx), ly = (float)(y0 - 0.25 * sy);
+        hdr_s[0] = lx;
+        hdr_s[1] = ly;
+        hdr_s[2] = (float)(EG / (1.5 * sx));
+        hdr_s[3] = (float)(EG / (1.5 * sy));
+        const double ext = fmax(amax, fmax(fabs((double)lx), fabs((double)ly))) + 2.0 * fmax(sx, sy);
+        absm_s = 1e-9 * ext * ext;  // absolute margin (>> the filter's 1e-13 (|x|^2 + max|c|^2))
+    }
+    __syncthreads();
+    const double lx = hdr_s[0], ly = hdr_s[1];
+    const double hx = 1.0 / (double)hdr_s[2], hy = 1.0 / (double)hdr_s[3];
+    const double absm = absm_s;
+    // pass 1: list lengths; pass 2 (after the offsets): the lists
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int cell = threadIdx.x; cell < EG_CELLS; cell += blockDim.x) {
+            const int ix = cell % EG, iy = cell / EG;
+            const double bx0 = lx + (ix - 0.02) * hx, bx1 = lx + (ix + 1.02) * hx;
+            const double by0 = ly + (iy - 0.02) * hy, by1 = ly + (iy + 1.02) * hy;
+            if (pass == 1 && n_s[cell] == 255) continue;
+            double U = INFINITY;
+            for (int c = 0; c < ksub; ++c) {
+                const double dx = fmax(fabs(c_s[c].x - bx0), fabs(c_s[c].x - bx1));
+                const double dy = fmax(fabs(c_s[c].y - by0), fabs(c_s[c].y - by1));
+                U = fmin(U, dx * dx + dy * dy);
+            }
+            const double thr = U * (1.0 + 1.0 / 128) + absm;
+            int n = 0;
+            unsigned char *dst = rec + EG_PL + (pass ? off_s[cell] : 0);
+            for (int c = 0; c < ksub; ++c) {
+                const double dx = fmax(0.0, fmax(bx0 - c_s[c].x, c_s[c].x - bx1));
+                const double dy = fmax(0.0, fmax(by0 - c_s[c].y, c_s[c].y - by1));
+                if (dx * dx + dy * dy <= thr) {
+                    if (pass == 1) dst[n] = (unsigned char)c;
+                    ++n;
+                }
+            }
+            if (pass == 0) n_s[cell] = n <= EG_LMAX ? (unsigned char)n : (unsigned char)255;
+        }
+        __syncthreads();
+        if (pass == 0 && threadIdx.x == 0) {  // offsets; lists past the pool -> full scan
+            int off = 0;
+            for (int cell = 0; cell < EG_CELLS; ++cell) {
+                const int n = n_s[cell];
+                if (n == 255 || off + n > EG_POOL) {
+                    n_s[cell] = 255;
+                    off_s[cell] = 0;
+                } else {
+                    off_s[cell] = (uint16_t)off;
+                    off += n;
+                }
+            }
+            used_s = off;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) reinterpret_cast<float *>(rec)[threadIdx.x] = hdr_s[threadIdx.x];
+    if (threadIdx.x == 4) reinterpret_cast<int *>(rec)[4] = used_s;
+    for (int cell = threadIdx.x; cell < EG_CELLS; cell += blockDim.x) {
+        reinterpret_cast<uint16_t *>(rec + EG_OFFS)[cell] = off_s[cell];
+        rec[EG_CNT + cell] = n_s[cell];
+    }
+}
+
+#ifndef PQKV_ENC_GRID_VPT
+#define PQKV_ENC_GRID_VPT 4  // vectors per thread per pass (their loads in flight together)
+#endif
+template <typename TX, typename CT, int VPT>
+__global__ void __launch_bounds__(256) encode_dsub2_grid(const TX *__restrict__ x, int64_t n,
+                                                         int64_t ld_x,
+                                                         const float *__restrict__ cents,
+                                                         const unsigned char *__restrict__ grid,
+                                                         int ksub, CT *__restrict__ codes,
+                                                         int64_t ld_codes, int64_t rot_base,
+                                                         int64_t x_bs, int64_t c_bs, int64_t g_bs,
+                                                         int64_t codes_bs) {
+    x += blockIdx.z * x_bs;
+    cents += blockIdx.z * c_bs;
+    grid += blockIdx.z * g_bs;
+    codes += blockIdx.z * codes_bs;
+    extern __shared__ double sm[];
+    double2 *c_s = reinterpret_cast<double2 *>(sm);                   // [ksub]
+    double *cc_s = sm + 2 * (size_t)ksub;                              // [ksub]
+    float2 *cf_s = reinterpret_cast<float2 *>(sm + 3 * (size_t)ksub);  // [ksub]
+    unsigned char *g_s = reinterpret_cast<unsigned char *>(sm + 4 * (size_t)ksub);  // record
+    __shared__ float ccmax_s;
+    const int i = blockIdx.x;
+    const float2 *ci = reinterpret_cast<const float2 *>(cents + (size_t)i * ksub * 2);
+    const unsigned char *rec = grid + (size_t)i * EG_REC;
+    if (threadIdx.x == 0) ccmax_s = 0.f;
+    {
+        // header, offsets, counts and the used part of the pool
+        const int used = __ldg(reinterpret_cast<const int *>(rec) + 4);
+        const int bytes = EG_PL + ((used + 15) & ~15);
+        const uint4 *src = reinterpret_cast<const uint4 *>(rec);
+        uint4 *dst = reinterpret_cast<uint4 *>(g_s);
+        for (int k = threadIdx.x; k < bytes / 16; k += blockDim.x) dst[k] = __ldg(src + k);
+    }
+    __syncthreads();
+    float ccmax = 0.f;
+    for (int c = threadIdx.x; c < ksub; c += blockDim.x) {
+        const float2 f = __ldg(ci + c);
+        const double a = f.x, b = f.y;
+        c_s[c] = make_double2(a, b);
+        cc_s[c] = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+        cf_s[c] = f;
+        ccmax = fmaxf(ccmax, (float)cc_s[c]);
+    }
+    atomicMax(reinterpret_cast<int *>(&ccmax_s), __float_as_int(ccmax));
+    __syncthreads();
+    ccmax = ccmax_s;
+    const float *hdr = reinterpret_cast<const float *>(g_s);
+    const float lx = hdr[0], ly = hdr[1], ihx = hdr[2], ihy = hdr[3];
+    const uint16_t *off_s = reinterpret_cast<const uint16_t *>(g_s + EG_OFFS);
+    const unsigned char *cnt_s = g_s + EG_CNT;
+    const unsigned char *pool_s = g_s + EG_PL;
+    const uint32_t cmask = (uint32_t)ksub - 1u;
+    const float trunc = __uint_as_float(0x3f800000u | cmask) - 1.f;  // ksub * 2^-23
+
+    for (int64_t v0 = ((int64_t)blockIdx.y * VPT) * blockDim.x + threadIdx.x; v0 < n;
+         v0 += (int64_t)gridDim.y * VPT * blockDim.x) {
+        float xa[VPT], xb[VPT];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {  // every load of the pass in flight at once
+            const int64_t v = v0 + (int64_t)k * blockDim.x;
+            const int64_t vv = v < n ? v : n - 1;
+            xa[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2);
+            xb[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2 + 1);
+        }
+#pragma unroll 1
+        for (int k = 0; k < VPT; ++k) {
+            const int64_t v = v0 + (int64_t)k * blockDim.x;
+            if (v >= n) break;
+            const float xf0 = xa[k], xf1 = xb[k];
+            const float fx = (xf0 - lx) * ihx, fy = (xf1 - ly) * ihy;
+            int nc = 255, off = 0;
+            if (fx >= 0.f && fx < (float)EG && fy >= 0.f && fy < (float)EG) {
+                const int cell = (int)fy * EG + (int)fx;
+                nc = cnt_s[cell];
+                off = off_s[cell];
+            }
+            // best / second-best keys (encode_dsub2_filter): the same distance
+            // formula, so the same keys for the same centroids
+            auto key_of = [&](int c) {
+                const float2 cv = cf_s[c];
+                const float dx = xf0 + (-cv.x), dy = xf1 + (-cv.y);
+                return (__float_as_uint(fmaf(dy, dy, dx * dx)) & ~cmask) | (uint32_t)c;
+            };
+            uint32_t b1 = 0xffffffffu, b2;
+            if (nc != 255) {
+                b2 = 0x7f7fffffu;  // a one-entry list has no competitor: FLT_MAX
+                for (int k2 = 0; k2 < nc; ++k2) {
+                    const uint32_t key = key_of(pool_s[off + k2]);
+                    b2 = min(b2, max(b1, key));
+                    b1 = min(b1, key);
+                }
+            } else {
+                b2 = 0xffffffffu;
+                for (int c = 0; c < ksub; ++c) {
+                    const uint32_t key = key_of(c);
+                    b2 = min(b2, max(b1, key));
+                    b1 = min(b1, key);
+                }
+            }
+            const float xx = fmaf(xf1, xf1, xf0 * xf0);
+            const float d1 = __uint_as_float(b1 & ~cmask), d2k = __uint_as_float(b2 & ~cmask);
+            const float tol = (2e-6f + 2.f * trunc) * d1 + 1e-13f * (xx + ccmax) + 1e-30f;
+            int a = (int)(b1 & cmask);
+            if (!(d2k > d1 + tol)) {  // near tie: the exact scan over every centroid
+                const double x0 = (double)xf0, x1 = (double)xf1;
+                const double xxd = __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1));
+                double best = INFINITY;
+                for (int c = 0; c < ksub; ++c) {
+                    const double2 cv = c_s[c];
+                    const double xc = __fma_rn(x1, cv.y, __dmul_rn(x0, cv.x));
+                    const double d2 = fmax(__dadd_rn(__fma_rn(-2.0, xc, xxd), cc_s[c]), 0.0);
+                    if (d2 < best) {
+                        best = d2;
+                        a = c;
+                    }
+                }
+            }
+            codes[code_cell(v, i, ld_codes, rot_base)] = (CT)a;
+        }
+    }
+}
+
+template <typename TX, typename CT>
+int launch_dsub2_grid(const void *x, int64_t n, int64_t ld_x, const float *cents,
+                      const unsigned char *grid, int M, int ksub, void *codes, int64_t ld_codes,
+                      int64_t rot_base, cudaStream_t st, int batches = 1, int64_t x_bs = 0,
+                      int64_t c_bs = 0, int64_t g_bs = 0, int64_t codes_bs = 0) {
+    constexpr int VPT = PQKV_ENC_GRID_VPT;
+    const size_t smem = (size_t)256 * 4 * sizeof(double) + EG_REC;  // the pool's worst case
+    auto k = encode_dsub2_grid<TX, CT, VPT>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
+        attr = true;
+    }
+    // persistent row blocks: ~4 CTAs (of ~54 KB shared memory) per SM over
+    // (subspace, row block) pairs
+    int64_t blocks = (n + 256 * VPT - 1) / (256 * VPT);
+    const int64_t target = std::max<int64_t>(1, (int64_t)4 * 148 / std::max(1, M * batches));
+    blocks = std::min<int64_t>(blocks, target);
+    dim3 g((unsigned)M, (unsigned)std::min<int64_t>(blocks, 65535), (unsigned)batches);
+    k<<<g, 256, smem, st>>>((const TX *)x, n, ld_x, cents, grid, ksub, (CT *)codes, ld_codes,
+                            rot_base, x_bs, c_bs, g_bs, codes_bs);
+    return launch_status("pqkv_encode_grid");
+}
+
 template <typename TX, typename CT, int VPT>
 int launch_dsub2_filter_vpt(const void *x, int64_t n, int64_t ld_x, const float *cents, int M,
                             int ksub, void *codes, int64_t ld_codes, int64_t rot_base,
@@ -508,6 +775,75 @@ extern "C" int pqkv_encode_batched(const void *x, int x_dtype, int batches, int6
         if (rc) return rc;
     }
     return PQKV_OK;
+}
+
+static bool grid_geometry(int d, int M, int nbits) { return d == 2 * M && nbits <= 8; }
+
+extern "C" int64_t pqkv_encode_grid_bytes(int d, int M, int nbits) {
+    return (geometry_ok(d, M, nbits) && grid_geometry(d, M, nbits)) ? (int64_t)M * EG_REC : 0;
+}
+
+extern "C" int pqkv_build_encode_grid(const float *centroids, int d, int M, int nbits, void *grid,
+                                      void *stream) {
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits) && grid_geometry(d, M, nbits),
+                   "pqkv_build_encode_grid: the candidate grid exists for dsub = 2, nbits <= 8");
+    PQKV_CHECK_ARG(centroids && grid, "pqkv_build_encode_grid: null pointer");
+    build_encode_grid_kernel<<<M, 256, 0, as_stream(stream)>>>(centroids, 1 << nbits,
+                                                               (unsigned char *)grid);
+    return launch_status("pqkv_build_encode_grid");
+}
+
+extern "C" int pqkv_encode_grid(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,
+                                const float *centroids, const void *grid, int M, int nbits,
+                                void *codes, int64_t ld_codes, int64_t rot_base, void *stream) {
+    if (grid == nullptr)
+        return pqkv_encode(x, x_dtype, n, d, ld_x, centroids, M, nbits, codes, ld_codes, rot_base,
+                           stream);
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits) && grid_geometry(d, M, nbits),
+                   "pqkv_encode_grid: the candidate grid exists for dsub = 2, nbits <= 8");
+    PQKV_CHECK_ARG(n >= 0, "pqkv_encode_grid: n must be >= 0");
+    PQKV_CHECK_ARG(ld_x >= d && ld_codes >= M, "pqkv_encode_grid: row strides too small");
+    if (n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(x && centroids && codes, "pqkv_encode_grid: null pointer");
+    PQKV_CHECK_ARG(rot_base < 0 || is_fast_geometry(d, M, nbits),
+                   "pqkv_encode_grid: the decode layout exists only for m64b8");
+    cudaStream_t st = as_stream(stream);
+    const int ksub = 1 << nbits;
+    const unsigned char *g = (const unsigned char *)grid;
+    switch (x_dtype) {
+        case PQKV_DTYPE_F32:
+            return launch_dsub2_grid<float, uint8_t>(x, n, ld_x, centroids, g, M, ksub, codes,
+                                                     ld_codes, rot_base, st);
+        case PQKV_DTYPE_BF16:
+            return launch_dsub2_grid<__nv_bfloat16, uint8_t>(x, n, ld_x, centroids, g, M, ksub,
+                                                             codes, ld_codes, rot_base, st);
+        case PQKV_DTYPE_F16:
+            return launch_dsub2_grid<__half, uint8_t>(x, n, ld_x, centroids, g, M, ksub, codes,
+                                                      ld_codes, rot_base, st);
+        default:
+            return fail(PQKV_EINVAL, "pqkv_encode_grid: unknown dtype %d", x_dtype);
+    }
+}
+
+extern "C" int pqkv_encode_batched_grid(const void *x, int batches, int64_t n, int d,
+                                        int64_t ld_x, int64_t x_bstride, const float *centroids,
+                                        int64_t c_bstride, const void *grid, int64_t g_bstride,
+                                        int M, int nbits, void *codes, int64_t ld_codes,
+                                        int64_t codes_bstride, int64_t rot_base, void *stream) {
+    PQKV_CHECK_ARG(batches >= 0 && batches <= 65535, "pqkv_encode_batched_grid: bad batch count");
+    PQKV_CHECK_ARG(geometry_ok(d, M, nbits) && grid_geometry(d, M, nbits),
+                   "pqkv_encode_batched_grid: the candidate grid exists for dsub = 2, nbits <= 8");
+    PQKV_CHECK_ARG(x_bstride >= 0 && c_bstride >= 0 && g_bstride >= 0 && codes_bstride >= 0,
+                   "pqkv_encode_batched_grid: negative batch stride");
+    if (batches == 0 || n == 0) return PQKV_OK;
+    PQKV_CHECK_ARG(x && centroids && grid && codes && ld_x >= d && ld_codes >= M,
+                   "pqkv_encode_batched_grid: bad arguments");
+    PQKV_CHECK_ARG(rot_base < 0 || is_fast_geometry(d, M, nbits),
+                   "pqkv_encode_batched_grid: the decode layout exists only for m64b8");
+    return launch_dsub2_grid<float, uint8_t>(x, n, ld_x, centroids, (const unsigned char *)grid,
+                                             M, 1 << nbits, codes, ld_codes, rot_base,
+                                             as_stream(stream), batches, x_bstride, c_bstride,
+                                             g_bstride, codes_bstride);
 }
 
 extern "C" int pqkv_encode(const void *x, int x_dtype, int64_t n, int d, int64_t ld_x,

@@ -45,12 +45,28 @@ def code_dtype(nbits: int) -> torch.dtype:
     return torch.uint8 if nbits <= 8 else torch.uint16
 
 
+def encode_grid(centroids: torch.Tensor, nbits: int, stream=None) -> torch.Tensor | None:
+    """The candidate grid of a (M, ksub, 2) codebook for encode(..., grid=)
+    (pqkv_build_encode_grid; None for geometries without one)."""
+    M, ksub, dsub = centroids.shape
+    nb = int(N.load(require_cuda=False).pqkv_encode_grid_bytes(M * dsub, M, nbits))
+    if nb <= 0:
+        return None
+    cents = _contig(centroids.float())
+    grid = torch.empty(nb, dtype=torch.uint8, device=cents.device)
+    _call(cents.device, "pqkv_build_encode_grid", N.ptr(cents), M * dsub, M, nbits, N.ptr(grid),
+          N.stream_ptr(stream, cents.device))
+    return grid
+
+
 def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tensor | None = None,
-           stream=None, layout: str = "rows", t_first: int = 0) -> torch.Tensor:
+           stream=None, layout: str = "rows", t_first: int = 0, grid=None) -> torch.Tensor:
     """Nearest-centroid codes of x (n, d) -> (n, M); bit-exact with assign_codes.
 
     layout="rows" is the reference CodesMatrix order; layout="decode" (m64b8)
-    writes the decode kernel's layout with row 0 at token index t_first."""
+    writes the decode kernel's layout with row 0 at token index t_first.
+    grid: the codebook's encode_grid() (dsub = 2): the filter scans each
+    point's candidate list instead of every centroid -- the same codes."""
     _dev_check(x, centroids)
     M, ksub, dsub = centroids.shape
     d = M * dsub
@@ -67,6 +83,11 @@ def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tens
         raise ValueError("codes output must be (n, M) with unit column stride")
     cents = _contig(centroids.float())
     rot = _rot_base(layout, t_first)
+    if grid is not None:
+        _call(x.device, "pqkv_encode_grid", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0),
+              N.ptr(cents), N.ptr(grid), M, nbits, N.ptr(out), out.stride(0), rot,
+              N.stream_ptr(stream, x.device))
+        return out
     _call(x.device, "pqkv_encode", N.ptr(x), N.DTYPE_CODE[x.dtype], n, d, x.stride(0), N.ptr(cents), M,
            nbits, N.ptr(out), out.stride(0), rot, N.stream_ptr(stream, x.device))
     return out
@@ -74,7 +95,7 @@ def encode(x: torch.Tensor, centroids: torch.Tensor, nbits: int, out: torch.Tens
 
 def encode_batched(x: torch.Tensor, centroids: torch.Tensor, nbits: int,
                    out: torch.Tensor | None = None, stream=None, layout: str = "rows",
-                   t_first: int = 0) -> torch.Tensor:
+                   t_first: int = 0, grids=None) -> torch.Tensor:
     """encode() over a batch of independent problems in one launch: x (Z, n, d),
     centroids (Z, M, ksub, dsub) -> (Z, n, M) -- e.g. every layer of a cache
     flush, each with its own codebook."""
@@ -90,6 +111,12 @@ def encode_batched(x: torch.Tensor, centroids: torch.Tensor, nbits: int,
         out = torch.empty((Z, n, M), dtype=code_dtype(nbits), device=x.device)
     if tuple(out.shape) != (Z, n, M) or not out.is_contiguous():
         raise ValueError("codes output must be a contiguous (Z, n, M) tensor")
+    if grids is not None:  # (Z, grid bytes): each problem's encode_grid()
+        grids = _contig(grids)
+        _call(x.device, "pqkv_encode_batched_grid", N.ptr(x), Z, n, d, d, n * d, N.ptr(cents),
+              M * ksub * dsub, N.ptr(grids), grids.shape[1], M, nbits, N.ptr(out), M, n * M,
+              _rot_base(layout, t_first), N.stream_ptr(stream, x.device))
+        return out
     _call(x.device, "pqkv_encode_batched", N.ptr(x), N.DTYPE_CODE[torch.float32], Z, n, d, d, n * d,
            N.ptr(cents), M * ksub * dsub, M, nbits, N.ptr(out), M, n * M,
            _rot_base(layout, t_first), N.stream_ptr(stream, x.device))

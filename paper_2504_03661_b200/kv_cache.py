@@ -193,10 +193,12 @@ class LayerKVCache:
                 self._ensure_store(self._n_q + n_enc)
                 K.encode(Kt[:n_enc].contiguous(), self.cb_K.device_centroids(self.device),
                          self.config.nbits, out=self._store_k[self._n_q: self._n_q + n_enc],
-                         layout=self._layout, t_first=self._n_q)
+                         layout=self._layout, t_first=self._n_q,
+                         grid=self.cb_K.device_encode_grid(self.device))
                 K.encode(Vt[:n_enc].contiguous(), self.cb_V.device_centroids(self.device),
                          self.config.nbits, out=self._store_v[self._n_q: self._n_q + n_enc],
-                         layout=self._layout, t_first=self._n_q)
+                         layout=self._layout, t_first=self._n_q,
+                         grid=self.cb_V.device_encode_grid(self.device))
             if keep:
                 self._ensure_recent(keep)
                 a = self._r0 + self._rlen
@@ -287,9 +289,11 @@ class LayerKVCache:
         rows_v = self._rv[first: first + batch]
         out_k = self._store_k[n0: n0 + batch]
         out_v = self._store_v[n0: n0 + batch]
+        gk = self.cb_K.device_encode_grid(self.device)
+        gv = self.cb_V.device_encode_grid(self.device)
         if not asynchronous:
-            K.encode(rows_k, cents_k, nb, out=out_k, layout=self._layout, t_first=n0)
-            K.encode(rows_v, cents_v, nb, out=out_v, layout=self._layout, t_first=n0)
+            K.encode(rows_k, cents_k, nb, out=out_k, layout=self._layout, t_first=n0, grid=gk)
+            K.encode(rows_v, cents_v, nb, out=out_v, layout=self._layout, t_first=n0, grid=gv)
             self._n_q += batch          # single publication point
             self._r0 += batch
             self._rlen -= batch
@@ -299,9 +303,9 @@ class LayerKVCache:
         self._side.wait_stream(main)    # the rows were written on the main stream
         with torch.cuda.stream(self._side):
             K.encode(rows_k, cents_k, nb, out=out_k, stream=self._side, layout=self._layout,
-                     t_first=n0)
+                     t_first=n0, grid=gk)
             K.encode(rows_v, cents_v, nb, out=out_v, stream=self._side, layout=self._layout,
-                     t_first=n0)
+                     t_first=n0, grid=gv)
             ev = torch.cuda.Event()
             ev.record(self._side)
         for t in (rows_k, rows_v, out_k, out_v):

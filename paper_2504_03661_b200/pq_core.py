@@ -130,6 +130,15 @@ class Codebook:
             self._dev[key] = to_device(self.centroids, torch.float32, dev).contiguous()
         return self._dev[key]
 
+    def device_encode_grid(self, device=None):
+        """The encoder's candidate grid (kernels.encode_grid; None when the
+        geometry has none), built once per device."""
+        dev = torch.device(device) if device is not None else default_device()
+        key = ("g", str(dev))
+        if key not in self._dev:
+            self._dev[key] = K.encode_grid(self.device_centroids(dev), self.config.nbits)
+        return self._dev[key]
+
     def device_key_layout(self, device=None) -> torch.Tensor:
         """Key codebook as the decode kernel reads it (pqkv_prepare_key_codebook)."""
         dev = torch.device(device) if device is not None else default_device()
@@ -225,7 +234,8 @@ def assign_codes(X, cb: Codebook) -> CodesMatrix:
         if x.dtype not in (torch.float32, torch.bfloat16, torch.float16):
             x = x.float()
         _finite_or_raise(x)
-    codes = K.encode(x, cb.device_centroids(x.device), cb.config.nbits)
+    codes = K.encode(x, cb.device_centroids(x.device), cb.config.nbits,
+                     grid=cb.device_encode_grid(x.device))
     if host:
         return CodesMatrix(codes=codes.cpu().numpy(), nbits=cb.config.nbits)
     return CodesMatrix(codes=codes, nbits=cb.config.nbits)

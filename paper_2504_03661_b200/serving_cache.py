@@ -70,6 +70,11 @@ class ServingCache:
         self.cents_k = [cents(c) for c in centroids_k]
         self.cents_v = [cents(c) for c in centroids_v]
         self.cents_k_all = torch.stack(self.cents_k)  # (L, M, ksub, dsub): batched flushes
+        # the encoder's candidate grids (None for geometries without one)
+        self.grid_k = [K.encode_grid(c, config.nbits) for c in self.cents_k]
+        self.grid_v = [K.encode_grid(c, config.nbits) for c in self.cents_v]
+        self.grid_k_all = (torch.stack(self.grid_k) if self.grid_k[0] is not None else None)
+        self.grid_v_all = (torch.stack(self.grid_v) if self.grid_v[0] is not None else None)
         self.cents_v_all = torch.stack(self.cents_v)
         # decode-kernel codebook layouts (static: prepared once, at load time)
         self.cb_k = [K.key_codebook_layout(c, config.nbits) for c in self.cents_k]
@@ -134,11 +139,11 @@ class ServingCache:
         and land with one strided copy; otherwise one launch per head."""
         B, Hkv, n, d = rows_k.shape
         M = self.config.M
-        for rows, cents, store in ((rows_k, self.cents_k[l], self.codes_k),
-                                   (rows_v, self.cents_v[l], self.codes_v)):
+        for rows, cents, grid, store in ((rows_k, self.cents_k[l], self.grid_k[l], self.codes_k),
+                                         (rows_v, self.cents_v[l], self.grid_v[l], self.codes_v)):
             if n % 8 == 0:
                 tmp = K.encode(rows.reshape(B * Hkv * n, d), cents, self.config.nbits,
-                               stream=stream, layout="decode", t_first=t_first)
+                               stream=stream, layout="decode", t_first=t_first, grid=grid)
                 with torch.cuda.stream(stream) if stream is not None else _nullctx():
                     store[l, :, :, t_first:t_first + n] = tmp.view(B, Hkv, n, M)
             else:
@@ -146,7 +151,7 @@ class ServingCache:
                     for h in range(Hkv):
                         K.encode(rows[b, h], cents, self.config.nbits,
                                  out=store[l, b, h, t_first:t_first + n], stream=stream,
-                                 layout="decode", t_first=t_first)
+                                 layout="decode", t_first=t_first, grid=grid)
 
     def _encode_all(self, rows_k, rows_v, t_first: int, stream=None) -> None:
         """rows (L, B, Hkv, n, d), n a multiple of 8 -> codes[:, :, :, t_first:+n]:
@@ -155,10 +160,10 @@ class ServingCache:
         strided copy into the store."""
         L, B, Hkv, n, d = rows_k.shape
         M = self.config.M
-        for rows, cents, store in ((rows_k, self.cents_k_all, self.codes_k),
-                                   (rows_v, self.cents_v_all, self.codes_v)):
+        for rows, cents, grids, store in ((rows_k, self.cents_k_all, self.grid_k_all, self.codes_k),
+                                          (rows_v, self.cents_v_all, self.grid_v_all, self.codes_v)):
             tmp = K.encode_batched(rows.reshape(L, B * Hkv * n, d), cents, self.config.nbits,
-                                   stream=stream, layout="decode", t_first=t_first)
+                                   stream=stream, layout="decode", t_first=t_first, grids=grids)
             with torch.cuda.stream(stream) if stream is not None else _nullctx():
                 store[:, :, :, t_first:t_first + n] = tmp.view(L, B, Hkv, n, M)
 
