@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(256) encode_dsub2_filter(const TX *__restrict_
 // centroid indices (at most EG_POOL bytes, so a CTA stages ~45 KB).
 constexpr int EG = 64;                              // cells per axis
 constexpr int EG_CELLS = EG * EG;
-constexpr int EG_POOL = 28 * 1024;                  // candidate-index bytes per subspace
+#ifndef PQKV_ENC_GRID_POOL
+#define PQKV_ENC_GRID_POOL 28
+#endif
+constexpr int EG_POOL = PQKV_ENC_GRID_POOL * 1024;  // candidate-index bytes per subspace
 constexpr int EG_LMAX = 24;                         // a longer list -> full scan
 constexpr int EG_HDR = 32;
 constexpr int EG_OFFS = EG_HDR, EG_CNT = EG_OFFS + 2 * EG_CELLS, EG_PL = EG_CNT + EG_CELLS;
@@ -444,7 +447,10 @@ __global__ void __launch_bounds__(256) build_encode_grid_kernel(const float *__r
 }
 
 #ifndef PQKV_ENC_GRID_VPT
-#define PQKV_ENC_GRID_VPT 4  // vectors per thread per pass (their loads in flight together)
+#define PQKV_ENC_GRID_VPT 2  // vectors per thread per pass (their loads in flight together)
+#endif
+#ifndef PQKV_ENC_GRID_CTAS
+#define PQKV_ENC_GRID_CTAS 4  // persistent CTAs per SM over (subspace, row block) pairs
 #endif
 template <typename TX, typename CT, int VPT>
 __global__ void __launch_bounds__(256) encode_dsub2_grid(const TX *__restrict__ x, int64_t n,
@@ -584,7 +590,8 @@ int launch_dsub2_grid(const void *x, int64_t n, int64_t ld_x, const float *cents
     // persistent row blocks: ~4 CTAs (of ~54 KB shared memory) per SM over
     // (subspace, row block) pairs
     int64_t blocks = (n + 256 * VPT - 1) / (256 * VPT);
-    const int64_t target = std::max<int64_t>(1, (int64_t)4 * 148 / std::max(1, M * batches));
+    const int64_t target =
+        std::max<int64_t>(1, (int64_t)PQKV_ENC_GRID_CTAS * 148 / std::max(1, M * batches));
     blocks = std::min<int64_t>(blocks, target);
     dim3 g((unsigned)M, (unsigned)std::min<int64_t>(blocks, 65535), (unsigned)batches);
     k<<<g, 256, smem, st>>>((const TX *)x, n, ld_x, cents, grid, ksub, (CT *)codes, ld_codes,
