@@ -45,6 +45,29 @@ __device__ __forceinline__ double load_x<__half>(const __half *p) {
     return (double)__half2float(*p);
 }
 
+// the subspace's two input values (one 8- or 4-byte load when aligned)
+template <typename TX>
+__device__ __forceinline__ void load_pair(const TX *p, float &a, float &b) {
+    if ((reinterpret_cast<uintptr_t>(p) & (2 * sizeof(TX) - 1)) == 0) {
+        if constexpr (sizeof(TX) == 4) {
+            const float2 v = __ldg(reinterpret_cast<const float2 *>(p));
+            a = v.x;
+            b = v.y;
+        } else {
+            const uint32_t v = __ldg(reinterpret_cast<const unsigned int *>(p));
+            TX lo, hi;
+            memcpy(&lo, &v, 2);
+            const uint16_t h = (uint16_t)(v >> 16);
+            memcpy(&hi, &h, 2);
+            a = (float)load_x<TX>(&lo);
+            b = (float)load_x<TX>(&hi);
+        }
+    } else {
+        a = (float)load_x<TX>(p);
+        b = (float)load_x<TX>(p + 1);
+    }
+}
+
 // numpy pairwise_sum for float64 (n < 8: sequential from 0.0; n <= 128: eight
 // strided accumulators; else recursive halves rounded down to a multiple of 8).
 template <typename Get>
@@ -511,8 +534,7 @@ __global__ void __launch_bounds__(256) encode_dsub2_grid(const TX *__restrict__ 
         for (int k = 0; k < VPT; ++k) {  // every load of the pass in flight at once
             const int64_t v = v0 + (int64_t)k * blockDim.x;
             const int64_t vv = v < n ? v : n - 1;
-            xa[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2);
-            xb[k] = (float)load_x<TX>(x + vv * ld_x + (int64_t)i * 2 + 1);
+            load_pair<TX>(x + vv * ld_x + (int64_t)i * 2, xa[k], xb[k]);
         }
 #pragma unroll 1
         for (int k = 0; k < VPT; ++k) {
