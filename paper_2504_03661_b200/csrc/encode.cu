@@ -536,8 +536,8 @@ __global__ void __launch_bounds__(256) encode_dsub2_grid(const TX *__restrict__ 
             const int64_t vv = v < n ? v : n - 1;
             load_pair<TX>(x + vv * ld_x + (int64_t)i * 2, xa[k], xb[k]);
         }
-#pragma unroll 1
-        for (int k = 0; k < VPT; ++k) {
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {  // unrolled: xa / xb stay in registers
             const int64_t v = v0 + (int64_t)k * blockDim.x;
             if (v >= n) break;
             const float xf0 = xa[k], xf1 = xb[k];
