@@ -1801,6 +1801,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
 #ifndef PQKV_PAIR_CLAMP
 #define PQKV_PAIR_CLAMP 1
 #endif
+#ifndef PQKV_PAIR_RING
+#define PQKV_PAIR_RING 3
+#endif
 namespace gp {
 constexpr int HG = 4;
 constexpr int UT = 16;       // tokens per warp per unit
@@ -1964,9 +1967,10 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
     gp::cluster_sync();  // the peer's mbarriers exist before any st.async
 
     const int group = A.Hq / A.Hkv;
-    UnitP Ur[2];
+    constexpr int PR = PQKV_PAIR_RING;  // ring depth (units in flight per warp)
+    UnitP Ur[PR];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) Ur[rr].ka = Ur[rr].kb = Ur[rr].va = Ur[rr].vb = uint2{0u, 0u};
+    for (int rr = 0; rr < PR; ++rr) Ur[rr].ka = Ur[rr].kb = Ur[rr].va = Ur[rr].vb = uint2{0u, 0u};
     CostMap cm;
     Segment s0;
     bool have_s0 = false;
@@ -2014,7 +2018,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
             const int64_t head_off = ((int64_t)b * A.Hkv + hkv) * A.ld_tok * M + 32 * c + 8 * w;
             const int u0 = s0.lo / UT;
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr)
+            for (int rr = 0; rr < PR; ++rr)
                 load_unit(Ur[rr], A.codes_k + head_off, A.codes_v + head_off, u0 + wu + rr * W,
                           s0.lo, s0.hi);
         }
@@ -2079,7 +2083,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
         const int u0 = lo / UT, u1 = (hi + UT - 1) / UT;
         if (!ring_loaded) {
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr)
+            for (int rr = 0; rr < PR; ++rr)
                 load_unit(Ur[rr], kbase, vbase, u0 + wu + rr * W, lo, hi);
         }
         ring_loaded = false;
@@ -2187,7 +2191,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
             if (lane == 0) mbar_expect_tx(bar_loc + buf * 8, 256);
             // refill this ring slot's key registers (the key phase is done with them)
             {
-                const int tn = (u + 2 * W) * UT + slot;
+                const int tn = (u + PR * W) * UT + slot;
 #if PQKV_PAIR_CLAMP
                 g4::ld8_into(U.ka, kbase + row(tn, lo, hi));
                 g4::ld8_into(U.kb, kbase + row(tn + 8, lo, hi));
@@ -2263,7 +2267,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
                 }
             }
             {
-                const int tn = (u + 2 * W) * UT + slot;
+                const int tn = (u + PR * W) * UT + slot;
 #if PQKV_PAIR_CLAMP
                 g4::ld8_into(U.va, vbase + row(tn, lo, hi));
                 g4::ld8_into(U.vb, vbase + row(tn + 8, lo, hi));
@@ -2274,13 +2278,15 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
             }
             u += W;
         };
-        for (int trip = 0; trip < nunits / 2; ++trip) {
+        for (int trip = 0; trip < nunits / PR; ++trip) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) asm volatile("" : "+r"(pk[k]));
-            unit_step(Ur[0]);
-            unit_step(Ur[1]);
+#pragma unroll
+            for (int rr = 0; rr < PR; ++rr) unit_step(Ur[rr]);
         }
-        if (nunits & 1) unit_step(Ur[0]);
+#pragma unroll
+        for (int rr = 0; rr < PR - 1; ++rr)
+            if (rr < nunits % PR) unit_step(Ur[rr]);
 
         // ---- epilogue: this CTA's 64 dims of the pair's record per head
         {
