@@ -4,7 +4,10 @@ Drop-in for the hot path of the reference package ``pqkv`` (MILLION,
 arXiv 2504.03661): codebook load, KV encode and quantized-cache decode
 attention keep the reference's names and semantics; the arithmetic runs in
 hand-written CUDA kernels in ``_lib/libpqkv_sm100.so`` reached through the C
-ABI declared in ``include/pqkv_sm100.h``.  There is no CPU fallback.
+ABI declared in ``include/pqkv_sm100.h``.  The encode / decode path has no
+CPU fallback (it raises without the library or a GPU).  Offline codebook
+training (``training``, torch arithmetic) runs on the GPU by default and on
+the CPU only when asked (``device="cpu"``, used by the CPU test suite).
 
 The batched serving path (many sequences, heads and layers per launch, GQA,
 sequence split across GPUs) is ``engine``.
