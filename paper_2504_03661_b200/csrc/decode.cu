@@ -1916,17 +1916,17 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
     constexpr int NPART = NT / 64;  // column-sum parts of 64 threads
     static_assert(NT % 64 == 0, "W must be even");
     static_assert(HG * W * 8 * 64 * 4 <= 2 * gp::TAB, "slot rows fit the key tables");
-    // the epilogue's column sums and max / sum reductions live in the dense
-    // area, which is free after a segment's dense record is written
-    static_assert((HG * NPART * 64 + 2 * HG * W) * 4 <= (2 * WMAX + WMAX * D) * 4,
-                  "epilogue scratch fits the dense area");
+    static_assert(2 * HG * W <= 4 * WMAX, "max / sum reductions fit the red region");
+    // the epilogue's column sums live in the dense area: they are written after
+    // the epilogue's first barrier, when every thread is past the dense merge
+    static_assert(HG * NPART * 64 <= 2 * WMAX + WMAX * D, "column sums fit the dense area");
     using gp::UnitP;
     const int Hqv = A.Hq / HG;
 
     extern __shared__ __align__(128) unsigned char smem[];
     float *rows_s = reinterpret_cast<float *>(smem);  // epilogue: slot rows in the tables
     float *colsum = reinterpret_cast<float *>(smem + OFF_DNS);  // [HG][NPART][64]
-    float *red_m = colsum + HG * NPART * 64;
+    float *red_m = reinterpret_cast<float *>(smem + OFF_RED);  // written before that barrier
     float *red_l = red_m + HG * W;
     float *dn_m = reinterpret_cast<float *>(smem + OFF_DNS);
     float *dn_l = dn_m + W;
