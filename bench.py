@@ -394,7 +394,7 @@ def append_overlap(dev, replay, stream, L, B, Hkv, warmup, R_f=32, rounds=3):
             "slowdown": with_flush / base - 1.0}
 
 
-def shard_plan(name, rank, world):
+def shard_plan(name, rank, world, force_split=False):
     """This rank's share of config `name` on `world` GPUs:
     batch sharding (each rank its own sequences, no collective, weak scaling);
     KV-head sharding for config 3 (rank r serves KV heads [r Hkv/N, (r+1) Hkv/N)
@@ -406,7 +406,7 @@ def shard_plan(name, rank, world):
     plan = {"workload": name, "rank": rank, "world": world, "L": L, "B": B, "Hq": Hq,
             "Hkv": Hkv, "n": n, "R": R, "tok": [0, n], "kv_heads": [0, Hkv], "tail": True,
             "mode": "batch", "jobs": world}
-    if world > 1 and name in SEQ_SPLIT:
+    if (world > 1 or force_split) and name in SEQ_SPLIT:
         from paper_2504_03661_b200.engine import shard_tokens
         a, b = shard_tokens(n, rank, world)
         plan.update(mode="sequence", n=b - a, tok=[a, b], tail=rank == world - 1, jobs=1)
@@ -605,7 +605,13 @@ def run_ours(args):
     if torch.cuda.device_count() < (local + 1):
         raise SystemExit(f"bench.py: rank {rank} needs GPU {local}; "
                          f"{torch.cuda.device_count()} visible")
-    if world > 1:
+    force_split = args.seq_split_one and world == 1 and args.config in SEQ_SPLIT
+    if world > 1 or force_split:
+        if force_split:  # a one-rank NCCL group: the split path's capture and merge on 1 GPU
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -627,8 +633,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    plan = shard_plan(args.config, rank, world)
-    w = Workload(args, plan, dev, stream, world > 1)
+    plan = shard_plan(args.config, rank, world, force_split)
+    w = Workload(args, plan, dev, stream, world > 1 or force_split)
     L, B, Hq, Hkv, n = w.L, w.B, w.Hq, w.Hkv, w.n
     seq_split = w.seq_split
     jobs = plan["jobs"]
@@ -888,7 +894,7 @@ def run_ours(args):
                                 "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -957,6 +963,9 @@ def main():
                     help="headline in the fp16 value-codebook mode (stated tolerance, DESIGN.md)")
     ap.add_argument("--no-f16-mode", action="store_true",
                     help="skip the secondary fp16 value-codebook measurement")
+    ap.add_argument("--seq-split-one", action="store_true",
+                    help="config 4 on one GPU through the sequence-split path (a one-rank NCCL "
+                         "group: the captured all-gather + rank-ordered merge, as at N > 1)")
     ap.add_argument("--no-extra-configs", action="store_true",
                     help="N > 1: skip the head-sharded / sequence-split configs beside config 2")
     ap.add_argument("--dry-run", action="store_true",

@@ -79,3 +79,14 @@ def test_launcher_refuses_missing_gpus():
                         "--steps", "1"], capture_output=True, text=True, cwd=ROOT,
                        timeout=300, env=env)
     assert r.returncode != 0 and "GPU(s) visible" in r.stderr
+
+
+@pytest.mark.gpu
+def test_sequence_split_path_on_one_gpu():
+    """Config 4 through the sequence-split path with a one-rank NCCL group: the
+    per-layer (m, l, acc) records, the NCCL all-gather and the rank-ordered
+    merge are captured in the step's CUDA graph (as at N > 1)."""
+    j = _run("--config", "llama3-gqa-128k", "--seq-split-one", "--steps", "2", "--warmup", "3",
+             "--no-cpu-baseline", "--no-encode", "--no-f16-mode")
+    assert j["sequence_split"]["step_mode"] == "cuda graph"
+    assert j["sequence_split"]["merge_ms_per_step"] > 0 and j["value"] > 0
