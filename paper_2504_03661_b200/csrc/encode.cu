@@ -602,12 +602,14 @@ int launch_dsub2_grid(const void *x, int64_t n, int64_t ld_x, const float *cents
     constexpr int VPT = PQKV_ENC_GRID_VPT;
     const size_t smem = (size_t)256 * 4 * sizeof(double) + EG_REC;  // the pool's worst case
     auto k = encode_dsub2_grid<TX, CT, VPT>;
-    static bool attr = false;
-    if (!attr) {
+    static int attr_set[64] = {0};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return fail(PQKV_ECUDA, "encode: %s", cudaGetErrorString(e));
-        attr = true;
+        if (dev < 64) attr_set[dev] = 1;
     }
     // persistent row blocks: ~4 CTAs (of ~54 KB shared memory) per SM over
     // (subspace, row block) pairs

@@ -216,8 +216,8 @@ class LayerKVCache:
                          non_blocking=False)
 
     def _publish_device(self, batch: int) -> None:
-        N.call("pqkv_publish_lengths", N.ptr(self._lens), batch,
-               N.stream_ptr(None, self.device))
+        K._call(self.device, "pqkv_publish_lengths", N.ptr(self._lens), batch,
+                N.stream_ptr(None, self.device))
 
     def append_decode(self, k_n, v_n) -> None:
         """Append the current token's full-precision KV pair; flush whole
@@ -229,9 +229,9 @@ class LayerKVCache:
             self._ensure_recent(1)
             # row r0 + rlen of the ring, and the device recent length + 1
             off = self._r0 * self.config.d * 4
-            N.call("pqkv_append_recent", N.ptr(k), N.ptr(v), self._rk.data_ptr() + off,
-                   self._rv.data_ptr() + off, N.ptr(self._lens), self.config.d,
-                   N.stream_ptr(None, self.device))
+            K._call(self.device, "pqkv_append_recent", N.ptr(k), N.ptr(v),
+                    self._rk.data_ptr() + off, self._rv.data_ptr() + off, N.ptr(self._lens),
+                    self.config.d, N.stream_ptr(None, self.device))
             self._rlen += 1
             self._n_total += 1
             needed = self._flush_needed_locked()
