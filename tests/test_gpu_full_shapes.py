@@ -140,13 +140,15 @@ def test_config4_eight_way_split_equals_unsplit():
     np.testing.assert_allclose(got, _oracle(x), rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("mode", ["exact", "f16_quad", "f16_pair"])
 @pytest.mark.parametrize("grow", [True, False])
-def test_early_codes_revalidates_lengths(grow):
+def test_early_codes_revalidates_lengths(grow, mode):
     """PQKV_DECODE_EARLY_CODES reads n_q before its grid-dependency wait.  A
     kernel that releases the decode at once and rewrites n_q 200 us later
     (pqkv_debug_delayed_fill) makes that pre-wait copy stale; the decode must
     notice after the wait and redo its split: same bits as a plain launch on
-    the new lengths."""
+    the new lengths -- for the exact GQA CTA pairs (group 4) and the fp16
+    four- and two-heads-per-CTA kernels."""
     from paper_2504_03661_b200 import _native as N
     from paper_2504_03661_b200 import kernels as K
     from paper_2504_03661_b200.engine import PQDecoder
@@ -155,11 +157,13 @@ def test_early_codes_revalidates_lengths(grow):
     x = _layer(B, Hq, Hkv, n, 16, seed=5)
     ck, cv = K.relayout(x["ck"], True), K.relayout(x["cv"], True)
     cbk = K.key_codebook_layout(x["cents_k"], 8)
-    cbv = K.value_codebook_layout(x["cents_v"], 8)
+    cbv = K.value_codebook_layout(x["cents_v"], 8, half=mode != "exact")
     old_n, new_n = (6000, 19000) if grow else (19000, 6000)
     cfg = PQConfig(128, 64, 8)
-    plain = PQDecoder(B, Hq, Hkv, cfg)
-    early = PQDecoder(B, Hq, Hkv, cfg, pdl=True, static_codebooks=True, early_codes=True)
+    kw = {} if mode == "exact" else dict(f16_key_table=True,
+                                         key_table_pairs=mode == "f16_pair")
+    plain = PQDecoder(B, Hq, Hkv, cfg, **kw)
+    early = PQDecoder(B, Hq, Hkv, cfg, pdl=True, static_codebooks=True, early_codes=True, **kw)
     args = (ck, cv, x["nq"], cbk, cbv, x["rk"], x["rv"], x["nr"], x["kc"], x["vc"])
     x["nq"].fill_(new_n)
     want = plain(x["q"], *args).clone()
@@ -173,7 +177,8 @@ def test_early_codes_revalidates_lengths(grow):
         assert torch.equal(got, want)
     # and the oracle agrees with the new lengths
     x["nq"].fill_(new_n)
-    np.testing.assert_allclose(want.cpu().numpy(), _oracle(x), rtol=RTOL, atol=ATOL)
+    tol = (RTOL, ATOL) if mode == "exact" else (RTOL16, ATOL16)
+    np.testing.assert_allclose(want.cpu().numpy(), _oracle(x), rtol=tol[0], atol=tol[1])
 
 
 @pytest.mark.parametrize("async_flush", [False, True])
