@@ -449,12 +449,14 @@ __global__ void __launch_bounds__(256) build_encode_grid_kernel(const float *__r
             int off = 0;
             for (int cell = 0; cell < EG_CELLS; ++cell) {
                 const int n = n_s[cell];
-                if (n == 255 || off + n > EG_POOL) {
+                // lists start on 4-byte boundaries: the encoder reads 4 candidates per load
+                const int n4 = (n + 3) & ~3;
+                if (n == 255 || off + n4 > EG_POOL) {
                     n_s[cell] = 255;
                     off_s[cell] = 0;
                 } else {
                     off_s[cell] = (uint16_t)off;
-                    off += n;
+                    off += n4;
                 }
             }
             used_s = off;
@@ -558,8 +560,11 @@ __global__ void __launch_bounds__(256) encode_dsub2_grid(const TX *__restrict__ 
             uint32_t b1 = 0xffffffffu, b2;
             if (nc != 255) {
                 b2 = 0x7f7fffffu;  // a one-entry list has no competitor: FLT_MAX
+                const uint32_t *pw = reinterpret_cast<const uint32_t *>(pool_s + off);
+                uint32_t word = 0;
                 for (int k2 = 0; k2 < nc; ++k2) {
-                    const uint32_t key = key_of(pool_s[off + k2]);
+                    if ((k2 & 3) == 0) word = pw[k2 >> 2];  // 4 candidates per load
+                    const uint32_t key = key_of((int)((word >> (8 * (k2 & 3))) & 0xffu));
                     b2 = min(b2, max(b1, key));
                     b1 = min(b1, key);
                 }
