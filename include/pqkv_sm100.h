@@ -380,6 +380,22 @@ int pqkv_debug_delayed_fill(int32_t *p, int n, int32_t v, long long ns,
  * rows). */
 int pqkv_append_recent(const float *k, const float *v, float *rk, float *rv,
                        int32_t *lens, int d, void *stream);
+
+/* decode_step's per-token work for one head of a cache with device lengths
+ * (attention.py:214-287 for a LayerKVCache): pqkv_decode_attention with B =
+ * Hq = Hkv = 1 reading n_q = lens[0] and the recent length lens[1], then
+ * pqkv_append_recent of (k_cur, v_cur) -- one call per token.  The plan holds
+ * the per-cache constants (codebook layouts, code stores, lens, scale,
+ * workspace); recent_k / recent_v point at the ring's first live row. */
+int pqkv_step_plan_create(const float *cb_k, const float *cb_v,
+                          const void *codes_k, const void *codes_v,
+                          int64_t ld_tok, int32_t *lens, float scale, int d,
+                          int M, int nbits, int num_ctas, float *partials,
+                          int32_t *counters, void **plan);
+int pqkv_step_run(void *plan, const float *q, const float *k_cur,
+                  const float *v_cur, float *recent_k, float *recent_v,
+                  int64_t ld_recent, float *out, void *stream);
+int pqkv_step_plan_destroy(void *plan);
 int pqkv_publish_lengths(int32_t *lens, int batch, void *stream);
 
 /* ---- paged code store (growth without copies) ---------------------------

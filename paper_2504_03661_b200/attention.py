@@ -298,6 +298,32 @@ def finalize(p: SoftmaxPartial):
     return p.acc / p.l
 
 
+def _decode_step_plan(q_n, k_n, v_n, cache, cb_K, cb_V, sc, dev, counters):
+    """decode_step for a LayerKVCache with device tensors: the cache's step
+    plan runs the fused decode (lengths read on the device, in stream order)
+    and the append of (k_n, v_n) in one library call."""
+    cfg = cb_K.config
+    d = cfg.d
+    q = to_device(q_n, torch.float32, dev).reshape(-1)
+    kc = to_device(k_n, torch.float32, dev).reshape(-1)
+    vc = to_device(v_n, torch.float32, dev).reshape(-1)
+    if q.shape[0] != d:
+        raise ValueError(f"query width {q.shape[0]} != codebook d {d}")
+    if kc.shape[0] != d or vc.shape[0] != d:
+        raise ValueError(f"k_n/v_n width must be d={d}")
+    if counters is not None:
+        n_q, r = cache.n_q, cache.recent_len()
+        counters.lut_lookups += n_q * cfg.M
+        counters.adds += n_q * cfg.M
+        counters.code_bytes_read += 2 * n_q * cfg.M * cfg.cell_width
+        counters.dense_bytes_read += 2 * (r + 1) * d * 4
+    out = torch.empty(d, dtype=torch.float32, device=dev)
+    cache.decode_append(q.contiguous(), kc.contiguous(), vc.contiguous(), sc,
+                        cb_K.device_key_layout(dev), cb_V.device_value_layout(dev),
+                        _step_workspace(cfg, dev), out)
+    return out
+
+
 def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
                 scale: float | None = None, strategy: str = "auto", block_size: int = 1024,
                 counters: Counters | None = None, timings: dict | None = None):
@@ -316,11 +342,9 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
     dev = getattr(cache, "device", None) or default_device()
     fast = (timings is None and hasattr(cache, "raw_snapshot")
             and K.is_fast_geometry(cfg.d, cfg.M, cfg.nbits))
-    lens = None
-    if fast and not host and hasattr(cache, "step_view"):
-        # device-resident lengths: one fused decode launch + one append launch
-        ck_raw, cv_raw, rk, rv, lens, n_q, r_host = cache.step_view()
-    elif fast and hasattr(cache, "raw_view"):  # one fused launch: views, stream-ordered
+    if fast and not host and hasattr(cache, "decode_append"):
+        return _decode_step_plan(q_n, k_n, v_n, cache, cb_K, cb_V, sc, dev, counters)
+    if fast and hasattr(cache, "raw_view"):  # one fused launch: views, stream-ordered
         ck_raw, cv_raw, rk, rv, n_q, _ = cache.raw_view()
     elif hasattr(cache, "raw_snapshot"):     # this package's GPU cache: no layout copies
         ck_raw, cv_raw, rk, rv, n_q, _ = cache.raw_snapshot()
@@ -363,23 +387,6 @@ def decode_step(q_n, k_n, v_n, cache, cb_K: Codebook, cb_V: Codebook,
     if kc.shape[0] != cfg.d or vc.shape[0] != cfg.d:
         raise ValueError(f"k_n/v_n width must be d={cfg.d}")
 
-    if lens is not None:
-        # the cache's stores and recent ring as they are; the kernel reads n_q
-        # and the recent length from lens in stream order
-        ws = _step_workspace(cfg, dev)
-        out = torch.empty((1, cfg.d), dtype=torch.float32, device=dev)
-        K.decode_attention(ws, 1, q.view(1, -1), sc, cb_K.device_key_layout(dev),
-                           ck_raw.view(1, 1, -1, cfg.M), cv_raw.view(1, 1, -1, cfg.M), lens[0:1],
-                           cb_V.device_value_layout(dev), recent_k=rk.view(1, 1, -1, cfg.d),
-                           recent_v=rv.view(1, 1, -1, cfg.d), n_recent=lens[1:2],
-                           k_cur=kc.view(1, 1, -1), v_cur=vc.view(1, 1, -1), out=out)
-        if counters is not None:
-            counters.lut_lookups += n_q * cfg.M
-            counters.adds += n_q * cfg.M
-            counters.code_bytes_read += 2 * n_q * cfg.M * cfg.cell_width
-            counters.dense_bytes_read += 2 * (r_host + 1) * cfg.d * 4
-        cache.append_decode(kc, vc)
-        return out[0]
     if fast:
         # one fused launch (quantized span + recent rows + current token, merge,
         # finalize) with a per-thread cached workspace

@@ -3112,3 +3112,48 @@ extern "C" int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_he
                                                                            d, out, lse, merged);
     return launch_status("pqkv_merge_partials");
 }
+
+// ---- decode_step's per-token path for one cached head -----------------------
+struct pqkv_step_plan {
+    const float *cb_k, *cb_v;
+    const void *codes_k, *codes_v;
+    int64_t ld_tok;
+    int32_t *lens;
+    float scale;
+    int d, M, nbits, num_ctas;
+    float *partials;
+    int32_t *counters;
+};
+
+extern "C" int pqkv_step_plan_create(const float *cb_k, const float *cb_v, const void *codes_k,
+                                     const void *codes_v, int64_t ld_tok, int32_t *lens,
+                                     float scale, int d, int M, int nbits, int num_ctas,
+                                     float *partials, int32_t *counters, void **plan) {
+    PQKV_CHECK_ARG(plan && cb_k && cb_v && codes_k && codes_v && lens && partials && counters,
+                   "pqkv_step_plan_create: null pointer");
+    PQKV_CHECK_ARG(is_fast_geometry(d, M, nbits), "pqkv_step_plan_create: m64b8 only");
+    PQKV_CHECK_ARG(num_ctas > 0 && ld_tok >= 0, "pqkv_step_plan_create: bad sizes");
+    auto *p = new pqkv_step_plan{cb_k, cb_v, codes_k, codes_v, ld_tok, lens, scale, d, M,
+                                 nbits, num_ctas, partials, counters};
+    *plan = p;
+    return PQKV_OK;
+}
+
+extern "C" int pqkv_step_plan_destroy(void *plan) {
+    delete static_cast<pqkv_step_plan *>(plan);
+    return PQKV_OK;
+}
+
+extern "C" int pqkv_step_run(void *plan, const float *q, const float *k_cur, const float *v_cur,
+                             float *recent_k, float *recent_v, int64_t ld_recent, float *out,
+                             void *stream) {
+    PQKV_CHECK_ARG(plan && q && k_cur && v_cur && recent_k && recent_v && out,
+                   "pqkv_step_run: null pointer");
+    const auto *p = static_cast<const pqkv_step_plan *>(plan);
+    int rc = pqkv_decode_attention(q, p->scale, p->cb_k, nullptr, 1, 1, 1, p->codes_k, p->codes_v,
+                                   p->ld_tok, p->lens, p->cb_v, p->d, p->M, p->nbits, recent_k,
+                                   recent_v, ld_recent, p->lens + 1, k_cur, v_cur, p->num_ctas,
+                                   p->partials, p->counters, out, nullptr, nullptr, 0, stream);
+    if (rc) return rc;
+    return pqkv_append_recent(k_cur, v_cur, recent_k, recent_v, p->lens, p->d, stream);
+}

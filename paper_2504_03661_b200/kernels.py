@@ -9,6 +9,7 @@ validates in Python (attention.py:75-76, 129-132; pq_core.py:275-278).
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import torch
@@ -379,6 +380,45 @@ def decode_attention(ws: DecodeWorkspace, Hkv: int, q, scale: float, cb_k_layout
            N.ptr(n_recent), N.ptr(k_cur), N.ptr(v_cur), ws.num_ctas, N.ptr(ws.partials),
            N.ptr(ws.counters), N.ptr(out), N.ptr(lse), N.ptr(merged), flags,
            N.stream_ptr(stream, codes_k.device))
+
+
+class StepPlan:
+    """pqkv_step_plan for one LayerKVCache head (decode_step's per-token
+    path): the per-cache constants are bound once; run() is one C call that
+    launches the fused decode and the append of (k, v) to the ring."""
+
+    def __init__(self, cache, cb_k_layout, cb_v_layout, scale: float, ws: DecodeWorkspace):
+        cfg = cache.config
+        if not is_fast_geometry(cfg.d, cfg.M, cfg.nbits) or ws.B * ws.Hq != 1:
+            raise ValueError("StepPlan: m64b8 single-head workspace only")
+        self.device = cache.device
+        self._keep = (cache._store_k, cache._store_v, cb_k_layout, cb_v_layout, ws)
+        h = ctypes.c_void_p()
+        _call(self.device, "pqkv_step_plan_create", N.ptr(cb_k_layout), N.ptr(cb_v_layout),
+              N.ptr(cache._store_k), N.ptr(cache._store_v), cache._store_k.shape[0],
+              N.ptr(cache._lens), float(scale), cfg.d, cfg.M, cfg.nbits, ws.num_ctas,
+              N.ptr(ws.partials), N.ptr(ws.counters), ctypes.byref(h))
+        self._h = h.value
+        self._run = N.load().pqkv_step_run
+        self._dev_index = self.device.index if self.device.index is not None else \
+            torch.cuda.current_device()
+
+    def run(self, q, k, v, rk_ptr: int, rv_ptr: int, ld_recent: int, out) -> None:
+        if torch.cuda.current_device() != self._dev_index:
+            with torch.cuda.device(self._dev_index):
+                return self.run(q, k, v, rk_ptr, rv_ptr, ld_recent, out)
+        rc = self._run(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), rk_ptr, rv_ptr,
+                       ld_recent, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        if rc:
+            N.check(rc, "pqkv_step_run")
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                N.load().pqkv_step_plan_destroy(h)
+            except Exception:  # interpreter teardown
+                pass
 
 
 def merge_partials(parts: torch.Tensor, out=None, lse=None, merged=None, stream=None) -> None:

@@ -95,6 +95,7 @@ class LayerKVCache:
         self._pending: list[tuple[torch.cuda.Event, int]] = []  # in-flight batches, FIFO
         self._pending_rows = 0
         self._lock = threading.RLock()
+        self._plan = None  # decode_append's (key, StepPlan)
         self.inline_flush_seconds = 0.0
         # numpy in -> numpy snapshots, like the reference (kv_cache.py:269-290);
         # decided by the first write (None until then)
@@ -235,6 +236,33 @@ class LayerKVCache:
             self._rlen += 1
             self._n_total += 1
             needed = self._flush_needed_locked()
+        self._flush_after_append(needed)
+
+    def decode_append(self, q, k, v, scale: float, cb_k_layout, cb_v_layout, ws, out) -> None:
+        """decode_step's per-token work (attention.py:214-287 then
+        append_decode) in one library call, pqkv_step_run: the fused decode of
+        q against the stored codes + recent ring + (k, v), then the append of
+        (k, v) to the ring.  q, k, v: (d,) float32 on this device; out: (d,).
+        The step plan (codebook layouts, stores, device lengths, workspace)
+        is built once and rebuilt when any of them moves."""
+        with self._lock:
+            self._publish_completed()
+            self._ensure_recent(1)
+            key = (self._store_k.data_ptr(), self._store_v.data_ptr(), cb_k_layout.data_ptr(),
+                   cb_v_layout.data_ptr(), float(scale), id(ws))
+            plan = self._plan
+            if plan is None or plan[0] != key:
+                plan = self._plan = (key, K.StepPlan(self, cb_k_layout, cb_v_layout, scale, ws))
+            d4 = self.config.d * 4
+            off = self._r0 * d4
+            plan[1].run(q, k, v, self._rk.data_ptr() + off, self._rv.data_ptr() + off,
+                        self._rk.shape[0] - self._r0, out)
+            self._rlen += 1
+            self._n_total += 1
+            needed = self._flush_needed_locked()
+        self._flush_after_append(needed)
+
+    def _flush_after_append(self, needed: bool) -> None:
         if needed and self.worker == "sync":
             t0 = time.perf_counter()
             with self._lock:

@@ -773,3 +773,44 @@ def test_randomized_batched_configs(seed):
     else:
         got, want = res
         np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("worker", ["sync", "thread"])
+def test_decode_step_plan_device_stream(worker):
+    """decode_step with device tensors goes through the cache's step plan
+    (pqkv_step_run: fused decode + append in one call).  Every step equals
+    the oracle on the snapshot taken before it, across ring regrowth and
+    compaction, background flushes, a scale change and a reloaded cache
+    (the plan is rebuilt when a bound pointer or constant moves)."""
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(11)
+    cfg = P.PQConfig(128, 64, 8)
+    ck = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    cv = rng.standard_normal((64, 256, 2)).astype(np.float32)
+    cbk, cbv = P.Codebook(cfg, ck, "key"), P.Codebook(cfg, cv, "value")
+    cache = P.LayerKVCache(cbk, cbv, recent_capacity=4, flush_threshold=4, worker=worker)
+    X = rng.standard_normal((300, 128)).astype(np.float32)
+    cache.prefill_ingest(torch.from_numpy(X[:200]).cuda(), torch.from_numpy(X[100:300]).cuda())
+    cache.drain()
+    plans = set()
+    for s in range(40):
+        q, k, v = (rng.standard_normal(128).astype(np.float32) for _ in range(3))
+        scale = None if s < 30 else 0.05
+        if s == 20:  # reload into a new cache: new stores, same codebooks
+            fresh = P.LayerKVCache(cbk, cbv, recent_capacity=4, flush_threshold=4,
+                                   worker=worker)
+            fresh.load_snapshot(cache.snapshot())
+            cache.close()
+            cache = fresh
+        snap = cache.snapshot()
+        ck_h, cv_h = _np(snap.codes_K.codes), _np(snap.codes_V.codes)
+        rk, rv = _np(snap.recent_K), _np(snap.recent_V)
+        got = P.decode_step(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
+                            torch.from_numpy(v).cuda(), cache, cbk, cbv, scale=scale)
+        plans.add(cache._plan[0])
+        want = O.decode_from_snapshot(q, k, v, ck_h, cv_h, rk, rv, ck, cv, scale=scale,
+                                      block_size=1 << 30)
+        np.testing.assert_allclose(got.cpu().numpy(), want, rtol=RTOL, atol=ATOL)
+    cache.drain()
+    assert cache.n_total == 240 and len(plans) >= 2
+    cache.close()
