@@ -68,6 +68,15 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 namespace fast {
 constexpr int M = 64, KSUB = 256, D = 128;
+// Lazy rescaling of the online softmax: the running max moves only when a
+// score exceeds it by more than kLazyRescale (log2 units), so weights are at
+// most 2^kLazyRescale and the accumulators are rescaled a few times per
+// segment instead of on most units.  Any reference point gives the same
+// (m, l, acc) record up to rounding (the merge rescales records by their m).
+#ifndef PQKV_LAZY_RESCALE
+#define PQKV_LAZY_RESCALE 8
+#endif
+constexpr float kLazyRescale = PQKV_LAZY_RESCALE;
 #ifndef PQKV_WARPS
 #define PQKV_WARPS 16
 #endif
@@ -405,7 +414,7 @@ __device__ __forceinline__ void process_units(const Unit *U, SlotState<HG> &S,
 #pragma unroll
         for (int n = 0; n < NU; ++n)
             mx = fmaxf(mx, fmaxf(okA[n] ? sa[n][h] : -INFINITY, okB[n] ? sb[n][h] : -INFINITY));
-        if (mx > S.m[h]) {
+        if (mx > S.m[h] + kLazyRescale * kLn2) {
             const float f = fast_exp2((S.m[h] - mx) * kLog2e);
             S.l[h] *= f;
 #pragma unroll
@@ -1186,6 +1195,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
 //   * value path: the half2 codebook entry is widened to float2 and feeds one
 //     FFMA2 per head with the fp32 weight (the pair kernel rounds the weights
 //     to fp16; here only the codebook and the table entries are rounded).
+#ifndef PQKV_GQA4_PERM
+#define PQKV_GQA4_PERM 1
+#endif
 namespace g4 {
 constexpr int HG = 4;
 constexpr int UT = 8;                          // tokens per warp per unit
@@ -1276,8 +1288,18 @@ __device__ __forceinline__ void key_scores(const uint2 k, const uint32_t (&pk)[4
 }
 
 // sum v[0..3] over the 8 lanes of a token: the transposing butterfly only --
-// lane w returns head (w >> 1) & 3 (lanes w, w ^ 1 hold the same bits)
+// lane w returns head (w >> 1) & 3 (lanes w, w ^ 1 hold the same bits).
+// PQKV_GQA4_PERM: the table stores subspace i's heads in the order k ^ (i >> 4)
+// (tab_build4), and every subspace of lane w has i >> 4 = w >> 1, so v[k] is
+// head k ^ (w >> 1): each level keeps v[0..] and sends v[2..] -- no selects.
 __device__ __forceinline__ float token_reduce_own(const float (&v)[HG], int w) {
+#if PQKV_GQA4_PERM
+    (void)w;
+    const float k0 = v[0] + __shfl_xor_sync(0xffffffffu, v[2], 4);
+    const float k1 = v[1] + __shfl_xor_sync(0xffffffffu, v[3], 4);
+    const float k = k0 + __shfl_xor_sync(0xffffffffu, k1, 2);
+    return k + __shfl_xor_sync(0xffffffffu, k, 1);
+#else
     const bool b4 = (w & 4) != 0, b2 = (w & 2) != 0;
     const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
     float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
@@ -1287,6 +1309,7 @@ __device__ __forceinline__ float token_reduce_own(const float (&v)[HG], int w) {
     float k = b2 ? k1 : k0;
     k += __shfl_xor_sync(0xffffffffu, s, 2);
     return k + __shfl_xor_sync(0xffffffffu, k, 1);
+#endif
 }
 
 // NU units: key phase, then the softmax at the owner lanes (lane w of a token
@@ -1316,7 +1339,7 @@ __device__ __forceinline__ void process4(const Unit4 *U, State4 &S, const uint32
 #pragma unroll
         for (int n = 0; n < NU; ++n)
             mx = fmaxf(mx, fmaxf(okA[n] ? oa[n] : -INFINITY, okB[n] ? ob[n] : -INFINITY));
-        const bool up = mx > S.m;
+        const bool up = mx > S.m + kLazyRescale;
         if (__any_sync(0xffffffffu, up)) {  // rare: rescale the slot's accumulators
             const float f = up ? fast_exp2(S.m - mx) : 1.f;
             if (up) {
@@ -1360,6 +1383,20 @@ __device__ __forceinline__ void process4(const Unit4 *U, State4 &S, const uint32
     }
 }
 
+// e[k] <- e[k ^ pq] (pq < 4), with selects (no indexed registers)
+__device__ __forceinline__ void perm_heads(float (&e)[HG], int pq) {
+    float a0 = e[0], a1 = e[1], a2 = e[2], a3 = e[3];
+    if (pq & 1) {
+        const float t0 = a0, t2 = a2;
+        a0 = a1, a1 = t0, a2 = a3, a3 = t2;
+    }
+    if (pq & 2) {
+        const float t0 = a0, t1 = a1;
+        a0 = a2, a1 = a3, a2 = t0, a3 = t1;
+    }
+    e[0] = a0, e[1] = a1, e[2] = a2, e[3] = a3;
+}
+
 // the four heads' tables as one fp16 table: entry (c, i) = (h0, h1, h2, h3);
 // slot f = tid + k NT of the [256][32] float4 key codebook layout holds
 // subspaces 2(f & 31), +1 of centroid f / 32 -> one 16-byte store
@@ -1380,12 +1417,19 @@ __device__ __forceinline__ void tab_build4(unsigned char *tab, const float4 (&cc
             e0[h] = scale * fmaf(qh[h].y, cc[k].y, qh[h].x * cc[k].x);
             e1[h] = scale * fmaf(qh[h].w, cc[k].w, qh[h].z * cc[k].z);
         }
+        const int c = f >> 5, i0 = 2 * (f & 31);
+#if PQKV_GQA4_PERM
+        const int pq = i0 >> 4;  // entry slot k holds head k ^ (i >> 4) (token_reduce_own)
+#else
+        const int pq = 0;
+#endif
+        perm_heads(e0, pq);
+        perm_heads(e1, pq);
         uint4 o;
-        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.x) : "f"(e0[1]), "f"(e0[0]));  // lo = head 0
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.x) : "f"(e0[1]), "f"(e0[0]));  // lo = slot 0
         asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.y) : "f"(e0[3]), "f"(e0[2]));
         asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.z) : "f"(e1[1]), "f"(e1[0]));
         asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(o.w) : "f"(e1[3]), "f"(e1[2]));
-        const int c = f >> 5, i0 = 2 * (f & 31);
         *reinterpret_cast<uint4 *>(tab + ((i0 >> 5) << 16) + (c << 8) + ((i0 & 31) << 3)) = o;
     }
 }
@@ -1630,16 +1674,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
                 for (int n = 0; n < 2; ++n) {
                     const int ta = tn + n * W * UT;
                     const uint8_t *p = kp + n * kStep;
-                    if (ta >= lo && ta < hi) Ur[n].ka = ld8(p);
-                    if (ta + 2 >= lo && ta + 2 < hi) Ur[n].kb = ld8(p + dB);
+                    if (ta >= lo && ta < hi) g4::ld8_into(Ur[n].ka, p);
+                    if (ta + 2 >= lo && ta + 2 < hi) g4::ld8_into(Ur[n].kb, p + dB);
                 }
             });
 #pragma unroll
             for (int n = 0; n < 2; ++n) {
                 const int ta = tn + n * W * UT;
                 const uint8_t *p = kp + n * kStep + dv;
-                if (ta >= lo && ta < hi) Ur[n].va = ld8(p);
-                if (ta + 2 >= lo && ta + 2 < hi) Ur[n].vb = ld8(p + dB);
+                if (ta >= lo && ta < hi) g4::ld8_into(Ur[n].va, p);
+                if (ta + 2 >= lo && ta + 2 < hi) g4::ld8_into(Ur[n].vb, p + dB);
             }
             u += 2 * W;
             kp += 2 * kStep;
@@ -1801,6 +1845,9 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa4_f16(const Args A) {
 #ifndef PQKV_PAIR_CLAMP
 #define PQKV_PAIR_CLAMP 1
 #endif
+#ifndef PQKV_PAIR_PERMW
+#define PQKV_PAIR_PERMW 1
+#endif
 #ifndef PQKV_PAIR_RING
 #define PQKV_PAIR_RING 3
 #endif
@@ -1892,9 +1939,17 @@ __device__ __forceinline__ void key_scores(const uint2 k, const uint32_t (&pk)[4
 
 // this lane's head (w = lane & 3) summed over the token's 4 lanes
 __device__ __forceinline__ float reduce_head(unsigned long long s01, unsigned long long s23, int w) {
-    const bool b2 = (w & 2) != 0, b1 = (w & 1) != 0;
+    const bool b1 = (w & 1) != 0;
+#if PQKV_PAIR_PERMW
+    // the table's regions are swapped for the subspaces of lanes with w & 2:
+    // s01 always holds this lane's head pair (2 b2, 2 b2 + 1)
+    const unsigned long long snd = s23;
+    unsigned long long keep = s01;
+#else
+    const bool b2 = (w & 2) != 0;
     const unsigned long long snd = b2 ? s01 : s23;
     unsigned long long keep = b2 ? s23 : s01;
+#endif
     const float2 sv = unpack2(snd);
     unsigned long long rcv;
     {
@@ -2111,8 +2166,16 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
                     e[h][1] = sc * fmaf(qv.w, cb.w, qv.z * cb.z);
                 }
                 const int off = (cc << 8) | (pr << 4);
-                *reinterpret_cast<float4 *>(smem + off) = make_float4(e[0][0], e[1][0], e[0][1], e[1][1]);
-                *reinterpret_cast<float4 *>(smem + gp::TAB + off) =
+#if PQKV_PAIR_PERMW
+                // subspaces 16..31 of the half are read by lanes with w & 2
+                // (reduce_head): their first region holds heads 2, 3
+                const int sw = (pr >> 3) << 16;
+#else
+                const int sw = 0;
+#endif
+                *reinterpret_cast<float4 *>(smem + (off ^ sw)) =
+                    make_float4(e[0][0], e[1][0], e[0][1], e[1][1]);
+                *reinterpret_cast<float4 *>(smem + ((gp::TAB + off) ^ sw)) =
                     make_float4(e[2][0], e[3][0], e[2][1], e[3][1]);
             }
         }
@@ -2212,7 +2275,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
                 const float sa = c == 0 ? oa + r.x : r.x + oa;
                 const float sb = c == 0 ? ob + r.y : r.y + ob;
                 const float mx = fmaxf(okA ? sa : -INFINITY, okB ? sb : -INFINITY);
-                const bool up = mx > S.m;
+                const bool up = mx > S.m + kLazyRescale;
                 if (__any_sync(0xffffffffu, up)) {  // rare: rescale the slot's accumulators
                     const float f = up ? fast_exp2(S.m - mx) : 1.f;
                     if (up) {
@@ -2221,7 +2284,11 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
                     }
 #pragma unroll
                     for (int h = 0; h < HG; ++h) {
+#if PQKV_PAIR_PERMW
+                        const float fh = __shfl_xor_sync(0xffffffffu, f, h);  // head h ^ w
+#else
                         const float fh = __shfl_sync(0xffffffffu, f, (lane & ~3) | h);
+#endif
 #pragma unroll
                         for (int k = 0; k < 8; ++k) fmul2(S.acc[h][k], fh);
                     }
@@ -2232,6 +2299,20 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
             }
             // the slot's four heads' weights in every lane of the slot
             float pa[HG], pb[HG];
+#if PQKV_PAIR_PERMW
+            {   // slot k holds head k ^ w (as S.acc[k]): no selects
+                const float xa = __shfl_xor_sync(0xffffffffu, pa_, 1);
+                const float xb = __shfl_xor_sync(0xffffffffu, pb_, 1);
+                pa[0] = pa_;
+                pa[1] = xa;
+                pa[2] = __shfl_xor_sync(0xffffffffu, pa_, 2);
+                pa[3] = __shfl_xor_sync(0xffffffffu, xa, 2);
+                pb[0] = pb_;
+                pb[1] = xb;
+                pb[2] = __shfl_xor_sync(0xffffffffu, pb_, 2);
+                pb[3] = __shfl_xor_sync(0xffffffffu, xb, 2);
+            }
+#else
             {
                 const float xa = __shfl_xor_sync(0xffffffffu, pa_, 1);
                 const float xb = __shfl_xor_sync(0xffffffffu, pb_, 1);
@@ -2251,6 +2332,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
                 pb[2] = b2 ? c0 : yb0;
                 pb[3] = b2 ? c1 : yb1;
             }
+#endif
             // value phase: one gather per code byte, four FFMA2
             {
                 const uint2 va = gp::rot8(U.va, rsx, rsy), vb = gp::rot8(U.vb, rsx, rsy);
@@ -2313,13 +2395,19 @@ __global__ void __launch_bounds__(W * 32, 1) decode_gqa_pair(const Args A) {
             for (int off = 4; off < 32; off <<= 1) lw += __shfl_xor_sync(0xffffffffu, lw, off);
             if (lane < HG) red_l[lane * W + warp] = lw;
 #pragma unroll
-            for (int h = 0; h < HG; ++h) {
+            for (int k = 0; k < HG; ++k) {
+#if PQKV_PAIR_PERMW
+                const int h = k ^ w;  // S.acc[k] holds head k ^ w
+                const float fh = __shfl_xor_sync(0xffffffffu, f, k);
+#else
+                const int h = k;
                 const float fh = __shfl_sync(0xffffffffu, f, (lane & ~3) | h);
+#endif
                 float *rows = rows_s + ((h * W + warp) * 8 + slot) * 64;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int i = gp::lane_subspace(c, slot, w, j) - 32 * c;
-                    const float2 a = unpack2(S.acc[h][j]);
+                    const float2 a = unpack2(S.acc[k][j]);
                     rows[2 * i] = a.x * fh;
                     rows[2 * i + 1] = a.y * fh;
                 }

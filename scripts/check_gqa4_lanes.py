@@ -34,4 +34,21 @@ for lane in range(32):
         assert sub_at(TAU_A[s], 8 * w + j) == sub_at(TAU_A[s] + 2, 8 * (w ^ 1) + j)
 for s in range(4):
     assert sorted(sub_at(TAU_A[s], 8 * w + j) for w in range(8) for j in range(8)) == list(range(64))
+# PQKV_GQA4_PERM: every subspace a lane reads has i >> 4 == w >> 1, so the
+# table's head order k ^ (i >> 4) is the lane's; simulate token_reduce_own
+for lane in range(32):
+    s, w = lane >> 3, lane & 7
+    for j in range(8):
+        assert sub_at(TAU_A[s], 8 * w + j) >> 4 == w >> 1
+vals = {(w, h): 10.0 ** w * (h + 1) for w in range(8) for h in range(4)}  # lane w's head-h partial
+def v(w, k):  # slot k of lane w holds head k ^ (w >> 1)
+    return vals[(w, k ^ (w >> 1))]
+for w in range(8):
+    k0 = v(w, 0) + v(w ^ 4, 2)
+    k1 = lambda x: v(x, 1) + v(x ^ 4, 3)
+    k = k0 + k1(w ^ 2)
+    kk = lambda x: (v(x, 0) + v(x ^ 4, 2)) + k1(x ^ 2)
+    got = k + kk(w ^ 1)
+    h = (w >> 1) & 3
+    assert abs(got - sum(vals[(x, h)] for x in range(8))) < 1e-6 * got, (w, got)
 print("gqa4 lane mapping: conflict free, A/B subspaces equal, rows covered")

@@ -34,4 +34,13 @@ for c in (0, 1):
     for s in range(8):
         cov = sorted(sub_at(s, 32 * c + 8 * w + j) for w in range(4) for j in range(8))
         assert cov == list(range(32 * c, 32 * c + 32))
+# PQKV_PAIR_PERMW: the subspaces of lane w have local bit 4 == w >> 1, so the
+# key tables swap their head-pair regions for local subspaces 16..31
+for c in (0, 1):
+    for lane in range(32):
+        s, w = lane >> 2, lane & 3
+        rho = 2 if s & 2 else 0
+        for t in (s, s + 8):
+            for j in range(8):
+                assert (sub_at(t, 32 * c + 8 * w + ((j + rho) & 7)) - 32 * c) >> 4 == w >> 1
 print("gqa pair lane mapping: conflict free, A/B subspaces equal, halves covered")
