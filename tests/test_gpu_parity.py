@@ -270,7 +270,7 @@ def _oracle_heads(q, ck_codes, cv_codes, n_q, rk, rv, n_r, kcur, vcur, cents_k, 
 
 
 def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_cv=False,
-                  f16_keys=False, pairs=False):
+                  f16_keys=False, pairs=False, q_scale=1.0):
     from paper_2504_03661_b200 import kernels as K
     from paper_2504_03661_b200.engine import PQDecoder
     import paper_2504_03661_b200 as P
@@ -278,7 +278,7 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_c
     cfg = P.PQConfig(128, 64, 8)
     cents_k = rng.standard_normal((64, 256, 2)).astype(np.float32)
     cents_v = rng.standard_normal((64, 256, 2)).astype(np.float32)
-    q = rng.standard_normal((B, Hq, 128)).astype(np.float32)
+    q = (rng.standard_normal((B, Hq, 128)) * q_scale).astype(np.float32)
     codes_k = rng.integers(0, 256, (B, Hkv, cap, 64), dtype=np.uint8)
     codes_v = rng.integers(0, 256, (B, Hkv, cap, 64), dtype=np.uint8)
     rk = rng.standard_normal((B, Hkv, R, 128)).astype(np.float32)
@@ -312,6 +312,25 @@ def _batched_case(B, Hq, Hkv, cap, n_q, n_r, R=32, seed=0, num_ctas=None, half_c
 def test_batched_decoder_vs_oracle(B, Hq, Hkv, cap, n_q, n_r):
     got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("q_scale", [0.05, 8.0])
+@pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r", [
+    (1, 4, 4, 6000, [6000], [31]),                    # MHA
+    (2, 8, 2, 9000, [8999, 4321], [5, 32]),           # GQA 4:1 (exact: CTA pairs)
+])
+def test_lazy_rescale_dynamic_range(B, Hq, Hkv, cap, n_q, n_r, q_scale):
+    """The online softmax moves its running max only past a 2^8 margin
+    (decode.cu kLazyRescale): flat (q x 0.05) and very peaked (q x 8, scores
+    spanning hundreds of log2 units, many max jumps) distributions stay
+    within the exact tolerance; the fp16 modes at q x 3."""
+    got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r, q_scale=q_scale)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    s16 = min(q_scale, 3.0)
+    for keys in ([False, True] if Hq != Hkv else [False]):
+        got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True,
+                                          f16_keys=keys, q_scale=s16)
+        np.testing.assert_allclose(got, want16, rtol=2e-3, atol=2e-4)
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,cap,n_q,n_r,num_ctas", [
