@@ -45,8 +45,10 @@ CONFIGS = {
     # BASELINE config 4: 128K context, B=4, Llama-3-8B shape; under torchrun the
     # sequence is split across ranks (one all-gather of partial records per layer)
     "llama3-gqa-128k": (32, 4, 32, 8, 131072, 31),
+    # config 4 also reported on the MHA 32/32 shape (Llama-2-7B)
+    "llama2-mha-128k": (32, 4, 32, 32, 131072, 31),
 }
-SEQ_SPLIT = {"llama3-gqa-128k"}
+SEQ_SPLIT = {"llama3-gqa-128k", "llama2-mha-128k"}
 # BASELINE config 3 is KV-head sharded under torchrun: rank r serves KV heads
 # [r Hkv/N, (r+1) Hkv/N) (and their query heads) of every sequence -- no
 # collective, total work fixed (strong scaling)
