@@ -386,7 +386,8 @@ int pqkv_append_recent(const float *k, const float *v, float *rk, float *rv,
  * Hq = Hkv = 1 reading n_q = lens[0] and the recent length lens[1], then
  * pqkv_append_recent of (k_cur, v_cur) -- one call per token.  The plan holds
  * the per-cache constants (codebook layouts, code stores, lens, scale,
- * workspace); recent_k / recent_v point at the ring's first live row. */
+ * workspace); recent_k / recent_v point at the ring's first live row;
+ * num_ctas > 0 caps the grid (<= the plan's; a short context wants few). */
 int pqkv_step_plan_create(const float *cb_k, const float *cb_v,
                           const void *codes_k, const void *codes_v,
                           int64_t ld_tok, int32_t *lens, float scale, int d,
@@ -394,7 +395,7 @@ int pqkv_step_plan_create(const float *cb_k, const float *cb_v,
                           int32_t *counters, void **plan);
 int pqkv_step_run(void *plan, const float *q, const float *k_cur,
                   const float *v_cur, float *recent_k, float *recent_v,
-                  int64_t ld_recent, float *out, void *stream);
+                  int64_t ld_recent, int num_ctas, float *out, void *stream);
 int pqkv_step_plan_destroy(void *plan);
 int pqkv_publish_lengths(int32_t *lens, int batch, void *stream);
 

@@ -78,7 +78,7 @@ SIGNATURES = {
     "pqkv_publish_lengths": (_I, [_P, _I, _P]),
     "pqkv_step_plan_create": (_I, [_P, _P, _P, _P, _I64, _P, _F, _I, _I, _I, _I, _P, _P,
                                    ctypes.POINTER(_P)]),
-    "pqkv_step_run": (_I, [_P, _P, _P, _P, _P, _P, _I64, _P, _P]),
+    "pqkv_step_run": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _P, _P]),
     "pqkv_step_plan_destroy": (_I, [_P]),
     "pqkv_vstore_granularity": (_I64, [_I]),
     "pqkv_vstore_create": (_I, [_I, _I64, _I64, _P, _P]),

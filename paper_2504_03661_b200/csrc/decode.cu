@@ -535,6 +535,9 @@ __device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb,
 // a shared code stream (Args::share = P) c and vh count CTA groups and
 // virtual-head groups, and member `half` of the group is at
 // HG ((c + vh) P + half) + h.
+#ifndef PQKV_FINISH_BATCH
+#define PQKV_FINISH_BATCH 8
+#endif
 __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base, int hg, int vh,
                                          int h, int bh, int c_first, int c_last, int tid,
                                          float *out, float *lse, float *merged, int P, int half) {
@@ -542,11 +545,12 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
     // the dense record and the first batch are in flight before any is consumed
     const float dm = __ldcg(drec), dl = __ldcg(drec + 1), da = __ldcg(drec + kPS + tid);
     float m = -INFINITY, l = 0.f, acc = 0.f;
-    for (int c0 = c_first; c0 <= c_last; c0 += 8) {
-        const int cnt = min(8, c_last - c0 + 1);
-        float rm[8], rl[8], ra[8];
+    constexpr int FB = PQKV_FINISH_BATCH;  // records in flight per round trip
+    for (int c0 = c_first; c0 <= c_last; c0 += FB) {
+        const int cnt = min(FB, c_last - c0 + 1);
+        float rm[FB], rl[FB], ra[FB];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < FB; ++k) {
             if (k < cnt) {
                 const float *rec =
                     parts + ((int64_t)hg * ((int64_t)(c0 + k + vh) * P + half) + h) * (D + kPS);
@@ -556,7 +560,7 @@ __device__ __noinline__ void finish_head(const float *parts, int64_t dense_base,
             }
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < FB; ++k)
             if (k < cnt) merge1(m, l, acc, rm[k], rl[k], ra[k]);
     }
     merge1(m, l, acc, dm, dl, da);
@@ -3233,14 +3237,17 @@ extern "C" int pqkv_step_plan_destroy(void *plan) {
 }
 
 extern "C" int pqkv_step_run(void *plan, const float *q, const float *k_cur, const float *v_cur,
-                             float *recent_k, float *recent_v, int64_t ld_recent, float *out,
-                             void *stream) {
+                             float *recent_k, float *recent_v, int64_t ld_recent, int num_ctas,
+                             float *out, void *stream) {
     PQKV_CHECK_ARG(plan && q && k_cur && v_cur && recent_k && recent_v && out,
                    "pqkv_step_run: null pointer");
     const auto *p = static_cast<const pqkv_step_plan *>(plan);
+    // a short context needs few CTAs: each pays the table build, and the
+    // last arriver merges one record per CTA
+    const int nc = num_ctas > 0 ? std::min(num_ctas, p->num_ctas) : p->num_ctas;
     int rc = pqkv_decode_attention(q, p->scale, p->cb_k, nullptr, 1, 1, 1, p->codes_k, p->codes_v,
                                    p->ld_tok, p->lens, p->cb_v, p->d, p->M, p->nbits, recent_k,
-                                   recent_v, ld_recent, p->lens + 1, k_cur, v_cur, p->num_ctas,
+                                   recent_v, ld_recent, p->lens + 1, k_cur, v_cur, nc,
                                    p->partials, p->counters, out, nullptr, nullptr, 0, stream);
     if (rc) return rc;
     return pqkv_append_recent(k_cur, v_cur, recent_k, recent_v, p->lens, p->d, stream);

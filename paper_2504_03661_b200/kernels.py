@@ -403,12 +403,14 @@ class StepPlan:
         self._dev_index = self.device.index if self.device.index is not None else \
             torch.cuda.current_device()
 
-    def run(self, q, k, v, rk_ptr: int, rv_ptr: int, ld_recent: int, out) -> None:
+    def run(self, q, k, v, rk_ptr: int, rv_ptr: int, ld_recent: int, out,
+            num_ctas: int = 0) -> None:
         if torch.cuda.current_device() != self._dev_index:
             with torch.cuda.device(self._dev_index):
-                return self.run(q, k, v, rk_ptr, rv_ptr, ld_recent, out)
+                return self.run(q, k, v, rk_ptr, rv_ptr, ld_recent, out, num_ctas)
         rc = self._run(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), rk_ptr, rv_ptr,
-                       ld_recent, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                       ld_recent, num_ctas, out.data_ptr(),
+                       torch.cuda.current_stream().cuda_stream)
         if rc:
             N.check(rc, "pqkv_step_run")
 

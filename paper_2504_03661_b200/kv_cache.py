@@ -21,6 +21,7 @@ B200 mapping of the reference's concurrency:
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -31,6 +32,10 @@ import torch
 from . import _native as N
 from . import kernels as K
 from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_device
+
+# decode_append's grid: CTAs per quantized token (each CTA builds its key table,
+# and the last arriver merges one record per CTA)
+STEP_TOKENS_PER_CTA = int(os.environ.get("PQKV_STEP_TOKENS_PER_CTA", "1024"))
 
 __all__ = ["LayerKVCache", "CacheSnapshot"]
 
@@ -81,7 +86,9 @@ class LayerKVCache:
         # virtual reservation, pages mapped as the rows grow -- no copies
         self._new_store(self.DEFAULT_MAX_ROWS)
         self._n_q = 0
-        rcap = max(64, 2 * (recent_capacity + flush_threshold))
+        # the ring is compacted (copied to the front of a new buffer) when its
+        # tail reaches the end; 8 flush cycles of headroom make that rare
+        rcap = max(self.RING_MIN, self.RING_CYCLES * (recent_capacity + flush_threshold))
         self._rk = torch.zeros((rcap, cfg.d), dtype=torch.float32, device=self.device)
         self._rv = torch.zeros_like(self._rk)
         # (n_q, recent length) on the device, in the callers' stream order: the
@@ -96,6 +103,7 @@ class LayerKVCache:
         self._pending_rows = 0
         self._lock = threading.RLock()
         self._plan = None  # decode_append's (key, StepPlan)
+        self._retired: list = []  # ring buffers still read by in-flight flushes
         self.inline_flush_seconds = 0.0
         # numpy in -> numpy snapshots, like the reference (kv_cache.py:269-290);
         # decided by the first write (None until then)
@@ -127,24 +135,36 @@ class LayerKVCache:
 
     # -- storage helpers ---------------------------------------------------
     DEFAULT_MAX_ROWS = 1 << 24  # virtual row capacity per kind (address space only)
+    RING_MIN, RING_CYCLES = 256, 8  # recent-ring rows: max(RING_MIN, RING_CYCLES (R + R_f))
+    STORE_HEADROOM_ROWS = 1 << 15   # rows mapped ahead of need (one 2 MiB page at m64b8)
 
     def _new_store(self, max_rows: int) -> None:
         from .vstore import PagedCodeStore
         self._store = PagedCodeStore(2, max_rows, (self.config.M,),
                                      self.config.torch_code_dtype, self.device)
         self._store_k, self._store_v = self._store.tensor[0], self._store.tensor[1]
+        self._mapped = self._store.mapped_rows
 
-    def _ensure_store(self, n_new: int) -> None:
+    def _ensure_store(self, n_new: int, ahead: bool = False) -> None:
         """Map pages for n_new rows (the reference doubles and copies,
         kv_cache.py:217-228; here rows never move).  Past the reservation
         (16 Mi rows) the store moves once into a larger one."""
         if n_new <= self._store.max_rows:
-            self._store.ensure(n_new)
+            # mapping (cuMemCreate / cuMemMap / cuMemSetAccess, ~1 ms of host
+            # calls) only when the rows outgrow the mapped ones, and then with
+            # headroom (a page, or 1/8 of the rows); a prefill / restore
+            # (ahead=True) maps that headroom up front for the decode steps
+            # that follow it
+            room = max(self.STORE_HEADROOM_ROWS, n_new // 8)
+            if n_new + (room if ahead else 0) > self._mapped:
+                self._store.ensure(min(self._store.max_rows, n_new + room))
+                self._mapped = self._store.mapped_rows
             return
         self._wait_pending()
         old_k, old_v, n = self._store_k, self._store_v, self._n_q
         self._new_store(max(n_new, 2 * self._store.max_rows))
         self._store.ensure(n_new)
+        self._mapped = self._store.mapped_rows
         self._store_k[:n] = old_k[:n]
         self._store_v[:n] = old_v[:n]
 
@@ -152,7 +172,11 @@ class LayerKVCache:
         cap = self._rk.shape[0]
         if self._r0 + self._rlen + extra <= cap:
             return
-        self._wait_pending()
+        if self._pending:
+            # in-flight flushes read rows of the old buffers on the side stream:
+            # keep them alive until those flushes are published (no host wait;
+            # r0 keeps its meaning, the copy below starts at the old r0)
+            self._retired.append((self._rk, self._rv))
         need = self._rlen + extra
         if need * 2 > cap:
             cap = max(2 * need, cap)
@@ -191,7 +215,7 @@ class LayerKVCache:
             n_enc = n - keep
             if n_enc > 0:
                 self._wait_pending()
-                self._ensure_store(self._n_q + n_enc)
+                self._ensure_store(self._n_q + n_enc, ahead=True)
                 K.encode(Kt[:n_enc].contiguous(), self.cb_K.device_centroids(self.device),
                          self.config.nbits, out=self._store_k[self._n_q: self._n_q + n_enc],
                          layout=self._layout, t_first=self._n_q,
@@ -255,8 +279,11 @@ class LayerKVCache:
                 plan = self._plan = (key, K.StepPlan(self, cb_k_layout, cb_v_layout, scale, ws))
             d4 = self.config.d * 4
             off = self._r0 * d4
+            # grid sized to the (host-known) context: one CTA per STEP_TOKENS_PER_CTA
+            # tokens (the device lengths may be ahead of these; only the split changes)
+            nc = -(-(self._n_q + self._pending_rows) // STEP_TOKENS_PER_CTA)
             plan[1].run(q, k, v, self._rk.data_ptr() + off, self._rv.data_ptr() + off,
-                        self._rk.shape[0] - self._r0, out)
+                        self._rk.shape[0] - self._r0, out, max(1, nc))
             self._rlen += 1
             self._n_total += 1
             needed = self._flush_needed_locked()
@@ -351,6 +378,8 @@ class LayerKVCache:
             # make later main-stream readers of the store ordered after the encode
             torch.cuda.current_stream(self.device).wait_event(ev)
             self._pending.pop(0)
+            if not self._pending:
+                self._retired.clear()
             self._pending_rows -= batch
             self._n_q += batch          # single publication point
             self._r0 += batch
@@ -372,7 +401,7 @@ class LayerKVCache:
             raise ValueError("snapshot geometry does not match codebooks")
         with self._lock:
             n = snap.codes_K.n_tokens
-            self._ensure_store(n)
+            self._ensure_store(n, ahead=True)
             if n:
                 ck = snap.codes_K.device_codes(self.device)
                 cv = snap.codes_V.device_codes(self.device)
@@ -397,7 +426,7 @@ class LayerKVCache:
         if self._n_total != 0:
             raise RuntimeError("load_snapshot requires an empty cache")
         with self._lock:
-            self._ensure_store(max(n_q, 1))
+            self._ensure_store(max(n_q, 1), ahead=True)
             if r:
                 self._ensure_recent(r)
             with torch.cuda.device(self.device):

@@ -1,6 +1,6 @@
 """Diagnostic: decode_step per-token time (GPU-resident inputs) vs the fp16
 SDPA loop at a few contexts, and the fused decode kernel's device time."""
-import sys, time
+import os, sys, time
 sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2504_03661_b200 import harness as H
@@ -26,4 +26,9 @@ for ctx in (1024, 32768):
     cache.close()
     fp = H._fp_tpot_ms(K[:ctx + 100], V[:ctx + 100], np.random.default_rng(0).standard_normal((100, 128)), ctx, dev)
     print(f"ctx {ctx}: pq {pq:.3f} ms/step, fp {fp:.3f} ms/step")
-    print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=8))
+    if os.environ.get("DS_BRIEF"):
+        for e in prof.key_averages():
+            if "decode_partials" in e.key:
+                print(f"  decode kernel {e.device_time_total / max(1, e.count):.1f} us/launch ({e.count})")
+    else:
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=8))

@@ -325,10 +325,13 @@ def test_lazy_rescale_dynamic_range(B, Hq, Hkv, cap, n_q, n_r, q_scale):
     spanning hundreds of log2 units, many max jumps) distributions stay
     within the exact tolerance -- its atol scaled by max(1, q_scale): the fp32
     table's absolute score error grows with |q| (the same bits with the lazy
-    margin off, PQKV_LAZY_RESCALE=0); the fp16 modes at q x 3."""
+    margin off, PQKV_LAZY_RESCALE=0); the fp16 modes at q x 2, the largest
+    scale their stated tolerance covers (test_gpu_gqa_tables.py; at q x 3 the
+    packed fp16 key table exceeds it with or without the lazy margin,
+    scripts/lazy_err.py)."""
     got, want = _batched_case(B, Hq, Hkv, cap, n_q, n_r, q_scale=q_scale)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL * max(1.0, q_scale))
-    s16 = min(q_scale, 3.0)
+    s16 = min(q_scale, 2.0)
     for keys in ([False, True] if Hq != Hkv else [False]):
         got, want, want16 = _batched_case(B, Hq, Hkv, cap, n_q, n_r, half_cv=True,
                                           f16_keys=keys, q_scale=s16)
@@ -797,13 +800,16 @@ def test_randomized_batched_configs(seed):
 
 
 @pytest.mark.parametrize("worker", ["sync", "thread"])
-def test_decode_step_plan_device_stream(worker):
+def test_decode_step_plan_device_stream(worker, monkeypatch):
     """decode_step with device tensors goes through the cache's step plan
     (pqkv_step_run: fused decode + append in one call).  Every step equals
     the oracle on the snapshot taken before it, across ring regrowth and
     compaction, background flushes, a scale change and a reloaded cache
     (the plan is rebuilt when a bound pointer or constant moves)."""
     import paper_2504_03661_b200 as P
+    # a ring of 8 rows: compactions (without a host wait) every few steps
+    monkeypatch.setattr(P.LayerKVCache, "RING_MIN", 8)
+    monkeypatch.setattr(P.LayerKVCache, "RING_CYCLES", 1)
     rng = np.random.default_rng(11)
     cfg = P.PQConfig(128, 64, 8)
     ck = rng.standard_normal((64, 256, 2)).astype(np.float32)
