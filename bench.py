@@ -75,11 +75,12 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(cfg_name):
-    """dram read+write bytes per launch of the decode kernel from a committed
-    `ncu --set full` capture summary (profiles/*decode_ncu.json), else None."""
+def ncu_capture(cfg_name):
+    """The committed `ncu --set full` capture record of this config's decode
+    kernel (profiles/*decode_ncu.json: dram bytes per launch, kernel name,
+    shared-load wavefronts per KV token), else {}."""
     pdir = os.path.join(ROOT, "profiles")
-    best = None
+    best = {}
     if os.path.isdir(pdir):
         for f in sorted(os.listdir(pdir)):
             if f.endswith("decode_ncu.json"):
@@ -87,10 +88,27 @@ def ncu_traffic(cfg_name):
                     with open(os.path.join(pdir, f)) as fh:
                         j = json.load(fh)
                     if j.get("config") == cfg_name:
-                        best = j.get("dram_bytes_per_launch")
+                        best = j
                 except Exception:
                     pass
     return best
+
+
+def kernel_label(cfg_name, f16_values=False):
+    """The decode kernel pqkv_decode_attention dispatches for this config's
+    headline mode (decode.cu, pqkv_decode_attention)."""
+    _L, _B, Hq, Hkv, _n, _R = CONFIGS[cfg_name]
+    group = Hq // Hkv
+    if group % 4 == 0 and not f16_values:
+        return "decode_gqa_pair (exact fp32 path, clusters of two CTAs)"
+    if group % 2 == 0 and f16_values:
+        return "decode_partials_m64b8 (two query heads per CTA, fp16 value codebook)"
+    return "decode_partials_m64b8 (fused pqkv_decode_attention)"
+
+
+def ncu_traffic(cfg_name):
+    """dram read+write bytes per launch of the decode kernel (ncu_capture), else None."""
+    return ncu_capture(cfg_name).get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -828,7 +846,10 @@ def run_ours(args):
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "frac_of_nominal_8000_gbs": achieved / 8000.0,
                          "traffic": ncu_traffic(args.config),
-                         "kernel": "decode_partials_m64b8 (fused pqkv_decode_attention)",
+                         "kernel": ncu_capture(args.config).get(
+                             "kernel", kernel_label(args.config, args.f16_value_codebook)),
+                         "shared_load_wavefronts_per_kv_token": ncu_capture(args.config).get(
+                             "shared_load_wavefronts_per_kv_token"),
                          "kernel_ms_per_launch": k_ms,
                          "kernel_ms_isolated_launch": iso_ms,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
