@@ -233,3 +233,30 @@ def test_integration_ctypes_binding_snippet():
     want = lut[np.arange(16)[None, :], codes].sum(axis=1)
     np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
     assert torch.cuda.is_available()
+
+
+def test_product_path_has_no_cpu_fallback():
+    """No GPU (this container) -> the reference-API calls raise instead of
+    computing on the host; a missing library raises naming the build step
+    (a subprocess: the library handle is process-global)."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    import paper_2504_03661_b200 as P
+    rng = np.random.default_rng(0)
+    cfg = P.PQConfig(128, 64, 8)
+    cb = P.Codebook(cfg, rng.standard_normal((64, 256, 2)).astype(np.float32), "key")
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        P.assign_codes(rng.standard_normal((4, 128)), cb)
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        P.build_key_lut(rng.standard_normal(128), cb)
+    code = ("import os, numpy as np\n"
+            "os.environ['PQKV_SM100_LIB'] = '/nonexistent/libpqkv_sm100.so'\n"
+            "from paper_2504_03661_b200 import _native as N\n"
+            "try:\n    N.load(require_cuda=False)\nexcept RuntimeError as e:\n"
+            "    print('raised:', e)\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                       timeout=120)
+    assert "raised:" in r.stdout and "no CPU fallback" in r.stdout, r.stdout + r.stderr
