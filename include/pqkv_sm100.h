@@ -242,6 +242,13 @@ int pqkv_decode_finish(const float *partials, int num_ctas, int B, int Hq,
 #define PQKV_DECODE_KEY_TABLE_PAIRS 64 /* with PQKV_DECODE_F16_KEY_TABLE: two
                              query heads per CTA even when the group is a
                              multiple of 4 */
+#define PQKV_DECODE_APPEND_RECENT 128 /* one head (B = Hq = Hkv = 1, m64b8, fp32
+                                      * values): after the merge the finishing CTA
+                                      * appends (k_cur, v_cur) at row n_recent[0] of
+                                      * recent_k / recent_v (ld_recent rows) and bumps
+                                      * n_recent[0] -- pqkv_append_recent fused into
+                                      * the launch (recent_k, recent_v, n_recent are
+                                      * written) */
 #define PQKV_DECODE_EARLY_CODES 8 /* the codes below n_q were written before
                              the previous kernel on the stream started (the
                              codes of a decode step are appended by an

@@ -21,6 +21,7 @@ DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 PARTIAL_HEADER = 4
 DECODE_PDL, DECODE_STATIC_CODEBOOKS, DECODE_F16_VALUE_CODEBOOK, DECODE_EARLY_CODES = 1, 2, 4, 8
 DECODE_ONE_HEAD_PER_CTA, DECODE_F16_KEY_TABLE, DECODE_KEY_TABLE_PAIRS = 16, 32, 64
+DECODE_APPEND_RECENT = 128  # one head: the finishing CTA appends (k_cur, v_cur) to the ring
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int

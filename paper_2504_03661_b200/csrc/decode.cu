@@ -162,6 +162,7 @@ struct Args {
                       // P virtual heads of one KV head (P j .. P j + P - 1), concurrently,
                       // so each code line is fetched from DRAM once and hit in L2 P - 1 times
     int trace_id;  // PQKV_TRACE builds: launch sequence number
+    int append;    // PQKV_DECODE_APPEND_RECENT (one head): the finisher appends (k_cur, v_cur)
 };
 
 #if PQKV_LANE8
@@ -535,6 +536,22 @@ __device__ __forceinline__ void merge1(float &m, float &l, float &acc, float mb,
 // a shared code stream (Args::share = P) c and vh count CTA groups and
 // virtual-head groups, and member `half` of the group is at
 // HG ((c + vh) P + half) + h.
+// PQKV_DECODE_APPEND_RECENT: after the merge, the finishing CTA's D threads
+// write (k_cur, v_cur) at row n_recent of the ring and bump n_recent (every
+// CTA of the head has arrived, so every read of the old length is done)
+__device__ __noinline__ void ring_append(const float *k_cur, const float *v_cur, float *rk,
+                                         float *rv, int32_t *n_recent, int64_t ld_recent,
+                                         int gt, int bar) {
+    const int r = __ldcg(n_recent);
+    const bool fits = r < ld_recent;
+    if (fits) {
+        rk[(int64_t)r * D + gt] = __ldg(k_cur + gt);
+        rv[(int64_t)r * D + gt] = __ldg(v_cur + gt);
+    }
+    named_bar_sync(bar, D);  // all D threads have read the old length
+    if (gt == 0 && fits) n_recent[0] = r + 1;
+}
+
 #ifndef PQKV_FINISH_BATCH
 #define PQKV_FINISH_BATCH 8
 #endif
@@ -1155,6 +1172,10 @@ __global__ void __launch_bounds__(W * 32, 1) decode_partials_m64b8(const Args A)
                     finish_head(A.parts, (int64_t)HG * A.num_ctas + (int64_t)A.B * A.Hq, HG,
                                 s2.bh, h, bq0 + h, c_first, c_last, gt, A.out, A.lse, A.merged,
                                 P, half);
+                if (A.append)
+                    ring_append(A.k_cur, A.v_cur, const_cast<float *>(A.recent_k),
+                                const_cast<float *>(A.recent_v), const_cast<int32_t *>(A.n_recent),
+                                A.ld_recent, gt, 1 + grp);
 #ifdef PQKV_TRACE
                 if (k == 0) PQKV_TR(15, clock64() - clk_segs);  // cycles to the merge's end
 #endif
@@ -3123,8 +3144,14 @@ extern "C" int pqkv_decode_attention(
     PQKV_CHECK_ARG((flags & ~(PQKV_DECODE_PDL | PQKV_DECODE_STATIC_CODEBOOKS |
                               PQKV_DECODE_F16_VALUE_CODEBOOK | PQKV_DECODE_EARLY_CODES |
                               PQKV_DECODE_ONE_HEAD_PER_CTA | PQKV_DECODE_F16_KEY_TABLE |
-                              PQKV_DECODE_KEY_TABLE_PAIRS)) == 0,
+                              PQKV_DECODE_KEY_TABLE_PAIRS | PQKV_DECODE_APPEND_RECENT)) == 0,
                    "pqkv_decode_attention: unknown flags");
+    PQKV_CHECK_ARG(!(flags & PQKV_DECODE_APPEND_RECENT) ||
+                       (B == 1 && Hq == 1 && Hkv == 1 && is_fast_geometry(d, M, nbits) &&
+                        recent_k && n_recent && k_cur &&
+                        !(flags & PQKV_DECODE_F16_VALUE_CODEBOOK)),
+                   "pqkv_decode_attention: PQKV_DECODE_APPEND_RECENT needs one head (m64b8, "
+                   "fp32 values) with a recent ring, its length and the current token");
     if (B == 0) return PQKV_OK;
     PQKV_CHECK_ARG(q && cb_k && codes_k && codes_v && n_q && cb_v && partials,
                    "pqkv_decode_attention: null pointer");
@@ -3153,6 +3180,7 @@ extern "C" int pqkv_decode_attention(
     a.merged = merged;
     a.early_cv = (flags & PQKV_DECODE_STATIC_CODEBOOKS) ? 1 : 0;
     a.early_codes = (flags & PQKV_DECODE_EARLY_CODES) ? 1 : 0;
+    a.append = (flags & PQKV_DECODE_APPEND_RECENT) ? 1 : 0;
     const bool pdl = (flags & PQKV_DECODE_PDL) != 0;
     // GQA: the CTAs serving the virtual heads of one KV head stream its codes
     // concurrently (one DRAM fetch, L2 hits for the others) -- P = virtual
@@ -3206,6 +3234,9 @@ extern "C" int pqkv_merge_partials(const float *parts, int n_parts, int64_t n_he
 }
 
 // ---- decode_step's per-token path for one cached head -----------------------
+#ifndef PQKV_STEP_FUSED_APPEND
+#define PQKV_STEP_FUSED_APPEND 1  // the append rides in the decode launch's finisher
+#endif
 struct pqkv_step_plan {
     const float *cb_k, *cb_v;
     const void *codes_k, *codes_v;
@@ -3248,7 +3279,8 @@ extern "C" int pqkv_step_run(void *plan, const float *q, const float *k_cur, con
     int rc = pqkv_decode_attention(q, p->scale, p->cb_k, nullptr, 1, 1, 1, p->codes_k, p->codes_v,
                                    p->ld_tok, p->lens, p->cb_v, p->d, p->M, p->nbits, recent_k,
                                    recent_v, ld_recent, p->lens + 1, k_cur, v_cur, nc,
-                                   p->partials, p->counters, out, nullptr, nullptr, 0, stream);
-    if (rc) return rc;
+                                   p->partials, p->counters, out, nullptr, nullptr,
+                                   PQKV_STEP_FUSED_APPEND ? PQKV_DECODE_APPEND_RECENT : 0, stream);
+    if (rc || PQKV_STEP_FUSED_APPEND) return rc;
     return pqkv_append_recent(k_cur, v_cur, recent_k, recent_v, p->lens, p->d, stream);
 }
