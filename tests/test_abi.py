@@ -60,6 +60,13 @@ def test_bad_arguments_fail_before_cuda(lib):
     assert lib.pqkv_encode(None, 0, 0, 128, 128, None, 64, 8, None, 64, -1, None) == 0
     # the decode layout exists only for m64b8
     assert lib.pqkv_encode(None, 0, 5, 64, 64, None, 32, 8, None, 32, 0, None) == N.PQKV_EINVAL
+    # the fused ring append is a one-head flag; the step plan checks its pointers
+    rc = lib.pqkv_decode_attention(None, 0.1, None, None, 2, 2, 2, None, None, 0, None, None,
+                                   128, 64, 8, None, None, 0, None, None, None, 4, None, None,
+                                   None, None, None, N.DECODE_APPEND_RECENT, None)
+    assert rc == N.PQKV_EINVAL and b"APPEND_RECENT" in lib.pqkv_last_error()
+    assert lib.pqkv_step_run(None, None, None, None, None, None, 0, 0, None,
+                             None) == N.PQKV_EINVAL
 
 
 def test_partials_size(lib):
