@@ -36,6 +36,10 @@ from .pq_core import Codebook, CodesMatrix, _is_tensor, default_device, to_devic
 # decode_append's grid: CTAs per quantized token (each CTA builds its key table,
 # and the last arriver merges one record per CTA)
 STEP_TOKENS_PER_CTA = int(os.environ.get("PQKV_STEP_TOKENS_PER_CTA", "1024"))
+# ... but at least this many (capped by the plan's grid): a short context is
+# latency bound, and 32 CTAs of a few units each beat one CTA walking them all
+# (1K tokens: 13.7 us per launch vs 16.5; scripts/ds_time.py)
+STEP_MIN_CTAS = int(os.environ.get("PQKV_STEP_MIN_CTAS", "32"))
 
 __all__ = ["LayerKVCache", "CacheSnapshot"]
 
@@ -280,8 +284,9 @@ class LayerKVCache:
             d4 = self.config.d * 4
             off = self._r0 * d4
             # grid sized to the (host-known) context: one CTA per STEP_TOKENS_PER_CTA
-            # tokens (the device lengths may be ahead of these; only the split changes)
-            nc = -(-(self._n_q + self._pending_rows) // STEP_TOKENS_PER_CTA)
+            # tokens, at least STEP_MIN_CTAS (the device lengths may be ahead of
+            # these; only the split changes)
+            nc = max(STEP_MIN_CTAS, -(-(self._n_q + self._pending_rows) // STEP_TOKENS_PER_CTA))
             plan[1].run(q, k, v, self._rk.data_ptr() + off, self._rv.data_ptr() + off,
                         self._rk.shape[0] - self._r0, out, max(1, nc))
             self._rlen += 1

@@ -6,21 +6,22 @@ import numpy as np, torch
 from paper_2504_03661_b200 import harness as H
 from paper_2504_03661_b200.attention import Counters, decode_step
 from paper_2504_03661_b200.kv_cache import LayerKVCache
-cfg = H.BenchConfig(context_lengths=[1024, 32768], gen_tokens=100)
+NS = int(os.environ.get("STEPS", "100"))
+cfg = H.BenchConfig(context_lengths=[1024, 32768], gen_tokens=NS)
 cb_K, cb_V = H._codebooks(cfg, None)
 dev = torch.device("cuda")
 for ctx in (1024, 32768):
-    K, V = H.synth_kv(H.SynthSpec(n_tokens=ctx + 100, d=128, seed=ctx))
+    K, V = H.synth_kv(H.SynthSpec(n_tokens=ctx + NS, d=128, seed=ctx))
     seed = LayerKVCache(cb_K, cb_V, worker="sync"); seed.prefill_ingest(K[:ctx], V[:ctx])
     snap = seed.snapshot()
-    q = torch.randn(100, 128, device=dev)
+    q = torch.randn(NS, 128, device=dev)
     kd = torch.from_numpy(np.ascontiguousarray(K[ctx:], np.float32)).to(dev)
     vd = torch.from_numpy(np.ascontiguousarray(V[ctx:], np.float32)).to(dev)
     for rep in range(3):
         cache = LayerKVCache(cb_K, cb_V, worker="thread"); cache.load_snapshot(snap)
         c = Counters(); torch.cuda.synchronize()
         ts = [time.perf_counter()]
-        for i in range(100):
+        for i in range(NS):
             decode_step(q[i], kd[i], vd[i], cache, cb_K, cb_V, counters=c)
             ts.append(time.perf_counter())
         torch.cuda.synchronize(); tend = time.perf_counter()
