@@ -14,9 +14,12 @@ decode_step :214-287).  The arithmetic runs in libpqkv_sm100.so:
                         in registers from the shared-memory codebook), split
                         over every SM and merged in a fixed order;
 * dense_partial      -> pqkv_decode_finish (recent rows, no quantized span)
-* decode_step        -> fused partials (LUT built in shared memory) +
-                        dense/current-token merge + finalize in two launches,
-                        then the cache append.
+* decode_step        -> one launch per token for a LayerKVCache with device
+                        tensors (pqkv_step_run: LUT in shared memory, fused
+                        partials, dense/current-token merge, finalize, and the
+                        append of (k_n, v_n) to the recent ring by the
+                        finishing CTA); other caches / host inputs take the
+                        fused decode launch followed by the cache append.
 
 The reference accumulates in float64 on the CPU; this path accumulates in
 float32 on the GPU.  Outputs agree within the tolerance stated in DESIGN.md
